@@ -1,0 +1,898 @@
+/*
+ * esoracle.c -- CPU ORACLE for the equistream-b200 hot path.  TEST
+ * INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py, and never by the product
+ * (paper_2601_16622_b200/), which fails loudly without its CUDA library.
+ *
+ * Plain C (C11, double precision, OpenMP over target atoms) restatement of
+ * the reference's algorithm for the fused equivariant attention path.  Every
+ * function cites the reference file:line (relative to /root/reference) it
+ * follows.  The reference headers themselves need Eigen (absent here); the
+ * so3 pieces of this file are pinned against those very headers compiled
+ * through a small Eigen shim (oracle/build_ref.sh -> oracle/_ref/libesref.so,
+ * see tests/test_oracle_vs_ref.py), the rest against the SPEC known-answer
+ * examples and the dense tensor-product oracle.
+ *
+ * Build: oracle/Makefile  (-O2 -ffp-contract=off -fopenmp; no FMA contraction
+ * so that neighbour distances are bit-identical to the GPU builder's
+ * __dmul_rn/__dadd_rn sequence).
+ *
+ * Feature layout ("irreps layout"): a node feature is [M][C] with
+ * M = (L+1)^2, row index ll = l*l + (m + l), channels innermost.  This is the
+ * byte order of the reference IrrepsFeature blocks (Eigen column-major
+ * C_l x (2l+1), irreps.hpp:69-71) stacked over l.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ESO_MAXL 8
+#define ESO_PI 3.14159265358979323846
+
+/* ------------------------------------------------------------------ */
+/* factorials.hpp:11-46                                                */
+/* ------------------------------------------------------------------ */
+static long double g_fact[65];
+static int g_fact_init = 0;
+static void fact_init(void) {
+  if (g_fact_init) return;
+  g_fact[0] = 1.0L;
+  for (int n = 1; n <= 64; ++n) g_fact[n] = g_fact[n - 1] * (long double)n;
+  g_fact_init = 1;
+}
+static long double factl(int n) { return g_fact[n]; }
+double eso_factorial(int n) {
+  fact_init();
+  if (n < 0 || n > 64) return -1.0;
+  return (double)g_fact[n];
+}
+static double dfact_odd(int n) { /* (2n-1)!!, factorials.hpp:35-39 */
+  double r = 1.0;
+  for (int k = 2 * n - 1; k > 1; k -= 2) r *= k;
+  return r;
+}
+static int psign(int n) { return (n % 2 == 0) ? 1 : -1; }
+
+/* ------------------------------------------------------------------ */
+/* harmonics.hpp:36-81 -- real orthonormal solid harmonics, m=-l..l,   */
+/* (-1)^m on the positive-m tesseral components (harmonics.hpp:76).    */
+/* ------------------------------------------------------------------ */
+void eso_solid_harmonics(int l, const double* r, double* out) {
+  fact_init();
+  const double x = r[0], y = r[1], z = r[2];
+  const double r2 = x * x + y * y + z * z;
+  if (l == 0) { out[0] = 0.28209479177387814; return; }
+  double a = 1.0, b = 0.0; /* Re/Im (x+iy)^mu */
+  for (int mu = 0; mu <= l; ++mu) {
+    if (mu > 0) {
+      const double an = a * x - b * y, bn = a * y + b * x;
+      a = an; b = bn;
+    }
+    double p2 = 0.0, pc = dfact_odd(mu);
+    for (int ll = mu + 1; ll <= l; ++ll) {
+      const double pn = ((2 * ll - 1) * z * pc - (ll + mu - 1) * r2 * p2) / (double)(ll - mu);
+      p2 = pc; pc = pn;
+    }
+    const double norm = sqrt((2 * l + 1) / (4.0 * ESO_PI) * (double)(factl(l - mu) / factl(l + mu)));
+    if (mu == 0) out[l] = norm * pc;
+    else {
+      const double s = sqrt(2.0) * norm * pc;
+      out[l + mu] = psign(mu) * s * a;
+      out[l - mu] = s * b;
+    }
+  }
+}
+
+/* harmonics.hpp:93-97 */
+double eso_on_axis_solid_harmonic(int l, double rn) {
+  return pow(rn, l) * sqrt((2 * l + 1) / (4.0 * ESO_PI));
+}
+
+/* ------------------------------------------------------------------ */
+/* clebsch.hpp:26-52 -- complex (Condon-Shortley) CG, Racah sum         */
+/* ------------------------------------------------------------------ */
+static int tri_ok(int a, int b, int c) { return c >= abs(a - b) && c <= a + b; }
+
+double eso_complex_cg(int j1, int m1, int j2, int m2, int J, int M) {
+  fact_init();
+  if (abs(m1) > j1 || abs(m2) > j2 || abs(M) > J) return 0.0;
+  if (M != m1 + m2) return 0.0;
+  if (!tri_ok(j1, j2, J)) return 0.0;
+  const long double delta = factl(j1 + j2 - J) * factl(j1 - j2 + J) * factl(-j1 + j2 + J) / factl(j1 + j2 + J + 1);
+  const long double pre = sqrtl((long double)(2 * J + 1) * delta * factl(J + M) * factl(J - M) * factl(j1 + m1) *
+                                factl(j1 - m1) * factl(j2 + m2) * factl(j2 - m2));
+  int kmin = 0, kmax = j1 + j2 - J;
+  if (j2 - J - m1 > kmin) kmin = j2 - J - m1;
+  if (j1 - J + m2 > kmin) kmin = j1 - J + m2;
+  if (j1 - m1 < kmax) kmax = j1 - m1;
+  if (j2 + m2 < kmax) kmax = j2 + m2;
+  long double sum = 0.0L;
+  for (int k = kmin; k <= kmax; ++k) {
+    const long double t = factl(k) * factl(j1 + j2 - J - k) * factl(j1 - m1 - k) * factl(j2 + m2 - k) *
+                          factl(J - j2 + m1 + k) * factl(J - j1 - m2 + k);
+    sum += psign(k) / t;
+  }
+  return (double)(pre * sum);
+}
+
+/* clebsch.hpp:56-85 -- Wigner 6j (Racah).  Used only by the factorized
+ * path; exposed for the known-answer test. */
+double eso_wigner_6j(int j1, int j2, int j3, int j4, int j5, int j6) {
+  fact_init();
+#define TOK(a, b, c) ((a) >= 0 && (b) >= 0 && (c) >= 0 && tri_ok(a, b, c))
+  if (!TOK(j1, j2, j3) || !TOK(j1, j5, j6) || !TOK(j4, j2, j6) || !TOK(j4, j5, j3)) return 0.0;
+#undef TOK
+#define TRI(a, b, c) (factl((a) + (b) - (c)) * factl((a) - (b) + (c)) * factl(-(a) + (b) + (c)) / factl((a) + (b) + (c) + 1))
+  const long double pre = sqrtl(TRI(j1, j2, j3) * TRI(j1, j5, j6) * TRI(j4, j2, j6) * TRI(j4, j5, j3));
+#undef TRI
+  int tmin = j1 + j2 + j3;
+  if (j1 + j5 + j6 > tmin) tmin = j1 + j5 + j6;
+  if (j4 + j2 + j6 > tmin) tmin = j4 + j2 + j6;
+  if (j4 + j5 + j3 > tmin) tmin = j4 + j5 + j3;
+  int tmax = j1 + j2 + j4 + j5;
+  if (j2 + j3 + j5 + j6 < tmax) tmax = j2 + j3 + j5 + j6;
+  if (j3 + j1 + j6 + j4 < tmax) tmax = j3 + j1 + j6 + j4;
+  long double sum = 0.0L;
+  for (int t = tmin; t <= tmax; ++t) {
+    const long double den = factl(t - j1 - j2 - j3) * factl(t - j1 - j5 - j6) * factl(t - j4 - j2 - j6) *
+                            factl(t - j4 - j5 - j3) * factl(j1 + j2 + j4 + j5 - t) * factl(j2 + j3 + j5 + j6 - t) *
+                            factl(j3 + j1 + j6 + j4 - t);
+    sum += psign(t) * factl(t + 1) / den;
+  }
+  return (double)(pre * sum);
+}
+
+/* ------------------------------------------------------------------ */
+/* clebsch.hpp:89-103 -- complex->real basis change u(m, mu)           */
+/* returned as re/im parts; clebsch.hpp:120-173 real table             */
+/* ------------------------------------------------------------------ */
+static void ubasis(int l, int m, int mu, double* re, double* im) {
+  const double s = 1.0 / sqrt(2.0);
+  *re = 0.0; *im = 0.0;
+  if (m == 0) { if (mu == 0) *re = 1.0; return; }
+  if (m > 0) {
+    if (mu == m) *re = s;
+    else if (mu == -m) *re = psign(m) * s;
+  } else {
+    const int a = -m; /* row l-a */
+    if (mu == -a) *im = s;                 /* u(l-a, l-a) = i/sqrt2 */
+    else if (mu == a) *im = -psign(a) * s; /* u(l-a, l+a) = -i (-1)^a /sqrt2 */
+  }
+  (void)l;
+}
+
+/* out[(mo+lo)*d1*d2 + (m1+l1)*d2 + (m2+l2)], returns 0 ok, -1 triangle
+ * violation, -2 imaginary residue (clebsch.hpp:164-167). */
+int eso_cg_real(int l1, int l2, int lo, double* out) {
+  if (!tri_ok(l1, l2, lo)) return -1;
+  const int d1 = 2 * l1 + 1, d2 = 2 * l2 + 1;
+  const int odd = ((l1 + l2 + lo) % 2) != 0;
+  for (int mo = -lo; mo <= lo; ++mo)
+    for (int m1 = -l1; m1 <= l1; ++m1)
+      for (int m2 = -l2; m2 <= l2; ++m2) {
+        double are = 0.0, aim = 0.0;
+        const int mu1s[2] = {m1, -m1}, mu2s[2] = {m2, -m2}, mus[2] = {mo, -mo};
+        for (int a = 0; a < (m1 == 0 ? 1 : 2); ++a)
+          for (int b = 0; b < (m2 == 0 ? 1 : 2); ++b)
+            for (int c = 0; c < (mo == 0 ? 1 : 2); ++c) {
+              const int mu1 = mu1s[a], mu2 = mu2s[b], muo = mus[c];
+              if (muo != mu1 + mu2) continue;
+              double uo_r, uo_i, u1_r, u1_i, u2_r, u2_i;
+              ubasis(lo, mo, muo, &uo_r, &uo_i);
+              ubasis(l1, m1, mu1, &u1_r, &u1_i);
+              ubasis(l2, m2, mu2, &u2_r, &u2_i);
+              u1_i = -u1_i; u2_i = -u2_i; /* conj */
+              /* w = uo * u1c * u2c */
+              const double t_r = uo_r * u1_r - uo_i * u1_i, t_i = uo_r * u1_i + uo_i * u1_r;
+              const double w_r = t_r * u2_r - t_i * u2_i, w_i = t_r * u2_i + t_i * u2_r;
+              if (w_r == 0.0 && w_i == 0.0) continue;
+              const double cg = eso_complex_cg(l1, mu1, l2, mu2, lo, muo);
+              are += w_r * cg; aim += w_i * cg;
+            }
+        if (odd) { /* multiply by -i */
+          const double nr = aim, ni = -are;
+          are = nr; aim = ni;
+        }
+        if (fabs(aim) > 1e-12) return -2;
+        out[(mo + lo) * d1 * d2 + (m1 + l1) * d2 + (m2 + l2)] = are;
+      }
+  return 0;
+}
+
+/* Cached tables for l <= ESO_MAXL/2 paths used by attention (l <= 4). */
+#define ESO_LT 5
+static double* g_cg[ESO_LT][ESO_LT][ESO_LT];
+static int g_cg_init = 0;
+static void cg_cache_init(void) {
+  if (g_cg_init) return;
+#pragma omp critical(eso_cg_cache)
+  {
+    if (!g_cg_init) {
+      for (int a = 0; a < ESO_LT; ++a)
+        for (int b = 0; b < ESO_LT; ++b)
+          for (int c = 0; c < ESO_LT; ++c) {
+            g_cg[a][b][c] = NULL;
+            if (!tri_ok(a, b, c)) continue;
+            double* t = (double*)calloc((size_t)(2 * a + 1) * (2 * b + 1) * (2 * c + 1), sizeof(double));
+            eso_cg_real(a, b, c, t);
+            g_cg[a][b][c] = t;
+          }
+      g_cg_init = 1;
+    }
+  }
+}
+static const double* cgt(int a, int b, int c) { return g_cg[a][b][c]; }
+
+/* ------------------------------------------------------------------ */
+/* tensor_product.hpp:18-49 -- literal dense CG product, per channel.  */
+/* Blocks are [2l+1][C] (m-major, channel innermost).                  */
+/* ------------------------------------------------------------------ */
+static void tp_dense_tab(const double* tab, const double* u, int l1, int cu, const double* v, int l2, int cv, int lo,
+                         double* out) {
+  const int C = cu > cv ? cu : cv;
+  const int d1 = 2 * l1 + 1, d2 = 2 * l2 + 1;
+  for (int mo = 0; mo < 2 * lo + 1; ++mo)
+    for (int c = 0; c < C; ++c) {
+      const int c1 = cu == 1 ? 0 : c, c2 = cv == 1 ? 0 : c;
+      double acc = 0.0;
+      for (int m1 = 0; m1 < d1; ++m1)
+        for (int m2 = 0; m2 < d2; ++m2) acc += tab[mo * d1 * d2 + m1 * d2 + m2] * u[m1 * cu + c1] * v[m2 * cv + c2];
+      out[mo * C + c] = acc;
+    }
+}
+
+int eso_tensor_product_dense(const double* u, int l1, int cu, const double* v, int l2, int cv, int lo, double* out) {
+  if (!tri_ok(l1, l2, lo)) return -1;
+  if (cu != cv && cu != 1 && cv != 1) return -3;
+  if (l1 < ESO_LT && l2 < ESO_LT && lo < ESO_LT) {
+    cg_cache_init();
+    tp_dense_tab(cgt(l1, l2, lo), u, l1, cu, v, l2, cv, lo, out);
+    return 0;
+  }
+  const int d1 = 2 * l1 + 1, d2 = 2 * l2 + 1;
+  double* tab = (double*)malloc(sizeof(double) * (size_t)(2 * lo + 1) * d1 * d2);
+  eso_cg_real(l1, l2, lo, tab);
+  tp_dense_tab(tab, u, l1, cu, v, l2, cv, lo, out);
+  free(tab);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Wigner-D.  The reference wigner.hpp:31-56 builds G_y with the wrong  */
+/* sign and is an anti-homomorphism; the oracle instead     */
+/* follows the convention anchor itself (wigner.hpp:19-20,              */
+/* SPEC.md:89,126): D(R) is the least-squares solution of               */
+/*   solid(l, R p_k) = D solid(l, p_k)  over 4(2l+1) spiral points      */
+/* ("least-squares fit of D from harmonic evaluations").     */
+/* D is row-major [(2l+1)][(2l+1)], acting on value vectors.            */
+/* ------------------------------------------------------------------ */
+static int solve_inplace(double* A, double* B, int n, int nrhs) { /* A X = B, X -> B */
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int r = col + 1; r < n; ++r)
+      if (fabs(A[r * n + col]) > fabs(A[piv * n + col])) piv = r;
+    if (fabs(A[piv * n + col]) < 1e-300) return -1;
+    if (piv != col) {
+      for (int k = 0; k < n; ++k) { double t = A[col * n + k]; A[col * n + k] = A[piv * n + k]; A[piv * n + k] = t; }
+      for (int k = 0; k < nrhs; ++k) { double t = B[col * nrhs + k]; B[col * nrhs + k] = B[piv * nrhs + k]; B[piv * nrhs + k] = t; }
+    }
+    const double d = A[col * n + col];
+    for (int r = 0; r < n; ++r) {
+      if (r == col) continue;
+      const double f = A[r * n + col] / d;
+      if (f == 0.0) continue;
+      for (int k = col; k < n; ++k) A[r * n + k] -= f * A[col * n + k];
+      for (int k = 0; k < nrhs; ++k) B[r * nrhs + k] -= f * B[col * nrhs + k];
+    }
+  }
+  for (int r = 0; r < n; ++r)
+    for (int k = 0; k < nrhs; ++k) B[r * nrhs + k] /= A[r * n + r];
+  return 0;
+}
+
+int eso_wigner_d(int l, const double* R, double* D) {
+  const int d = 2 * l + 1;
+  if (l == 0) { D[0] = 1.0; return 0; }
+  const int np = 4 * d;
+  double* Y = (double*)malloc(sizeof(double) * d * np);  /* Y[m][k] = solid(l, p_k) */
+  double* Z = (double*)malloc(sizeof(double) * d * np);  /* Z[m][k] = solid(l, R p_k) */
+  double tmp[2 * ESO_MAXL + 1];
+  const double ga = ESO_PI * (3.0 - sqrt(5.0));
+  for (int k = 0; k < np; ++k) { /* golden spiral points on the unit sphere */
+    const double zz = 1.0 - (2.0 * k + 1.0) / np;
+    const double rr = sqrt(1.0 - zz * zz);
+    const double p[3] = {rr * cos(ga * k), rr * sin(ga * k), zz};
+    const double q[3] = {R[0] * p[0] + R[1] * p[1] + R[2] * p[2], R[3] * p[0] + R[4] * p[1] + R[5] * p[2],
+                         R[6] * p[0] + R[7] * p[1] + R[8] * p[2]};
+    eso_solid_harmonics(l, p, tmp);
+    for (int m = 0; m < d; ++m) Y[m * np + k] = tmp[m];
+    eso_solid_harmonics(l, q, tmp);
+    for (int m = 0; m < d; ++m) Z[m * np + k] = tmp[m];
+  }
+  /* D Y = Z  ->  (Y Y^T) D^T = Y Z^T */
+  double* A = (double*)malloc(sizeof(double) * d * d);
+  double* B = (double*)malloc(sizeof(double) * d * d);
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double s = 0.0, t = 0.0;
+      for (int k = 0; k < np; ++k) { s += Y[a * np + k] * Y[b * np + k]; t += Y[a * np + k] * Z[b * np + k]; }
+      A[a * d + b] = s; B[a * d + b] = t;
+    }
+  int st = solve_inplace(A, B, d, d); /* B = D^T */
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) D[a * d + b] = B[b * d + a];
+  free(Y); free(Z); free(A); free(B);
+  return st;
+}
+
+/* ------------------------------------------------------------------ */
+/* SPEC eaas (gauge SPEC.md:216): R with R r = |r| e_z */
+/* rotating about (r^ x e_z)/|.| by arccos(r^.e_z); identity / pi about */
+/* e_x within 1e-6 of +/- e_z.  Row-major 3x3.                          */
+/* ------------------------------------------------------------------ */
+int eso_alignment_rotation(const double* r, double* R) {
+  const double n = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (n <= 1e-8) return -1; /* degenerate */
+  const double u[3] = {r[0] / n, r[1] / n, r[2] / n};
+  const double s = sqrt(u[0] * u[0] + u[1] * u[1]);
+  for (int i = 0; i < 9; ++i) R[i] = 0.0;
+  if (s < 1e-6 && u[2] > 0) { R[0] = R[4] = R[8] = 1.0; return 0; }
+  if (s < 1e-6 && u[2] < 0) { R[0] = 1.0; R[4] = -1.0; R[8] = -1.0; return 0; }
+  /* axis k = u x e_z = (u_y, -u_x, 0)/s; angle t: cos t = u_z, sin t = s */
+  const double kx = u[1] / s, ky = -u[0] / s, kz = 0.0;
+  const double c = u[2], sn = s, C1 = 1.0 - c;
+  R[0] = c + kx * kx * C1;      R[1] = kx * ky * C1 - kz * sn; R[2] = kx * kz * C1 + ky * sn;
+  R[3] = ky * kx * C1 + kz * sn; R[4] = c + ky * ky * C1;     R[5] = ky * kz * C1 - kx * sn;
+  R[6] = kz * kx * C1 - ky * sn; R[7] = kz * ky * C1 + kx * sn; R[8] = c + kz * kz * C1;
+  return 0;
+}
+
+/* for each m_o the surviving source m_i and coefficient
+ * cg_real(li,lf,lo)[m_o](m_i, 0) (the m_f = 0 slice; conventions.hpp:29-31).
+ * src[m_o+lo] = m_i or -1000 when absent.  Returns the entry count. */
+int eso_reindex_rule(int li, int lf, int lo, int* src, double* coef) {
+  cg_cache_init();
+  if (!tri_ok(li, lf, lo) || li >= ESO_LT || lf >= ESO_LT || lo >= ESO_LT) return -1;
+  const double* t = cgt(li, lf, lo);
+  const int d1 = 2 * li + 1, d2 = 2 * lf + 1;
+  int cnt = 0;
+  for (int mo = -lo; mo <= lo; ++mo) {
+    src[mo + lo] = -1000; coef[mo + lo] = 0.0;
+    for (int mi = -li; mi <= li; ++mi) {
+      const double c = t[(mo + lo) * d1 * d2 + (mi + li) * d2 + lf];
+      if (fabs(c) > 1e-14) {
+        src[mo + lo] = mi; coef[mo + lo] = c; ++cnt;
+      }
+    }
+  }
+  return cnt;
+}
+
+typedef struct { int src[2 * ESO_LT + 1]; double coef[2 * ESO_LT + 1]; } eso_rule;
+static eso_rule g_rule[ESO_LT][ESO_LT][ESO_LT];
+static int g_rule_init = 0;
+static const eso_rule* rule_of(int li, int lf, int lo) {
+  if (!g_rule_init) {
+#pragma omp critical(eso_rule_cache)
+    {
+      if (!g_rule_init) {
+        for (int a = 0; a < ESO_LT; ++a)
+          for (int b = 0; b < ESO_LT; ++b)
+            for (int c = 0; c < ESO_LT; ++c)
+              if (tri_ok(a, b, c)) eso_reindex_rule(a, b, c, g_rule[a][b][c].src, g_rule[a][b][c].coef);
+        g_rule_init = 1;
+      }
+    }
+  }
+  return &g_rule[li][lf][lo];
+}
+
+/* apply_reindex: out[m_o] = coef * h~[m_i] * rmag */
+void eso_apply_reindex(int li, int lf, int lo, const double* ht, int C, double rmag, double* out) {
+  int src[2 * ESO_LT + 1];
+  double coef[2 * ESO_LT + 1];
+  eso_reindex_rule(li, lf, lo, src, coef);
+  for (int mo = 0; mo < 2 * lo + 1; ++mo)
+    for (int c = 0; c < C; ++c)
+      out[mo * C + c] = (src[mo] == -1000) ? 0.0 : coef[mo] * ht[(src[mo] + li) * C + c] * rmag;
+}
+
+/* eaas_tensor_product: align -> reindex -> unalign.
+ * h: [2li+1][C]; Rgauge optional (NULL -> SPEC gauge).  r = 0 returns the
+ * exact dense result. */
+int eso_eaas_tp(const double* h, int li, int C, const double* r, int lf, int lo, const double* Rgauge, double* out) {
+  if (!tri_ok(li, lf, lo)) return -1;
+  const double n = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  const int di = 2 * li + 1, dout = 2 * lo + 1;
+  if (n <= 1e-8) {
+    double y[2 * ESO_LT + 1];
+    eso_solid_harmonics(lf, r, y);
+    return eso_tensor_product_dense(h, li, C, y, lf, 1, lo, out);
+  }
+  double R[9];
+  if (Rgauge) memcpy(R, Rgauge, sizeof(R));
+  else eso_alignment_rotation(r, R);
+  double Di[(2 * ESO_LT + 1) * (2 * ESO_LT + 1)], Do[(2 * ESO_LT + 1) * (2 * ESO_LT + 1)];
+  eso_wigner_d(li, R, Di);
+  eso_wigner_d(lo, R, Do);
+  double* ht = (double*)malloc(sizeof(double) * di * C);
+  double* w = (double*)malloc(sizeof(double) * dout * C);
+  for (int a = 0; a < di; ++a) /* align: h~ = D_i h (per channel value vector) */
+    for (int c = 0; c < C; ++c) {
+      double s = 0.0;
+      for (int b = 0; b < di; ++b) s += Di[a * di + b] * h[b * C + c];
+      ht[a * C + c] = s;
+    }
+  eso_apply_reindex(li, lf, lo, ht, C, eso_on_axis_solid_harmonic(lf, n), w);
+  for (int a = 0; a < dout; ++a) /* unalign: out = D_o^T w */
+    for (int c = 0; c < C; ++c) {
+      double s = 0.0;
+      for (int b = 0; b < dout; ++b) s += Do[b * dout + a] * w[b * C + c];
+      out[a * C + c] = s;
+    }
+  free(ht); free(w);
+  return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Neighbour index (build_neighbors SPEC.md:431-439):  */
+/* per atom the K nearest j != i with d^2 < r_cut^2 (strict), sorted by */
+/* (d^2, j), sentinel -1.  Atoms only pair inside their segment          */
+/* (seg_ptr[B+1], molecule batches) and, with box != NULL, under the      */
+/* minimum-image convention (the PBC extension of SURVEY F7).  d^2 is     */
+/* ((dx*dx + dy*dy) + dz*dz) in double, no contraction -- the exact      */
+/* sequence the GPU builder uses, so lists are bit-identical.            */
+/* ------------------------------------------------------------------ */
+static inline double pair_d2(const double* pi, const double* pj, const double* box) {
+  double dx = pj[0] - pi[0], dy = pj[1] - pi[1], dz = pj[2] - pi[2];
+  if (box) {
+    dx = dx - box[0] * rint(dx / box[0]);
+    dy = dy - box[1] * rint(dy / box[1]);
+    dz = dz - box[2] * rint(dz / box[2]);
+  }
+  const double xx = dx * dx, yy = dy * dy, zz = dz * dz;
+  const double s = xx + yy;
+  return s + zz;
+}
+
+typedef struct { double d2; int j; } eso_cand;
+static int cand_cmp(const void* a, const void* b) {
+  const eso_cand* x = (const eso_cand*)a;
+  const eso_cand* y = (const eso_cand*)b;
+  if (x->d2 < y->d2) return -1;
+  if (x->d2 > y->d2) return 1;
+  return (x->j > y->j) - (x->j < y->j);
+}
+
+/* Returns 0, or -1 if an atom has more than max_cand in-cutoff
+ * candidates (never for sane systems; max_cand = 4096). */
+int eso_build_neighbors(int N, const double* pos, int nseg, const int* seg_ptr, const double* box, int K, double r_cut,
+                        int* nbr, double* dist, int* count) {
+  const double rc2 = r_cut * r_cut;
+  int err = 0;
+  int one_seg[2] = {0, N};
+  if (!seg_ptr) { seg_ptr = one_seg; nseg = 1; }
+  for (int s = 0; s < nseg; ++s) {
+    const int a0 = seg_ptr[s], a1 = seg_ptr[s + 1];
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int i = a0; i < a1; ++i) {
+      eso_cand* cand = (eso_cand*)malloc(sizeof(eso_cand) * 4096);
+      int nc = 0;
+      for (int j = a0; j < a1; ++j) {
+        if (j == i) continue;
+        const double d2 = pair_d2(pos + 3 * i, pos + 3 * j, box);
+        if (d2 < rc2) {
+          if (nc < 4096) { cand[nc].d2 = d2; cand[nc].j = j; }
+          ++nc;
+        }
+      }
+      if (nc > 4096) {
+#pragma omp atomic write
+        err = -1;
+        nc = 4096;
+      }
+      qsort(cand, (size_t)nc, sizeof(eso_cand), cand_cmp);
+      const int keep = nc < K ? nc : K;
+      for (int k = 0; k < K; ++k) {
+        nbr[(size_t)i * K + k] = k < keep ? cand[k].j : -1;
+        if (dist) dist[(size_t)i * K + k] = k < keep ? sqrt(cand[k].d2) : 0.0;
+      }
+      count[i] = keep;
+      free(cand);
+    }
+  }
+  return err;
+}
+
+/* ------------------------------------------------------------------ */
+/* Projections, Eq. (6) PAPER.md:277-287 / SPEC.md:257-265, plus W_H.  */
+/* W: [(L+1)][C][Dq + Dq + Cv]  (per-l channel mixing, never mixing m).  */
+/* q,k: [N][M][Dq], v: [N][M][Cv].                                      */
+/* ------------------------------------------------------------------ */
+void eso_project(int N, int L, int C, int Dq, int Cv, const double* h, const double* W, double* q, double* k, double* v) {
+  const int M = (L + 1) * (L + 1), Wc = 2 * Dq + Cv;
+#pragma omp parallel for schedule(static)
+  for (int n = 0; n < N; ++n)
+    for (int l = 0; l <= L; ++l)
+      for (int m = 0; m < 2 * l + 1; ++m) {
+        const int mm = l * l + m;
+        const double* x = h + ((size_t)n * M + mm) * C;
+        const double* w = W + (size_t)l * C * Wc;
+        for (int o = 0; o < Wc; ++o) {
+          double s = 0.0;
+          for (int c = 0; c < C; ++c) s += x[c] * w[(size_t)c * Wc + o];
+          if (o < Dq) q[((size_t)n * M + mm) * Dq + o] = s;
+          else if (o < 2 * Dq) k[((size_t)n * M + mm) * Dq + (o - Dq)] = s;
+          else v[((size_t)n * M + mm) * Cv + (o - 2 * Dq)] = s;
+        }
+      }
+}
+
+/* Backward of eso_project: dh and dW from dq, dk, dv. */
+void eso_project_bwd(int N, int L, int C, int Dq, int Cv, const double* h, const double* W, const double* dq,
+                     const double* dk, const double* dv, double* dh, double* dW) {
+  const int M = (L + 1) * (L + 1), Wc = 2 * Dq + Cv;
+#pragma omp parallel for schedule(static)
+  for (int n = 0; n < N; ++n)
+    for (int l = 0; l <= L; ++l)
+      for (int m = 0; m < 2 * l + 1; ++m) {
+        const int mm = l * l + m;
+        const double* w = W + (size_t)l * C * Wc;
+        for (int c = 0; c < C; ++c) {
+          double s = 0.0;
+          for (int o = 0; o < Wc; ++o) {
+            double g;
+            if (o < Dq) g = dq[((size_t)n * M + mm) * Dq + o];
+            else if (o < 2 * Dq) g = dk[((size_t)n * M + mm) * Dq + (o - Dq)];
+            else g = dv[((size_t)n * M + mm) * Cv + (o - 2 * Dq)];
+            s += g * w[(size_t)c * Wc + o];
+          }
+          dh[((size_t)n * M + mm) * C + c] = s;
+        }
+      }
+  if (!dW) return;
+#pragma omp parallel for schedule(static)
+  for (int lc = 0; lc < (L + 1) * C; ++lc) {
+    const int l = lc / C, c = lc % C;
+    for (int o = 0; o < Wc; ++o) {
+      double s = 0.0;
+      for (int n = 0; n < N; ++n)
+        for (int m = 0; m < 2 * l + 1; ++m) {
+          const int mm = l * l + m;
+          double g;
+          if (o < Dq) g = dq[((size_t)n * M + mm) * Dq + o];
+          else if (o < 2 * Dq) g = dk[((size_t)n * M + mm) * Dq + (o - Dq)];
+          else g = dv[((size_t)n * M + mm) * Cv + (o - 2 * Dq)];
+          s += h[((size_t)n * M + mm) * C + c] * g;
+        }
+      dW[((size_t)l * C + c) * Wc + o] = s;
+    }
+  }
+}
+
+/* ------------------------------------------------------------------ */
+/* Stream attention (Alg. 1).         */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  int N, K, H, L;
+  int Dq, Cv;        /* q/k channels per (l,m) row; value channels */
+  double r_cut;
+  int value_mode;    /* 0 = plain (phi * v_j, SPEC stream_aggregate),
+                        1 = dense CG (v_j (x) R^lf(r_ij) summed over paths; the
+                            edge_centric_message oracle SPEC.md:342-350),
+                        2 = EAAS per pair (the reference CPU path) */
+  int phi_mode;      /* 0 = cosine cutoff, 1 = phi == 1 */
+  const double* box; /* NULL or [3] minimum image */
+} eso_attn_desc;
+
+static inline void pair_vec(const double* pos, int i, int j, const double* box, double* r) {
+  r[0] = pos[3 * j] - pos[3 * i]; r[1] = pos[3 * j + 1] - pos[3 * i + 1]; r[2] = pos[3 * j + 2] - pos[3 * i + 2];
+  if (box) for (int a = 0; a < 3; ++a) r[a] = r[a] - box[a] * rint(r[a] / box[a]);
+}
+static inline double phi_of(const eso_attn_desc* d, double rn) {
+  if (d->phi_mode == 1) return 1.0;
+  return rn < d->r_cut ? 0.5 * (cos(ESO_PI * rn / d->r_cut) + 1.0) : 0.0;
+}
+
+/* Value message x[M][Cv] of pair (i,j) for the chosen value mode, phi included.
+ * Mode 1 is the literal per-path dense CG product (tensor_product.hpp:18-49).
+ * Mode 2 is EAAS organised the way a CPU implementation
+ * would: one alignment rotation and D^l per pair, align each l_i block
+ * once, sparse re-index every path, un-align each l_o block once. */
+static void pair_value(const eso_attn_desc* d, const double* v, int j, const double* r, double phi, double* x) {
+  const int L = d->L, M = (L + 1) * (L + 1), Cv = d->Cv;
+  const double* vj = v + (size_t)j * M * Cv;
+  if (d->value_mode == 0) {
+    for (int t = 0; t < M * Cv; ++t) x[t] = phi * vj[t];
+    return;
+  }
+  memset(x, 0, sizeof(double) * M * Cv);
+  const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  if (d->value_mode == 1 || rn <= 1e-8) {
+    double* tmp = (double*)malloc(sizeof(double) * (2 * L + 1) * Cv);
+    double y[2 * ESO_LT + 1];
+    for (int li = 0; li <= L; ++li)
+      for (int lf = 0; lf <= L; ++lf) {
+        eso_solid_harmonics(lf, r, y);
+        for (int lo = 0; lo <= L; ++lo) {
+          if (!tri_ok(li, lf, lo)) continue;
+          tp_dense_tab(cgt(li, lf, lo), vj + (size_t)li * li * Cv, li, Cv, y, lf, 1, lo, tmp);
+          double* xo = x + (size_t)lo * lo * Cv;
+          for (int t = 0; t < (2 * lo + 1) * Cv; ++t) xo[t] += phi * tmp[t];
+        }
+      }
+    free(tmp);
+    return;
+  }
+  double R[9];
+  eso_alignment_rotation(r, R);
+  double* ht = (double*)malloc(sizeof(double) * M * Cv);
+  double* w = (double*)calloc((size_t)M * Cv, sizeof(double));
+  double D[ESO_LT][(2 * ESO_LT - 1) * (2 * ESO_LT - 1)];
+  for (int l = 0; l <= L; ++l) {
+    const int dl = 2 * l + 1;
+    eso_wigner_d(l, R, D[l]);
+    for (int a = 0; a < dl; ++a)
+      for (int c = 0; c < Cv; ++c) {
+        double s = 0.0;
+        for (int b = 0; b < dl; ++b) s += D[l][a * dl + b] * vj[(size_t)(l * l + b) * Cv + c];
+        ht[(size_t)(l * l + a) * Cv + c] = s;
+      }
+  }
+  for (int li = 0; li <= L; ++li)
+    for (int lf = 0; lf <= L; ++lf) {
+      const double rmag = eso_on_axis_solid_harmonic(lf, rn);
+      for (int lo = 0; lo <= L; ++lo) {
+        if (!tri_ok(li, lf, lo)) continue;
+        const eso_rule* ru = rule_of(li, lf, lo);
+        for (int mo = 0; mo < 2 * lo + 1; ++mo) {
+          if (ru->src[mo] == -1000) continue;
+          const double cf = ru->coef[mo] * rmag;
+          const double* hs = ht + (size_t)(li * li + ru->src[mo] + li) * Cv;
+          double* wo = w + (size_t)(lo * lo + mo) * Cv;
+          for (int c = 0; c < Cv; ++c) wo[c] += cf * hs[c];
+        }
+      }
+    }
+  for (int l = 0; l <= L; ++l) {
+    const int dl = 2 * l + 1;
+    for (int a = 0; a < dl; ++a)
+      for (int c = 0; c < Cv; ++c) {
+        double s = 0.0;
+        for (int b = 0; b < dl; ++b) s += D[l][b * dl + a] * w[(size_t)(l * l + b) * Cv + c];
+        x[(size_t)(l * l + a) * Cv + c] = phi * s;
+      }
+  }
+  free(ht); free(w);
+}
+
+/* stream_aggregate: one pass per atom with (mu, z, A)
+ * per head in double, zero output for zero-neighbour rows
+ * (SPEC.md:311).  out [N][M][Cv]; lse [N][H] = mu + log z (or -inf). */
+void eso_attn_fwd(const eso_attn_desc* d, const double* q, const double* k, const double* v, const double* pos,
+                  const int* nbr, double* out, double* lse) {
+  const int N = d->N, K = d->K, H = d->H, L = d->L, M = (L + 1) * (L + 1);
+  const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
+  const double tau = 1.0 / sqrt((double)M * dqh);
+  cg_cache_init();
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * M * Cv);
+    double* A = (double*)malloc(sizeof(double) * M * Cv);
+    double* mu = (double*)malloc(sizeof(double) * H);
+    double* z = (double*)malloc(sizeof(double) * H);
+    double* s = (double*)malloc(sizeof(double) * H);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < N; ++i) {
+      for (int h = 0; h < H; ++h) { mu[h] = -INFINITY; z[h] = 0.0; }
+      memset(A, 0, sizeof(double) * M * Cv);
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = nbr[(size_t)i * K + kk];
+        if (j < 0) continue; /* Alg. 1 line "if j is padding: continue" */
+        double r[3];
+        pair_vec(pos, i, j, d->box, r);
+        const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        for (int h = 0; h < H; ++h) {
+          double acc = 0.0;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+              acc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
+          s[h] = tau * acc; /* Eq. 18 with b == 0 */
+        }
+        pair_value(d, v, j, r, phi_of(d, rn), x);
+        for (int h = 0; h < H; ++h) { /* Eqs. 15-17 */
+          const double mu2 = s[h] > mu[h] ? s[h] : mu[h];
+          const double sc = exp(mu[h] - mu2), e = exp(s[h] - mu2);
+          z[h] = z[h] * sc + e;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * cvh; c < (h + 1) * cvh; ++c)
+              A[mm * Cv + c] = A[mm * Cv + c] * sc + e * x[mm * Cv + c];
+          mu[h] = mu2;
+        }
+      }
+      for (int h = 0; h < H; ++h) {
+        const int empty = !(z[h] > 0.0);
+        for (int mm = 0; mm < M; ++mm)
+          for (int c = h * cvh; c < (h + 1) * cvh; ++c)
+            out[((size_t)i * M + mm) * Cv + c] = empty ? 0.0 : A[mm * Cv + c] / z[h];
+        if (lse) lse[(size_t)i * H + h] = empty ? -INFINITY : mu[h] + log(z[h]);
+      }
+    }
+    free(x); free(A); free(mu); free(z); free(s);
+  }
+}
+
+/* dense_reference_aggregate: materialise the N x K x H
+ * score matrix, two-pass stable softmax, then the weighted sum. */
+void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k, const double* v, const double* pos,
+                        const int* nbr, double* out) {
+  const int N = d->N, K = d->K, H = d->H, L = d->L, M = (L + 1) * (L + 1);
+  const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
+  const double tau = 1.0 / sqrt((double)M * dqh);
+  cg_cache_init();
+  double* S = (double*)malloc(sizeof(double) * (size_t)N * K * H);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < N; ++i)
+    for (int kk = 0; kk < K; ++kk) {
+      const int j = nbr[(size_t)i * K + kk];
+      for (int h = 0; h < H; ++h) {
+        double acc = -INFINITY;
+        if (j >= 0) {
+          acc = 0.0;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+              acc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
+          acc *= tau;
+        }
+        S[((size_t)i * K + kk) * H + h] = acc;
+      }
+    }
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * M * Cv);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < N; ++i) {
+      double* o = out + (size_t)i * M * Cv;
+      memset(o, 0, sizeof(double) * M * Cv);
+      for (int h = 0; h < H; ++h) { /* pass 1: max and normaliser */
+        double mx = -INFINITY, z = 0.0;
+        for (int kk = 0; kk < K; ++kk) { double sv = S[((size_t)i * K + kk) * H + h]; if (sv > mx) mx = sv; }
+        if (mx == -INFINITY) continue;
+        for (int kk = 0; kk < K; ++kk) { double sv = S[((size_t)i * K + kk) * H + h]; if (sv != -INFINITY) z += exp(sv - mx); }
+        for (int kk = 0; kk < K; ++kk) S[((size_t)i * K + kk) * H + h] =
+            (S[((size_t)i * K + kk) * H + h] == -INFINITY) ? 0.0 : exp(S[((size_t)i * K + kk) * H + h] - mx) / z;
+      }
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = nbr[(size_t)i * K + kk];
+        if (j < 0) continue;
+        double r[3];
+        pair_vec(pos, i, j, d->box, r);
+        const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        pair_value(d, v, j, r, phi_of(d, rn), x);
+        for (int h = 0; h < H; ++h) {
+          const double a = S[((size_t)i * K + kk) * H + h];
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * cvh; c < (h + 1) * cvh; ++c) o[mm * Cv + c] += a * x[mm * Cv + c];
+        }
+      }
+    }
+    free(x);
+  }
+  free(S);
+}
+
+/* Per-pair linear value operator T (x = T v per channel, phi included):
+ * T[(lo,mo)][(li,mi)] = phi sum_lf sum_mf C^{lo mo}_{li mi, lf mf} R^lf_mf(r)
+ * for value_mode 1/2 (identical maps, Prop. 1), identity*phi for mode 0. */
+static void pair_T(const eso_attn_desc* d, const double* r, double phi, double* T) {
+  const int L = d->L, M = (L + 1) * (L + 1);
+  memset(T, 0, sizeof(double) * M * M);
+  if (d->value_mode == 0) { for (int a = 0; a < M; ++a) T[a * M + a] = phi; return; }
+  double y[2 * ESO_LT + 1];
+  for (int li = 0; li <= L; ++li)
+    for (int lf = 0; lf <= L; ++lf) {
+      eso_solid_harmonics(lf, r, y);
+      for (int lo = 0; lo <= L; ++lo) {
+        if (!tri_ok(li, lf, lo)) continue;
+        const double* t = cgt(li, lf, lo);
+        const int d1 = 2 * li + 1, d2 = 2 * lf + 1;
+        for (int mo = 0; mo < 2 * lo + 1; ++mo)
+          for (int mi = 0; mi < d1; ++mi) {
+            double s = 0.0;
+            for (int mf = 0; mf < d2; ++mf) s += t[mo * d1 * d2 + mi * d2 + mf] * y[mf];
+            T[(lo * lo + mo) * M + li * li + mi] += phi * s;
+          }
+      }
+    }
+}
+
+/* stream_aggregate_backward: gradients of
+ * sum <dout, out> w.r.t. q, k, v by recomputation from (q,k,v,lse). */
+void eso_attn_bwd(const eso_attn_desc* d, const double* q, const double* k, const double* v, const double* pos,
+                  const int* nbr, const double* out, const double* lse, const double* dout, double* dq, double* dk,
+                  double* dv) {
+  const int N = d->N, K = d->K, H = d->H, L = d->L, M = (L + 1) * (L + 1);
+  const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
+  const double tau = 1.0 / sqrt((double)M * dqh);
+  cg_cache_init();
+  memset(dq, 0, sizeof(double) * (size_t)N * M * Dq);
+  memset(dk, 0, sizeof(double) * (size_t)N * M * Dq);
+  memset(dv, 0, sizeof(double) * (size_t)N * M * Cv);
+  /* serial over i (scatter onto j), parallel inside would race: keep simple */
+  double* T = (double*)malloc(sizeof(double) * M * M);
+  double* Delta = (double*)malloc(sizeof(double) * H);
+  double* y = (double*)malloc(sizeof(double) * M * Cv);
+  for (int i = 0; i < N; ++i) {
+    for (int h = 0; h < H; ++h) {
+      double s = 0.0;
+      for (int mm = 0; mm < M; ++mm)
+        for (int c = h * cvh; c < (h + 1) * cvh; ++c)
+          s += dout[((size_t)i * M + mm) * Cv + c] * out[((size_t)i * M + mm) * Cv + c];
+      Delta[h] = s;
+    }
+    for (int kk = 0; kk < K; ++kk) {
+      const int j = nbr[(size_t)i * K + kk];
+      if (j < 0) continue;
+      double r[3];
+      pair_vec(pos, i, j, d->box, r);
+      const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+      pair_T(d, r, phi_of(d, rn), T);
+      /* y = T^T dout_i  [M][Cv] */
+      for (int a = 0; a < M; ++a)
+        for (int c = 0; c < Cv; ++c) {
+          double s = 0.0;
+          for (int o = 0; o < M; ++o) s += T[o * M + a] * dout[((size_t)i * M + o) * Cv + c];
+          y[a * Cv + c] = s;
+        }
+      for (int h = 0; h < H; ++h) {
+        double sc = 0.0;
+        for (int mm = 0; mm < M; ++mm)
+          for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+            sc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
+        const double p = exp(tau * sc - lse[(size_t)i * H + h]);
+        double dp = 0.0;
+        for (int mm = 0; mm < M; ++mm)
+          for (int c = h * cvh; c < (h + 1) * cvh; ++c) {
+            dp += y[mm * Cv + c] * v[((size_t)j * M + mm) * Cv + c];
+            dv[((size_t)j * M + mm) * Cv + c] += p * y[mm * Cv + c];
+          }
+        const double ds = p * (dp - Delta[h]);
+        for (int mm = 0; mm < M; ++mm)
+          for (int c = h * dqh; c < (h + 1) * dqh; ++c) {
+            dq[((size_t)i * M + mm) * Dq + c] += tau * ds * k[((size_t)j * M + mm) * Dq + c];
+            dk[((size_t)j * M + mm) * Dq + c] += tau * ds * q[((size_t)i * M + mm) * Dq + c];
+          }
+      }
+    }
+  }
+  free(T); free(Delta); free(y);
+}
+
+/* Per-pair operator for tests (exposes pair_T). */
+void eso_pair_operator(int L, int value_mode, double r_cut, int phi_mode, const double* r, double* T) {
+  eso_attn_desc d;
+  memset(&d, 0, sizeof(d));
+  d.L = L; d.value_mode = value_mode; d.r_cut = r_cut; d.phi_mode = phi_mode;
+  cg_cache_init();
+  const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+  pair_T(&d, r, phi_of(&d, rn), T);
+}
+
+int eso_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+void eso_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
