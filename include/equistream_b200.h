@@ -1,0 +1,162 @@
+/*
+ * equistream_b200.h -- C ABI of libequistream_b200.so, the B200-native
+ * (sm_100a) drop-in for the hot path of the reference `equistream` library
+ * (/root/reference, arXiv 2601.16622 E2Former-V2): the fused on-the-fly
+ * equivariant attention with per-pair EAAS, forward and recompute backward,
+ * its neighbour/tile builder and its Q/K/V projections.
+ *
+ * Every entry point names the reference interface it replaces.  The
+ * reference ships these as C++20 header-only library types and SPEC
+ * operations (paths relative to /root/reference):
+ *
+ *   es_attn_fwd            <- stream_aggregate            SPEC.md:275-283 (Alg. 1)
+ *   es_attn_bwd            <- stream_aggregate_backward
+ *   es_neighbors_build     <- build_neighbors             SPEC.md:431-439 (NeighborIndex SPEC.md:237-242)
+ *   es_neighbors_transpose <- (the scatter relation build_neighbors implies; used by es_attn_bwd)
+ *   es_tile_mask           <- north-star tile-skip mask over NeighborIndex
+ *   es_project_fwd         <- project_qk + W_H
+ *   es_project_bwd         <- gradient of project_qk / W_H
+ *   es_conventions_manifest<- so3::conventions_manifest() proj/include/equistream/so3/conventions.hpp:13-38
+ *   es_cg_real / es_reindex_table / es_wigner_d_host
+ *                          <- so3::cg_real clebsch.hpp:179, eaas build_reindex_rule SPEC.md:181,
+ *                             so3::wigner_d wigner.hpp:70 (host-side tables the kernels use)
+ *
+ * Conventions (the reference's, restated): real orthonormal harmonics,
+ * m = -l..l ascending, (-1)^m on positive-m components; feature blocks are
+ * value vectors v -> D v; node features are "irreps layout" [N][M][C] with
+ * M = (L+1)^2, row l*l + (m+l), channels innermost (the byte order of the
+ * reference IrrepsFeature blocks, irreps.hpp:69-71).
+ *
+ * Rules of the ABI: plain C types, caller-owned device buffers (the library
+ * never allocates or frees caller memory), `stream` is a cudaStream_t passed
+ * as void* (NULL = legacy default stream), every call is stream-ordered and
+ * returns an es_status; no exception crosses the boundary.  On failure,
+ * es_last_error() returns a thread-local description.  There is no CPU
+ * fallback: without an sm_100a device every compute call fails with
+ * ES_CUDA_ERROR.
+ */
+#ifndef EQUISTREAM_B200_H
+#define EQUISTREAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ES_ABI_VERSION 1
+
+typedef enum {
+  ES_OK = 0,
+  ES_INVALID_ARGUMENT = 1, /* maps to std::invalid_argument (reference errors, irreps.hpp:37-41) */
+  ES_UNSUPPORTED = 2,      /* valid request outside the compiled kernel set */
+  ES_CUDA_ERROR = 3,       /* maps to std::runtime_error */
+  ES_NCCL_ERROR = 4
+} es_status;
+
+typedef enum { ES_F32 = 0, ES_BF16 = 1 } es_dtype;
+
+typedef enum {
+  ES_VALUE_PLAIN = 0, /* value = phi(r_ij) * v_j: SPEC stream_aggregate with precomputed h' */
+  ES_VALUE_EAAS = 1   /* value = phi(r_ij) * sum_paths (v_j (x) R^lf(r_ij))^lo via per-pair EAAS
+                         (north star; == edge_centric_message SPEC.md:342-350) */
+} es_value_mode;
+
+typedef enum {
+  ES_PHI_COSINE = 0, /* phi = (cos(pi r / r_cut) + 1) / 2 for r < r_cut */
+  ES_PHI_ONE = 1     /* phi == 1 */
+} es_phi_mode;
+
+/* Attention problem.  q, k: [N][M][2C]; v, out, dout: [N][M][C]
+ * (dtype), lse: [N][H] float32, pos: [N][3] float64, nbr: [N][K] int32 with
+ * sentinel -1 (NeighborIndex).  Head h owns q/k channels [h*2C/H, (h+1)*2C/H)
+ * and value channels [h*C/H, (h+1)*C/H) at every (l, m) row; d_k = 2*M*C/H,
+ * tau = 1/sqrt(d_k), b(r) == 0.  Attention weights softmax over the valid
+ * neighbours of each atom; atoms without neighbours produce 0 and lse=-inf
+ * (SPEC.md:311). */
+typedef struct {
+  int32_t N, K, H, L, C;
+  int32_t value_mode; /* es_value_mode */
+  int32_t phi_mode;   /* es_phi_mode */
+  int32_t dtype;      /* es_dtype of q, k, v, out, dout, dq, dk, dv */
+  double r_cut;
+  int32_t periodic;   /* 1: minimum image in box[] */
+  double box[3];
+} es_attn_desc;
+
+/* Compiled kernel set: L in [0, 4]; C in {32, 64, 128, 256}; C/H in
+ * {8, 16, 32, ...} with C/H >= 2 (L <= 2) or >= 1 (L >= 3). */
+es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
+                      const int32_t* nbr, void* out, float* lse, void* stream);
+
+/* Workspace: es_attn_bwd_workspace_size(d) bytes (per-pair-head dscore
+ * buffer, O(N*K*H) scalars -- never O(N*K*C)). rev_ptr/rev_pair
+ * come from es_neighbors_transpose on the same nbr. */
+size_t es_attn_bwd_workspace_size(const es_attn_desc* d);
+es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
+                      const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
+                      const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Neighbour index: per atom the K nearest j != i with d^2 < r_cut^2, sorted
+ * by (d^2, j), padded with -1, restricted to the atom's segment
+ * (seg_ptr[nseg+1] contiguous molecule ranges, or NULL for one system) and,
+ * if periodic, under the minimum image.  d^2 is evaluated in double with
+ * round-to-nearest and no contraction, ((dx*dx + dy*dy) + dz*dz), so lists
+ * are bit-identical to the CPU oracle.  dist (optional, may be NULL) gets
+ * float(sqrt(d^2)); count[N] the filled slots. */
+typedef struct {
+  int32_t N, K, nseg;
+  int32_t periodic;
+  double r_cut;
+  double box[3];
+} es_nbr_desc;
+size_t es_neighbors_workspace_size(const es_nbr_desc* d);
+es_status es_neighbors_build(const es_nbr_desc* d, const double* pos, const int32_t* seg_ptr, int32_t* nbr,
+                             float* dist, int32_t* count, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Transposed (key-major) relation of nbr: for key j, entries
+ * rev_pair[rev_ptr[j] .. rev_ptr[j+1]) hold i*K + slot with nbr[i][slot] == j,
+ * ascending (deterministic).  rev_ptr: [N+1], rev_pair: [N*K]. */
+size_t es_neighbors_transpose_workspace_size(int32_t N, int32_t K);
+es_status es_neighbors_transpose(int32_t N, int32_t K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair,
+                                 void* workspace, size_t workspace_bytes, void* stream);
+
+/* Tile-skip mask: bit (qb, kb) of mask[qb * ceil(nkb/32) + kb/32] is set iff
+ * some atom of query block qb (tq atoms) lists a neighbour in key block kb
+ * (tk atoms).  mask must be zeroed by the caller. */
+es_status es_tile_mask(int32_t N, int32_t K, const int32_t* nbr, int32_t tq, int32_t tk, uint32_t* mask,
+                       void* stream);
+
+/* Projections, Eq. (6) + W_H: per degree l a channel-mixing matrix
+ * W[l] = [W_Q | W_K | W_V] of shape [C][2*Dq + C] (Dq = 2C: W_Q = [W_Q1 | W_Q2]).
+ * h: [N][M][C] (dtype), W: [L+1][C][2Dq+C] (dtype), outputs q,k [N][M][Dq], v [N][M][C]. */
+typedef struct {
+  int32_t N, L, C;
+  int32_t dtype;
+} es_proj_desc;
+es_status es_project_fwd(const es_proj_desc* d, const void* h, const void* W, void* q, void* k, void* v,
+                         void* stream);
+/* dh [N][M][C] (dtype, overwritten); dW [L+1][C][2Dq+C] float32 (overwritten) or NULL. */
+es_status es_project_bwd(const es_proj_desc* d, const void* h, const void* W, const void* dq, const void* dk,
+                         const void* dv, void* dh, float* dW, void* stream);
+
+/* Host-side introspection of the tables the kernels use. */
+const char* es_conventions_manifest(void);
+double es_cg_real(int32_t l1, int32_t m1, int32_t l2, int32_t m2, int32_t lo, int32_t mo);
+/* Aligned-frame re-index polynomial of entry (lo, li, m) for max degree L:
+ * coefficient of source +m (a) and -m (b) as sum_lf coef[lf] r^lf, lf = 0..4. */
+es_status es_reindex_table(int32_t L, int32_t lo, int32_t li, int32_t m, double* a5, double* b5);
+/* D^l(R) by the kernels' harmonic-fit construction, in double (R row-major). */
+es_status es_wigner_d_host(int32_t l, const double* R, double* D);
+
+const char* es_last_error(void);
+int32_t es_abi_version(void);
+/* 1 if a CUDA device of compute capability 10.x is visible. */
+int32_t es_device_ok(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EQUISTREAM_B200_H */

@@ -1,0 +1,96 @@
+"""ctypes binding of libequistream_b200.so (the C ABI in include/equistream_b200.h).
+
+There is no CPU fallback: if the library is missing or no sm_100a device is
+visible, every compute entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libequistream_b200.so")
+
+ES_OK, ES_INVALID_ARGUMENT, ES_UNSUPPORTED, ES_CUDA_ERROR, ES_NCCL_ERROR = range(5)
+ES_F32, ES_BF16 = 0, 1
+ES_VALUE_PLAIN, ES_VALUE_EAAS = 0, 1
+ES_PHI_COSINE, ES_PHI_ONE = 0, 1
+
+
+class AttnDesc(ct.Structure):
+    _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("H", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32),
+                ("value_mode", ct.c_int32), ("phi_mode", ct.c_int32), ("dtype", ct.c_int32),
+                ("r_cut", ct.c_double), ("periodic", ct.c_int32), ("box", ct.c_double * 3)]
+
+
+class NbrDesc(ct.Structure):
+    _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("nseg", ct.c_int32), ("periodic", ct.c_int32),
+                ("r_cut", ct.c_double), ("box", ct.c_double * 3)]
+
+
+class ProjDesc(ct.Structure):
+    _fields_ = [("N", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32), ("dtype", ct.c_int32)]
+
+
+class EsError(RuntimeError):
+    pass
+
+
+class EsInvalidArgument(EsError, ValueError):
+    """ES_INVALID_ARGUMENT -- the reference's std::invalid_argument."""
+
+
+class EsUnsupported(EsError):
+    pass
+
+
+_lib = None
+
+EXPORTS = [
+    "es_attn_fwd", "es_attn_bwd", "es_attn_bwd_workspace_size", "es_neighbors_build",
+    "es_neighbors_workspace_size", "es_neighbors_transpose", "es_neighbors_transpose_workspace_size",
+    "es_tile_mask", "es_project_fwd", "es_project_bwd", "es_conventions_manifest", "es_cg_real",
+    "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
+]
+
+
+def lib() -> ct.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EsError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                          "(python -m paper_2601_16622_b200.build); there is no CPU fallback")
+        L = ct.CDLL(LIB_PATH)
+        vp, i32, sz, dp = ct.c_void_p, ct.c_int32, ct.c_size_t, ct.POINTER(ct.c_double)
+        L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 8
+        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 14 + [sz, vp]
+        L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
+        L.es_attn_bwd_workspace_size.restype = sz
+        L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]
+        L.es_neighbors_workspace_size.argtypes = [ct.POINTER(NbrDesc)]
+        L.es_neighbors_workspace_size.restype = sz
+        L.es_neighbors_transpose.argtypes = [i32, i32, vp, vp, vp, vp, sz, vp]
+        L.es_neighbors_transpose_workspace_size.argtypes = [i32, i32]
+        L.es_neighbors_transpose_workspace_size.restype = sz
+        L.es_tile_mask.argtypes = [i32, i32, vp, i32, i32, vp, vp]
+        L.es_project_fwd.argtypes = [ct.POINTER(ProjDesc)] + [vp] * 6
+        L.es_project_bwd.argtypes = [ct.POINTER(ProjDesc)] + [vp] * 8
+        L.es_conventions_manifest.restype = ct.c_char_p
+        L.es_last_error.restype = ct.c_char_p
+        L.es_cg_real.restype = ct.c_double
+        L.es_cg_real.argtypes = [i32] * 6
+        L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
+        L.es_wigner_d_host.argtypes = [i32, dp, dp]
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == ES_OK:
+        return
+    msg = f"{what}: {lib().es_last_error().decode(errors='replace')}"
+    if status == ES_INVALID_ARGUMENT:
+        raise EsInvalidArgument(msg)
+    if status == ES_UNSUPPORTED:
+        raise EsUnsupported(msg)
+    raise EsError(msg)

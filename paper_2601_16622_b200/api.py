@@ -1,0 +1,259 @@
+"""Python mirror of the reference operator interface for the hot path
+(SPEC.md stream_attention :232-325, bench.build_neighbors :431-439), over the
+C ABI.  Names, argument meaning and error behaviour follow the SPEC:
+shape/precondition violations raise ValueError (EsInvalidArgument, the
+reference's std::invalid_argument), internal/CUDA failures RuntimeError.
+
+All tensors are CUDA tensors; launches go to torch's current stream.  No
+CPU fallback exists -- a CPU tensor is an argument error.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import EsInvalidArgument, check, lib
+
+_DT = {torch.float32: _lib.ES_F32, torch.bfloat16: _lib.ES_BF16}
+_VALUE = {"plain": _lib.ES_VALUE_PLAIN, "eaas": _lib.ES_VALUE_EAAS}
+_PHI = {"cosine": _lib.ES_PHI_COSINE, "one": _lib.ES_PHI_ONE}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, name: str, dtype=None, shape=None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        raise EsInvalidArgument(f"{name}: expected a tensor")
+    if not t.is_cuda:
+        raise EsInvalidArgument(f"{name}: must be a CUDA tensor (no CPU fallback)")
+    if dtype is not None and t.dtype != dtype:
+        raise EsInvalidArgument(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise EsInvalidArgument(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if not t.is_contiguous():
+        raise EsInvalidArgument(f"{name}: must be contiguous")
+    return t
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def conventions_manifest() -> str:
+    return lib().es_conventions_manifest().decode()
+
+
+# ------------------------------------------------------------------ neighbours
+@dataclass
+class NeighborIndex:
+    """NeighborIndex: table [N][K] int32, sentinel -1,
+    rows sorted by (d^2, j); distances [N][K] float32; count [N]."""
+    table: torch.Tensor
+    distances: torch.Tensor | None
+    count: torch.Tensor
+    r_cut: float
+    box: tuple | None = None
+    _rev: tuple | None = None
+
+    @property
+    def N(self) -> int:
+        return self.table.shape[0]
+
+    @property
+    def K(self) -> int:
+        return self.table.shape[1]
+
+    def transpose(self):
+        if self._rev is None:
+            self._rev = neighbors_transpose(self.table)
+        return self._rev
+
+
+def build_neighbors(pos: torch.Tensor, K: int, r_cut: float, seg_ptr: torch.Tensor | None = None,
+                    box=None, with_distances: bool = True) -> NeighborIndex:
+    """build_neighbors: K nearest j != i with |r_ij| < r_cut,
+    inside the atom's segment (molecule batch) and under the minimum image
+    when `box` is given.  Bit-identical to the CPU oracle."""
+    pos = _need(pos, "pos", torch.float64)
+    if pos.dim() != 2 or pos.shape[1] != 3:
+        raise EsInvalidArgument("pos: expected [N, 3]")
+    if K < 1:
+        raise EsInvalidArgument("build_neighbors: K >= 1")
+    N = pos.shape[0]
+    dev = pos.device
+    d = _lib.NbrDesc()
+    d.N, d.K, d.r_cut = N, int(K), float(r_cut)
+    d.nseg = 0
+    if seg_ptr is not None:
+        seg_ptr = _need(seg_ptr, "seg_ptr", torch.int32)
+        d.nseg = seg_ptr.numel() - 1
+    d.periodic = 0 if box is None else 1
+    if box is not None:
+        for a in range(3):
+            d.box[a] = float(box[a])
+    nbr = torch.empty((N, K), dtype=torch.int32, device=dev)
+    dist = torch.empty((N, K), dtype=torch.float32, device=dev) if with_distances else None
+    cnt = torch.empty((N,), dtype=torch.int32, device=dev)
+    ws = _workspace(lib().es_neighbors_workspace_size(ct.byref(d)), dev)
+    check(lib().es_neighbors_build(ct.byref(d), _ptr(pos), _ptr(seg_ptr), _ptr(nbr), _ptr(dist), _ptr(cnt),
+                                   _ptr(ws), ws.numel(), _stream()), "es_neighbors_build")
+    return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box))
+
+
+def neighbors_transpose(table: torch.Tensor):
+    """Key-major relation: (rev_ptr [N+1], rev_pair [N*K]) with
+    rev_pair[rev_ptr[j]:rev_ptr[j+1]] = sorted {i*K+slot : table[i,slot] == j}."""
+    table = _need(table, "table", torch.int32)
+    N, K = table.shape
+    rev_ptr = torch.empty(N + 1, dtype=torch.int32, device=table.device)
+    rev_pair = torch.empty(max(N * K, 1), dtype=torch.int32, device=table.device)
+    ws = _workspace(lib().es_neighbors_transpose_workspace_size(N, K), table.device)
+    check(lib().es_neighbors_transpose(N, K, _ptr(table), _ptr(rev_ptr), _ptr(rev_pair), _ptr(ws), ws.numel(),
+                                       _stream()), "es_neighbors_transpose")
+    return rev_ptr, rev_pair
+
+
+def tile_mask(table: torch.Tensor, tq: int = 32, tk: int = 32) -> torch.Tensor:
+    """Tile-skip bitmask [ceil(N/tq)][ceil(ceil(N/tk)/32)] uint32 (stored int32)."""
+    table = _need(table, "table", torch.int32)
+    N, K = table.shape
+    nqb = (N + tq - 1) // tq
+    words = ((N + tk - 1) // tk + 31) // 32
+    mask = torch.zeros((nqb, words), dtype=torch.int32, device=table.device)
+    check(lib().es_tile_mask(N, K, _ptr(table), tq, tk, _ptr(mask), _stream()), "es_tile_mask")
+    return mask
+
+
+# ------------------------------------------------------------------ projections
+def _proj_desc(h: torch.Tensor, L: int) -> _lib.ProjDesc:
+    d = _lib.ProjDesc()
+    d.N, d.L, d.C = h.shape[0], int(L), h.shape[2]
+    d.dtype = _DT[h.dtype]
+    return d
+
+
+def project_qk(h: torch.Tensor, W: torch.Tensor, L: int):
+    """project_qk + W_H (Eq. 6): h [N][M][C], W [L+1][C][5C]
+    -> q, k [N][M][2C], v [N][M][C] (same dtype)."""
+    if h.dtype not in _DT:
+        raise EsInvalidArgument("h: dtype must be float32 or bfloat16")
+    M = (L + 1) ** 2
+    _need(h, "h")
+    if h.dim() != 3 or h.shape[1] != M:
+        raise EsInvalidArgument(f"h: expected [N, {M}, C]")
+    N, _, C = h.shape
+    _need(W, "W", h.dtype, (L + 1, C, 5 * C))
+    q = torch.empty((N, M, 2 * C), dtype=h.dtype, device=h.device)
+    k = torch.empty_like(q)
+    v = torch.empty((N, M, C), dtype=h.dtype, device=h.device)
+    d = _proj_desc(h, L)
+    check(lib().es_project_fwd(ct.byref(d), _ptr(h), _ptr(W), _ptr(q), _ptr(k), _ptr(v), _stream()),
+          "es_project_fwd")
+    return q, k, v
+
+
+def project_qk_backward(h, W, L, dq, dk, dv, want_dW: bool = True):
+    d = _proj_desc(h, L)
+    for t, n in ((dq, "dq"), (dk, "dk"), (dv, "dv")):
+        _need(t, n, h.dtype)
+    dh = torch.empty_like(h)
+    dW = torch.empty(W.shape, dtype=torch.float32, device=h.device) if want_dW else None
+    check(lib().es_project_bwd(ct.byref(d), _ptr(h), _ptr(W), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dh), _ptr(dW),
+                               _stream()), "es_project_bwd")
+    return dh, dW
+
+
+# ------------------------------------------------------------------ attention
+@dataclass
+class AttentionConfig:
+    heads: int
+    L: int
+    r_cut: float = 6.0
+    value_mode: str = "eaas"
+    phi: str = "cosine"
+    box: tuple | None = None
+
+    def desc(self, N: int, K: int, C: int, dtype: torch.dtype) -> _lib.AttnDesc:
+        if self.value_mode not in _VALUE:
+            raise EsInvalidArgument(f"value_mode must be one of {list(_VALUE)}")
+        if self.phi not in _PHI:
+            raise EsInvalidArgument(f"phi must be one of {list(_PHI)}")
+        d = _lib.AttnDesc()
+        d.N, d.K, d.H, d.L, d.C = N, K, int(self.heads), int(self.L), C
+        d.value_mode = _VALUE[self.value_mode]
+        d.phi_mode = _PHI[self.phi]
+        d.dtype = _DT[dtype]
+        d.r_cut = float(self.r_cut)
+        d.periodic = 0 if self.box is None else 1
+        if self.box is not None:
+            for a in range(3):
+                d.box[a] = float(self.box[a])
+        return d
+
+
+@dataclass
+class SavedAttention:
+    """What stream_aggregate_backward needs (SPEC.md:293 'saved inputs')."""
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    pos: torch.Tensor
+    idx: NeighborIndex
+    out: torch.Tensor
+    lse: torch.Tensor
+    cfg: AttentionConfig
+
+
+def _check_qkv(q, k, v, pos, idx, cfg):
+    if q.dtype not in _DT:
+        raise EsInvalidArgument("q: dtype must be float32 or bfloat16")
+    M = (cfg.L + 1) ** 2
+    _need(v, "v", q.dtype)
+    if v.dim() != 3 or v.shape[1] != M:
+        raise EsInvalidArgument(f"v: expected [N, {M}, C]")
+    N, _, C = v.shape
+    _need(q, "q", q.dtype, (N, M, 2 * C))
+    _need(k, "k", q.dtype, (N, M, 2 * C))
+    _need(pos, "pos", torch.float64, (N, 3))
+    _need(idx.table, "idx.table", torch.int32)
+    if idx.table.shape[0] != N:
+        raise EsInvalidArgument("idx: row count != N")
+    return N, C
+
+
+def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig):
+    """stream_aggregate (Alg. 1): returns (m [N][M][C], lse [N][H] f32)."""
+    N, C = _check_qkv(q, k, v, pos, idx, cfg)
+    out = torch.empty_like(v)
+    lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
+    d = cfg.desc(N, idx.K, C, q.dtype)
+    check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
+                            _ptr(lse), _stream()), "es_attn_fwd")
+    return out, lse
+
+
+def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention):
+    """stream_aggregate_backward: (grad_q, grad_k, grad_v) of
+    sum <grad_m, m>, by recomputation (no O(N*K*C) buffer)."""
+    s = saved
+    N, C = _check_qkv(s.q, s.k, s.v, s.pos, s.idx, s.cfg)
+    grad_m = _need(grad_m.contiguous(), "grad_m", s.q.dtype, tuple(s.v.shape))
+    rev_ptr, rev_pair = s.idx.transpose()
+    d = s.cfg.desc(N, s.idx.K, C, s.q.dtype)
+    ws = _workspace(lib().es_attn_bwd_workspace_size(ct.byref(d)), s.q.device)
+    dq = torch.empty_like(s.q)
+    dk = torch.empty_like(s.k)
+    dv = torch.empty_like(s.v)
+    check(lib().es_attn_bwd(ct.byref(d), _ptr(s.q), _ptr(s.k), _ptr(s.v), _ptr(s.pos), _ptr(s.idx.table),
+                            _ptr(rev_ptr), _ptr(rev_pair), _ptr(s.out), _ptr(s.lse), _ptr(grad_m), _ptr(dq),
+                            _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()), "es_attn_bwd")
+    return dq, dk, dv

@@ -1,0 +1,358 @@
+// Neighbour index builder (build_neighbors) + transposed
+// relation + tile-skip mask, sm_100a.
+//
+// Bit-exactness contract with the CPU oracle: every candidate's squared
+// distance is ((dx*dx + dy*dy) + dz*dz) in double, each operation rounded
+// to nearest with no FMA contraction (__dmul_rn / __dadd_rn), minimum image
+// dx - box*rint(dx/box) under PBC; a pair is kept iff d2 < r_cut^2 (strict),
+// j != i, same segment; the list is the K smallest by (d2, j).  Since the
+// output is a pure function of that candidate set, the search structure
+// (hashed cell grid or per-segment scan) cannot change a single bit.
+//
+// Search structures:
+//  * segmented input (molecule batches): thread per atom scans its segment;
+//  * one system: hashed uniform grid, cell edge >= r_cut, 27-cell stencil,
+//    exact cell-coordinate filter against hash collisions; under PBC the grid
+//    tiles the box (>= 3 cells per axis).
+#include <cub/cub.cuh>
+
+#include "es_internal.h"
+
+namespace es {
+
+constexpr int kMaxK = 128;
+
+__device__ __forceinline__ double d2_exact(double xi, double yi, double zi, double xj, double yj, double zj,
+                                           int periodic, double bx, double by, double bz) {
+  double dx = __dsub_rn(xj, xi), dy = __dsub_rn(yj, yi), dz = __dsub_rn(zj, zi);
+  if (periodic) {
+    dx = __dsub_rn(dx, __dmul_rn(bx, rint(__ddiv_rn(dx, bx))));
+    dy = __dsub_rn(dy, __dmul_rn(by, rint(__ddiv_rn(dy, by))));
+    dz = __dsub_rn(dz, __dmul_rn(bz, rint(__ddiv_rn(dz, bz))));
+  }
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+struct TopK {
+  double d2[kMaxK];
+  int j[kMaxK];
+  int n;
+  __device__ void insert(double d, int jj, int K) {
+    if (n == K) {
+      if (d > d2[K - 1] || (d == d2[K - 1] && jj > j[K - 1])) return;
+      --n;
+    }
+    int p = n;
+    while (p > 0 && (d2[p - 1] > d || (d2[p - 1] == d && j[p - 1] > jj))) {
+      d2[p] = d2[p - 1];
+      j[p] = j[p - 1];
+      --p;
+    }
+    d2[p] = d;
+    j[p] = jj;
+    ++n;
+  }
+};
+
+struct NbrK {
+  int N, K, nseg, periodic;
+  double rc2, bx, by, bz;
+};
+
+__device__ __forceinline__ void emit(const NbrK& p, int i, const TopK& t, int32_t* nbr, float* dist, int32_t* count) {
+  for (int s = 0; s < p.K; ++s) {
+    nbr[(size_t)i * p.K + s] = s < t.n ? t.j[s] : -1;
+    if (dist) dist[(size_t)i * p.K + s] = s < t.n ? (float)sqrt(t.d2[s]) : 0.f;
+  }
+  count[i] = t.n;
+}
+
+__global__ void __launch_bounds__(128) nbr_segment_kernel(NbrK p, const double* __restrict__ pos,
+                                                          const int32_t* __restrict__ seg_ptr,
+                                                          int32_t* __restrict__ nbr, float* __restrict__ dist,
+                                                          int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  int a0 = 0, a1 = p.N;
+  if (seg_ptr) {
+    int lo = 0, hi = p.nseg;  // find s with seg_ptr[s] <= i < seg_ptr[s+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (seg_ptr[mid] <= i) lo = mid;
+      else hi = mid;
+    }
+    a0 = seg_ptr[lo];
+    a1 = seg_ptr[lo + 1];
+  }
+  TopK t;
+  t.n = 0;
+  const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+  for (int j = a0; j < a1; ++j) {
+    if (j == i) continue;
+    const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
+    if (d < p.rc2) t.insert(d, j, p.K);
+  }
+  emit(p, i, t, nbr, dist, count);
+}
+
+// ---------------------------------------------------------------- hashed grid
+struct GridK {
+  double cs[3];  // cell edge per axis
+  int nc[3];     // cells per axis (PBC only)
+  int periodic;
+  unsigned mask;  // bucket count - 1
+};
+
+__device__ __forceinline__ unsigned cell_hash(int cx, int cy, int cz, unsigned mask) {
+  return ((unsigned)cx * 73856093u ^ (unsigned)cy * 19349663u ^ (unsigned)cz * 83492791u) & mask;
+}
+
+__device__ __forceinline__ int4 cell_of(const GridK& g, double x, double y, double z, double bx, double by,
+                                        double bz) {
+  int4 c;
+  if (g.periodic) {
+    const double xw = x - bx * floor(x / bx), yw = y - by * floor(y / by), zw = z - bz * floor(z / bz);
+    c.x = min(max((int)floor(xw / g.cs[0]), 0), g.nc[0] - 1);
+    c.y = min(max((int)floor(yw / g.cs[1]), 0), g.nc[1] - 1);
+    c.z = min(max((int)floor(zw / g.cs[2]), 0), g.nc[2] - 1);
+  } else {
+    c.x = (int)floor(x / g.cs[0]);
+    c.y = (int)floor(y / g.cs[1]);
+    c.z = (int)floor(z / g.cs[2]);
+  }
+  c.w = 0;
+  return c;
+}
+
+__global__ void grid_key_kernel(int N, GridK g, NbrK p, const double* __restrict__ pos, unsigned* __restrict__ key,
+                                int* __restrict__ idx, int4* __restrict__ cell) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int4 c = cell_of(g, pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], p.bx, p.by, p.bz);
+  cell[i] = c;
+  key[i] = cell_hash(c.x, c.y, c.z, g.mask);
+  idx[i] = i;
+}
+
+__global__ void grid_bounds_kernel(int N, const unsigned* __restrict__ skey, int* __restrict__ start,
+                                   int* __restrict__ end) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= N) return;
+  const unsigned k = skey[s];
+  if (s == 0 || skey[s - 1] != k) start[k] = s;
+  if (s == N - 1 || skey[s + 1] != k) end[k] = s + 1;
+}
+
+__global__ void __launch_bounds__(128) nbr_grid_kernel(NbrK p, GridK g, const double* __restrict__ pos,
+                                                       const int4* __restrict__ cell, const int* __restrict__ sidx,
+                                                       const int* __restrict__ start, const int* __restrict__ end,
+                                                       int32_t* __restrict__ nbr, float* __restrict__ dist,
+                                                       int32_t* __restrict__ count) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.N) return;
+  TopK t;
+  t.n = 0;
+  const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
+  const int4 ci = cell[i];
+  for (int ox = -1; ox <= 1; ++ox)
+    for (int oy = -1; oy <= 1; ++oy)
+      for (int oz = -1; oz <= 1; ++oz) {
+        int cx = ci.x + ox, cy = ci.y + oy, cz = ci.z + oz;
+        if (g.periodic) {
+          cx = (cx + g.nc[0]) % g.nc[0];
+          cy = (cy + g.nc[1]) % g.nc[1];
+          cz = (cz + g.nc[2]) % g.nc[2];
+        }
+        const unsigned h = cell_hash(cx, cy, cz, g.mask);
+        for (int s = start[h]; s < end[h]; ++s) {
+          const int j = sidx[s];
+          const int4 cj = cell[j];
+          if (cj.x != cx || cj.y != cy || cj.z != cz || j == i) continue;
+          const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by,
+                                    p.bz);
+          if (d < p.rc2) t.insert(d, j, p.K);
+        }
+      }
+  emit(p, i, t, nbr, dist, count);
+}
+
+namespace {
+unsigned pow2_at_least(unsigned n) {
+  unsigned b = 1024;
+  while (b < n) b <<= 1;
+  return b;
+}
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct GridWs {
+  size_t key, skey, idx, sidx, cell, start, end, cub, total;
+  size_t cub_bytes;
+};
+GridWs grid_ws(int N) {
+  GridWs w{};
+  const unsigned nb = pow2_at_least(2u * (unsigned)N);
+  size_t cub_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
+                                  (int*)nullptr, N);
+  size_t o = 0;
+  w.key = o; o += align256(sizeof(unsigned) * N);
+  w.skey = o; o += align256(sizeof(unsigned) * N);
+  w.idx = o; o += align256(sizeof(int) * N);
+  w.sidx = o; o += align256(sizeof(int) * N);
+  w.cell = o; o += align256(sizeof(int4) * N);
+  w.start = o; o += align256(sizeof(int) * nb);
+  w.end = o; o += align256(sizeof(int) * nb);
+  w.cub = o; o += align256(cub_bytes);
+  w.cub_bytes = cub_bytes;
+  w.total = o;
+  return w;
+}
+bool use_grid(const NbrArgs& a) {
+  if (a.nseg > 1) return false;
+  if (a.N <= 1024) return false;
+  if (a.periodic) {
+    for (int d = 0; d < 3; ++d)
+      if (a.box[d] / a.r_cut < 3.0) return false;
+  }
+  return true;
+}
+}  // namespace
+
+size_t nbr_workspace_bytes(const NbrArgs& a) {
+  if (!use_grid(a)) return 256;
+  return grid_ws(a.N).total;
+}
+
+es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* seg_ptr, int32_t* nbr, float* dist,
+                           int32_t* count, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (a.K > kMaxK) return fail(ES_UNSUPPORTED, "neighbors: K > 128");
+  if (a.N == 0) return ES_OK;
+  NbrK p;
+  p.N = a.N; p.K = a.K; p.nseg = a.nseg; p.periodic = a.periodic;
+  p.rc2 = a.r_cut * a.r_cut;
+  p.bx = a.box[0]; p.by = a.box[1]; p.bz = a.box[2];
+  const int tpb = 128, blocks = (a.N + tpb - 1) / tpb;
+  if (!use_grid(a)) {
+    const int32_t* sp = (seg_ptr && a.nseg >= 1) ? seg_ptr : nullptr;  // NULL: one segment [0, N)
+    nbr_segment_kernel<<<blocks, tpb, 0, st>>>(p, pos, sp, nbr, dist, count);
+    return cuda_status(cudaGetLastError(), "nbr_segment_kernel");
+  }
+  const GridWs w = grid_ws(a.N);
+  if (ws_bytes < w.total) return fail(ES_INVALID_ARGUMENT, "neighbors: workspace too small");
+  char* base = (char*)ws;
+  GridK g;
+  g.periodic = a.periodic;
+  for (int d = 0; d < 3; ++d) {
+    if (a.periodic) {
+      g.nc[d] = (int)floor(a.box[d] / a.r_cut);
+      g.cs[d] = a.box[d] / g.nc[d];
+    } else {
+      g.nc[d] = 0;
+      g.cs[d] = a.r_cut * 1.000001;
+    }
+  }
+  const unsigned nb = pow2_at_least(2u * (unsigned)a.N);
+  g.mask = nb - 1;
+  unsigned* key = (unsigned*)(base + w.key);
+  unsigned* skey = (unsigned*)(base + w.skey);
+  int* idx = (int*)(base + w.idx);
+  int* sidx = (int*)(base + w.sidx);
+  int4* cell = (int4*)(base + w.cell);
+  int* start = (int*)(base + w.start);
+  int* end = (int*)(base + w.end);
+  grid_key_kernel<<<blocks, tpb, 0, st>>>(a.N, g, p, pos, key, idx, cell);
+  size_t cb = w.cub_bytes;
+  int bits = 1;
+  while ((1u << bits) < nb) ++bits;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(base + w.cub, cb, key, skey, idx, sidx, a.N, 0, bits, st);
+  if (e != cudaSuccess) return cuda_status(e, "neighbors: radix sort");
+  cudaMemsetAsync(start, 0, sizeof(int) * nb, st);
+  cudaMemsetAsync(end, 0, sizeof(int) * nb, st);
+  grid_bounds_kernel<<<blocks, tpb, 0, st>>>(a.N, skey, start, end);
+  nbr_grid_kernel<<<blocks, tpb, 0, st>>>(p, g, pos, cell, sidx, start, end, nbr, dist, count);
+  return cuda_status(cudaGetLastError(), "nbr_grid_kernel");
+}
+
+// ---------------------------------------------------------------- transpose
+__global__ void tr_keys_kernel(int N, int K, const int32_t* __restrict__ nbr, unsigned* __restrict__ key,
+                               int* __restrict__ val, int* __restrict__ cnt) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * K) return;
+  const int j = nbr[t];
+  key[t] = j >= 0 ? (unsigned)j : (unsigned)N;
+  val[t] = (int)t;
+  if (j >= 0) atomicAdd(&cnt[j], 1);
+}
+
+namespace {
+struct TrWs {
+  size_t key, skey, val, cnt, cub, total, cub_sort, cub_scan;
+};
+TrWs tr_ws(int N, int K) {
+  TrWs w{};
+  const int n = N * K;
+  size_t cs = 0, cc = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, cs, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
+                                  (int*)nullptr, n);
+  cub::DeviceScan::ExclusiveSum(nullptr, cc, (int*)nullptr, (int*)nullptr, N + 1);
+  size_t o = 0;
+  w.key = o; o += align256(sizeof(unsigned) * n);
+  w.skey = o; o += align256(sizeof(unsigned) * n);
+  w.val = o; o += align256(sizeof(int) * n);
+  w.cnt = o; o += align256(sizeof(int) * (N + 1));
+  w.cub = o; o += align256(cs > cc ? cs : cc);
+  w.cub_sort = cs; w.cub_scan = cc;
+  w.total = o;
+  return w;
+}
+}  // namespace
+
+size_t transpose_workspace_bytes(int N, int K) { return tr_ws(N, K).total; }
+
+es_status nbr_transpose_launch(int N, int K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair, void* ws,
+                               size_t ws_bytes, cudaStream_t st) {
+  const TrWs w = tr_ws(N, K);
+  if (ws_bytes < w.total) return fail(ES_INVALID_ARGUMENT, "neighbors_transpose: workspace too small");
+  if (N == 0) return ES_OK;
+  char* base = (char*)ws;
+  unsigned* key = (unsigned*)(base + w.key);
+  unsigned* skey = (unsigned*)(base + w.skey);
+  int* val = (int*)(base + w.val);
+  int* cnt = (int*)(base + w.cnt);
+  const int n = N * K;
+  cudaMemsetAsync(cnt, 0, sizeof(int) * (N + 1), st);
+  tr_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(N, K, nbr, key, val, cnt);
+  int bits = 1;
+  while ((1u << bits) <= (unsigned)N) ++bits;
+  size_t cb = w.cub_sort;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(base + w.cub, cb, key, skey, val, (int*)rev_pair, n, 0, bits, st);
+  if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: sort");
+  cb = w.cub_scan;
+  e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, N + 1, st);
+  if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: scan");
+  return cuda_status(cudaGetLastError(), "neighbors_transpose");
+}
+
+// ---------------------------------------------------------------- tile mask
+__global__ void tile_mask_kernel(int N, int K, const int32_t* __restrict__ nbr, int tq, int tk, int words,
+                                 uint32_t* __restrict__ mask) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * K) return;
+  const int j = nbr[t];
+  if (j < 0) return;
+  const int i = (int)(t / K);
+  const int qb = i / tq, kb = j / tk;
+  atomicOr(&mask[(size_t)qb * words + kb / 32], 1u << (kb % 32));
+}
+
+es_status tile_mask_launch(int N, int K, const int32_t* nbr, int tq, int tk, uint32_t* mask, cudaStream_t st) {
+  if (tq <= 0 || tk <= 0) return fail(ES_INVALID_ARGUMENT, "tile_mask: tile sizes must be positive");
+  if (N == 0) return ES_OK;
+  const int nkb = (N + tk - 1) / tk;
+  const int words = (nkb + 31) / 32;
+  const size_t n = (size_t)N * K;
+  tile_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, K, nbr, tq, tk, words, mask);
+  return cuda_status(cudaGetLastError(), "tile_mask_kernel");
+}
+
+}  // namespace es

@@ -1,0 +1,280 @@
+"""GPU parity: every kernel through the C ABI against the CPU oracle on the
+same seeded inputs.  Tolerances (normwise, max|gpu - ref| / max|ref|):
+  * neighbour / tile / transpose lists: bit-exact
+  * fp32 path: <= 1e-5
+  * bf16-input path (fp32 accumulation): <= 2e-2
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import pyoracle as po
+from paper_2601_16622_b200 import systems as S
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")]
+
+F32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def es():
+    import paper_2601_16622_b200 as es
+    from paper_2601_16622_b200 import _lib
+    assert _lib.lib().es_device_ok() == 1, "not an sm_100 device"
+    return es
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def dev(x, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(x)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+# ------------------------------------------------------------------ neighbours
+NBR_CASES = {
+    "fcc2048_grid": lambda: (S.gen_fcc_system(2048, 3.8, 0), None, None, 64),
+    "fcc600_scan": lambda: (S.gen_fcc_system(600, 3.8, 1), None, None, 64),
+    "fcc3000_K8": lambda: (S.gen_fcc_system(3000, 3.8, 2), None, None, 8),
+    "batch": lambda: (lambda b: (b.pos, b.seg_ptr, None, 32))(S.molecule_batch(64, 40, 60, 3)),
+    "pbc_grid": lambda: (lambda b: (b.pos, None, b.box, 64))(S.periodic_box(6000, 12, 3.8, 4)),
+    "pbc_small_box": lambda: (lambda b: (b.pos, None, b.box, 64))(S.periodic_box(100, 4, 3.8, 5)),
+}
+
+
+@pytest.mark.parametrize("case", list(NBR_CASES))
+def test_neighbors_bit_exact(es, oracle, case):
+    pos, seg, box, K = NBR_CASES[case]()
+    ref_nbr, ref_dist, ref_cnt = po.build_neighbors(pos, K, 6.0, seg_ptr=seg, box=box)
+    idx = es.build_neighbors(dev(pos), K, 6.0, None if seg is None else dev(seg), box)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(idx.table.cpu().numpy(), ref_nbr)
+    np.testing.assert_array_equal(idx.count.cpu().numpy(), ref_cnt)
+    np.testing.assert_array_equal(idx.distances.cpu().numpy(), ref_dist.astype(np.float32))
+
+
+def test_neighbors_edge_cases(es):
+    two = dev(np.array([[0.0, 0, 0], [1.0, 0, 0]]))
+    idx = es.build_neighbors(two, 4, 2.0)
+    assert idx.table.cpu().tolist() == [[1, -1, -1, -1], [0, -1, -1, -1]]
+    none = es.build_neighbors(dev(S.gen_fcc_system(3000, 3.8, 0)), 4, 1.0)
+    assert (none.table == -1).all() and (none.count == 0).all()
+    empty = es.build_neighbors(torch.zeros((0, 3), dtype=torch.float64, device="cuda"), 4, 6.0)
+    assert empty.table.shape == (0, 4)
+
+
+def test_transpose_and_tile_mask(es, oracle):
+    pos = S.gen_fcc_system(1500, 3.8, 7)
+    nbr, _, _ = po.build_neighbors(pos, 16, 6.0)  # K-truncated: asymmetric relation
+    t = dev(nbr)
+    rev_ptr, rev_pair = es.neighbors_transpose(t)
+    rev_ptr = rev_ptr.cpu().numpy()
+    rev_pair = rev_pair.cpu().numpy()
+    N, K = nbr.shape
+    for j in range(N):
+        exp = np.sort(np.nonzero(nbr.ravel() == j)[0])
+        np.testing.assert_array_equal(rev_pair[rev_ptr[j]:rev_ptr[j + 1]], exp)
+    mask = es.tile_mask(t, 32, 64).cpu().numpy().view(np.uint32)
+    exp = np.zeros_like(mask)
+    for i in range(N):
+        for j in nbr[i][nbr[i] >= 0]:
+            exp[i // 32, (j // 64) // 32] |= np.uint32(1 << ((j // 64) % 32))
+    np.testing.assert_array_equal(mask, exp)
+
+
+# ------------------------------------------------------------------ projections
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("L,C", [(2, 64), (4, 32), (1, 128)])
+def test_projection_fwd_bwd(es, oracle, dtype, L, C):
+    N = 37
+    h = S.random_features(N, L, C, 1)
+    W = S.random_weights(L, C, 1)
+    if dtype == torch.bfloat16:  # compare on the same (bf16-rounded) inputs
+        h = torch.tensor(h).to(dtype).double().numpy()
+        W = torch.tensor(W).to(dtype).double().numpy()
+    q, k, v = es.project_qk(dev(h, dtype), dev(W, dtype), L)
+    rq, rk, rv = po.project(h, W, L)
+    tol = F32_TOL if dtype == torch.float32 else BF16_TOL
+    for a, b in ((q, rq), (k, rk), (v, rv)):
+        assert rel(a.float().cpu(), b) < tol
+    rng = np.random.default_rng(2)
+    g = [rng.standard_normal(x.shape) for x in (rq, rk, rv)]
+    if dtype == torch.bfloat16:
+        g = [torch.tensor(x).to(dtype).double().numpy() for x in g]
+    dh, dW = es.project_qk_backward(dev(h, dtype), dev(W, dtype), L, *(dev(x, dtype) for x in g))
+    rdh, rdW = po.project_bwd(h, W, L, *g)
+    assert rel(dh.float().cpu(), rdh) < tol
+    assert rel(dW.cpu(), rdW) < tol
+
+
+# ------------------------------------------------------------------ attention
+def _attn_inputs(N, L, C, H, K, seed, seg=False, box=None):
+    if box is not None:
+        sysm = S.periodic_box(N, 4, 3.8, seed)
+        pos, segp, box = sysm.pos, None, sysm.box
+    elif seg:
+        b = S.molecule_batch(6, 20, 40, seed)
+        pos, segp = b.pos, b.seg_ptr
+        N = len(pos)
+    else:
+        pos, segp = S.gen_fcc_system(N, 3.8, seed), None
+    nbr, _, _ = po.build_neighbors(pos, K, 6.0, seg_ptr=segp, box=box)
+    h = S.random_features(len(pos), L, C, seed)
+    W = S.random_weights(L, C, seed)
+    q, k, v = po.project(h, W, L)
+    return pos, nbr, q, k, v, box
+
+
+def _run_attn(es, pos, nbr, q, k, v, L, H, vm, dtype, box=None, dout=None):
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    cfg = AttentionConfig(heads=H, L=L, r_cut=6.0, value_mode=vm, box=None if box is None else tuple(box))
+    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    tq, tk, tv = dev(q, dtype), dev(k, dtype), dev(v, dtype)
+    tp = dev(pos)
+    out, lse = es.stream_aggregate(tq, tk, tv, tp, idx, cfg)
+    grads = None
+    if dout is not None:
+        grads = es.stream_aggregate_backward(dev(dout, dtype), SavedAttention(tq, tk, tv, tp, idx, out, lse, cfg))
+    torch.cuda.synchronize()
+    return out, lse, grads
+
+
+ATTN_CASES = [  # (L, C, H, N, K)
+    (0, 64, 8, 64, 64), (1, 64, 8, 80, 64), (2, 64, 8, 64, 64), (2, 128, 8, 150, 64), (2, 32, 4, 90, 32),
+    (3, 64, 4, 70, 64), (4, 128, 8, 60, 64), (2, 256, 8, 40, 64),
+]
+
+
+@pytest.mark.parametrize("vm", ["eaas", "plain"])
+@pytest.mark.parametrize("L,C,H,N,K", ATTN_CASES)
+def test_attention_fwd_bwd_fp32(es, oracle, vm, L, C, H, N, K):
+    pos, nbr, q, k, v, _ = _attn_inputs(N, L, C, H, K, seed=L + C)
+    nbr[5] = -1          # zero-neighbour row
+    nbr[7, 3:] = -1      # short row
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE if vm == "eaas" else po.VALUE_PLAIN)
+    rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
+    dout = np.random.default_rng(3).standard_normal(rout.shape)
+    out, lse, (dq, dk, dv) = _run_attn(es, pos, nbr, q, k, v, L, H, vm, torch.float32, dout=dout)
+    assert rel(out.cpu(), rout) < F32_TOL
+    fin = np.isfinite(rlse)
+    assert np.all(np.isneginf(lse.cpu().numpy()[~fin]))
+    assert rel(lse.cpu().numpy()[fin], rlse[fin]) < F32_TOL
+    assert np.all(out.cpu().numpy()[5] == 0)
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, dout)
+    assert rel(dq.cpu(), rdq) < F32_TOL
+    assert rel(dk.cpu(), rdk) < F32_TOL
+    assert rel(dv.cpu(), rdv) < F32_TOL
+
+
+@pytest.mark.parametrize("L,C,H,N,K", [(2, 128, 8, 120, 64), (4, 128, 8, 50, 64), (1, 64, 4, 80, 32)])
+def test_attention_bf16(es, oracle, L, C, H, N, K):
+    pos, nbr, q, k, v, _ = _attn_inputs(N, L, C, H, K, seed=11)
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE)
+    rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
+    dout = torch.tensor(np.random.default_rng(4).standard_normal(rout.shape)).bfloat16().double().numpy()
+    out, lse, (dq, dk, dv) = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, dout=dout)
+    assert rel(out.float().cpu(), rout) < BF16_TOL
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, dout)
+    for a, b in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        assert rel(a.float().cpu(), b) < BF16_TOL
+
+
+def test_attention_periodic_and_batch(es, oracle):
+    for kw in ({"box": True}, {"seg": True}):
+        L, C, H = 2, 64, 8
+        pos, nbr, q, k, v, box = _attn_inputs(200, L, C, H, 64, seed=21, seg=kw.get("seg", False),
+                                              box=np.zeros(3) if kw.get("box") else None)
+        P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
+        rout, _ = po.attn_fwd(P, q, k, v, pos, nbr)
+        out, _, _ = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.float32, box=box)
+        assert rel(out.cpu(), rout) < F32_TOL
+
+
+def test_attention_coincident_atoms(es, oracle):
+    """r_ij = 0 pairs: only l_f = 0 paths survive."""
+    L, C, H = 2, 64, 8
+    pos = S.gen_fcc_system(40, 3.8, 2)
+    pos[3] = pos[4]
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0)
+    h = S.random_features(40, L, C, 2)
+    q, k, v = po.project(h, S.random_weights(L, C, 2), L)
+    rout, _ = po.attn_fwd(po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE), q, k, v, pos, nbr)
+    out, _, _ = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.float32)
+    assert rel(out.cpu(), rout) < F32_TOL
+
+
+def test_layer_equivariance_and_autograd(es, oracle):
+    """Full block (projections + attention) on GPU: rotate-in == rotate-out
+    (Acceptance 4) and autograd grads == oracle chain rule."""
+    from paper_2601_16622_b200.api import AttentionConfig
+    L, C, H = 2, 64, 8
+    pos = S.gen_fcc_system(120, 3.8, 9)
+    h = S.random_features(120, L, C, 9)
+    W = S.random_weights(L, C, 9)
+    rng = np.random.default_rng(10)
+    qq = rng.standard_normal(4)
+    qq /= np.linalg.norm(qq)
+    w, x, y, z = qq
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+    Db = np.zeros((9, 9))
+    for l in range(3):
+        Db[l * l:(l + 1) ** 2, l * l:(l + 1) ** 2] = po.wigner_d(l, R)
+    cfg = AttentionConfig(heads=H, L=L)
+    tp = dev(pos)
+    idx = es.build_neighbors(tp, 64, 6.0)
+    th = dev(h, torch.float32).requires_grad_(True)
+    tW = dev(W, torch.float32).requires_grad_(True)
+    out = es.attention_layer(th, tW, tp, idx, cfg)
+    g = rng.standard_normal(out.shape)
+    out.backward(dev(g, torch.float32))
+    idx2 = es.build_neighbors(dev(pos @ R.T), 64, 6.0)
+    out2 = es.attention_layer(dev(np.einsum("ab,nbc->nac", Db, h), torch.float32), tW.detach(), dev(pos @ R.T),
+                              idx2, cfg)
+    rot = np.einsum("ab,nbc->nac", Db, out.detach().cpu().numpy())
+    assert rel(out2.detach().cpu(), rot) < 1e-5
+    # oracle chain rule
+    q, k, v = po.project(h, W, L)
+    nbr = idx.table.cpu().numpy()
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE)
+    rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
+    assert rel(out.detach().cpu(), rout) < F32_TOL
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, g)
+    rdh, rdW = po.project_bwd(h, W, L, rdq, rdk, rdv)
+    assert rel(th.grad.cpu(), rdh) < F32_TOL
+    assert rel(tW.grad.cpu(), rdW) < F32_TOL
+
+
+@pytest.mark.slow
+def test_full_size_properties_config2(es):
+    """Config 2 at full size (4096 molecules): linearity of the layer in v and
+    zero-padding neutrality -- size-independent properties (the oracle is
+    too slow at 205k atoms; parity at small sizes above)."""
+    from paper_2601_16622_b200.api import AttentionConfig
+    b = S.molecule_batch(4096, 40, 60, 0)
+    L, C, H = 2, 128, 8
+    tp = dev(b.pos)
+    idx = es.build_neighbors(tp, 64, 6.0, dev(b.seg_ptr))
+    N = len(b.pos)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    q = torch.randn(N, 9, 2 * C, device="cuda", generator=g)
+    k = torch.randn(N, 9, 2 * C, device="cuda", generator=g)
+    v1 = torch.randn(N, 9, C, device="cuda", generator=g)
+    v2 = torch.randn(N, 9, C, device="cuda", generator=g)
+    cfg = AttentionConfig(heads=H, L=L)
+    o1, _ = es.stream_aggregate(q, k, v1, tp, idx, cfg)
+    o2, _ = es.stream_aggregate(q, k, v2, tp, idx, cfg)
+    o12, _ = es.stream_aggregate(q, k, v1 + 2 * v2, tp, idx, cfg)
+    assert rel((o1 + 2 * o2).cpu(), o12.cpu()) < 1e-5
+    assert torch.isfinite(o12).all()
+    cnt = idx.count.cpu().numpy()
+    assert 10 < cnt.mean() < 20
