@@ -71,6 +71,11 @@ struct ProjArgs {
 };
 es_status proj_fwd_launch(const ProjArgs& a, const void* h, const void* W, void* q, void* k, void* v,
                           cudaStream_t st);
+bool proj_tc_supported(const ProjArgs& a);
+es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, void* q, void* k, void* v,
+                             cudaStream_t st);
+es_status proj_bwd_tc_launch(const ProjArgs& a, const void* h, const void* W, const void* dq, const void* dk,
+                             const void* dv, void* dh, float* dW, cudaStream_t st);
 es_status proj_bwd_launch(const ProjArgs& a, const void* h, const void* W, const void* dq, const void* dk,
                           const void* dv, void* dh, float* dW, cudaStream_t st);
 

@@ -7,6 +7,8 @@
 // mixing never touches m (it commutes with D^l), so q.k stays invariant.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "es_internal.h"
 
 namespace es {
@@ -164,15 +166,26 @@ es_status bwd_t(const ProjArgs& a, const void* h, const void* W, const void* dq,
 }
 }  // namespace
 
+static bool force_simt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ES_PROJ_SIMT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 es_status proj_fwd_launch(const ProjArgs& a, const void* h, const void* W, void* q, void* k, void* v,
                           cudaStream_t st) {
   if (a.N == 0) return ES_OK;
+  if (!force_simt() && proj_tc_supported(a)) return proj_fwd_tc_launch(a, h, W, q, k, v, st);
   return a.dtype == ES_BF16 ? fwd_t<__nv_bfloat16>(a, h, W, q, k, v, st) : fwd_t<float>(a, h, W, q, k, v, st);
 }
 
 es_status proj_bwd_launch(const ProjArgs& a, const void* h, const void* W, const void* dq, const void* dk,
                           const void* dv, void* dh, float* dW, cudaStream_t st) {
   if (a.N == 0) return ES_OK;
+  if (!force_simt() && proj_tc_supported(a)) return proj_bwd_tc_launch(a, h, W, dq, dk, dv, dh, dW, st);
   return a.dtype == ES_BF16 ? bwd_t<__nv_bfloat16>(a, h, W, dq, dk, dv, dh, dW, st)
                             : bwd_t<float>(a, h, W, dq, dk, dv, dh, dW, st);
 }

@@ -1,0 +1,385 @@
+// tcgen05 / TMEM / TMA projections for the bf16 path (north-star subsystem 1):
+// Eq. (6) + W_H per degree l as UMMA GEMMs, operands staged by TMA with
+// 128-byte swizzle, fp32 accumulators in tensor memory, epilogue from TMEM.
+//
+//   fwd : Y[(n,l,m), o]  = h[n,(l,m),:] . W[l][:, o]        A K-major (h rows), B MN-major (W as stored)
+//   dh  : dh[(n,l,m), c] = G[n,(l,m),:] . W[l][c, :]        A K-major (dq|dk|dv rows), B K-major (W rows)
+//   dW  : dW[l][c, o]   += sum_(n,m) h[.,c] G[., o]         A MN-major (h), B MN-major (G); split-K, fp32 red
+// where G = [dq | dk | dv] along o.  The rows of degree l are the (n, m)
+// pairs of the irreps layout -- a 3-D TMA box (C, M, N) picks them without
+// any host-side re-layout.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "es_internal.h"
+#include "umma.cuh"
+
+namespace es {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// bf16 tensor map, dims innermost-first, 128B swizzle
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+              const uint32_t* box) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t gd[5], gs[4];
+  cuuint32_t bd[5], es_[5];
+  for (int i = 0; i < rank; ++i) {
+    gd[i] = dims[i];
+    bd[i] = box[i];
+    es_[i] = 1;
+  }
+  for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bd, es_,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct TcP {
+  int N, M, C, L;
+};
+
+__device__ __forceinline__ int degree_of_row(int mm) {
+  int l = 0;
+  while ((l + 1) * (l + 1) <= mm) ++l;
+  return l;
+}
+
+__device__ __forceinline__ void store_row32(bf16* dst, const uint32_t (&r)[32]) {
+  uint4 pk[4];
+  uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+    const __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]));
+    w[t] = *reinterpret_cast<const uint32_t*>(&b);
+  }
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) d[t] = pk[t];
+}
+
+// ------------------------------------------------------------------ forward
+// grid (ceil(N/128), M, 5): tile = 128 atoms at one (l,m) row x 128 output columns; K = C = 128.
+__global__ void __launch_bounds__(128) proj_fwd_tc_kernel(const __grid_constant__ CUtensorMap mh,
+                                                          const __grid_constant__ CUtensorMap mw, TcP p,
+                                                          bf16* __restrict__ q, bf16* __restrict__ k,
+                                                          bf16* __restrict__ v) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
+  uint8_t* Bs = smem + 32768;         // [2 kb][2 nb][64 k-rows][64] bf16, 8 KB each
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * 128, mm = blockIdx.y, chunk = blockIdx.z;
+  const int l = degree_of_row(mm);
+  const int o0 = chunk * 128;
+  if (threadIdx.x == 0) {
+    umma::prefetch_tmap(&mh);
+    umma::prefetch_tmap(&mw);
+    umma::mbar_init(&bars[0], 1);
+    umma::mbar_init(&bars[1], 1);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 128);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t taddr = *tslot;
+  if (threadIdx.x == 0) {
+    umma::mbar_arrive_expect_tx(&bars[0], 65536);
+    umma::tma_load_3d(As, &mh, &bars[0], 0, mm, n0);
+    umma::tma_load_3d(As + 16384, &mh, &bars[0], 64, mm, n0);
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb)
+        umma::tma_load_2d(Bs + (kb * 2 + nb) * 8192, &mw, &bars[0], o0 + 64 * nb, l * p.C + 64 * kb);
+    umma::mbar_wait(&bars[0], 0);
+    umma::tc_fence_after();
+    constexpr uint32_t idesc = umma::idesc_bf16(128, 128, 0, 1);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int kb = s >> 2, ks = s & 3;
+      const uint64_t ad = umma::sdesc(umma::smem_u32(As + kb * 16384) + ks * 32, 16, 1024);
+      const uint64_t bd = umma::sdesc(umma::smem_u32(Bs + kb * 16384) + ks * 2048, 8192, 1024);
+      umma::mma_f16(taddr, ad, bd, idesc, s > 0 ? 1u : 0u);
+    }
+    umma::mma_commit(&bars[1]);
+  }
+  umma::mbar_wait(&bars[1], 0);
+  umma::tc_fence_after();
+  const int n = n0 + warp * 32 + lane;
+  bf16* dst;
+  if (o0 < 2 * p.C) dst = q + ((size_t)n * p.M + mm) * (2 * p.C) + o0;
+  else if (o0 < 4 * p.C) dst = k + ((size_t)n * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
+  else dst = v + ((size_t)n * p.M + mm) * p.C + (o0 - 4 * p.C);
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t r[32];
+    umma::tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
+    if (n < p.N) store_row32(dst + cc * 32, r);
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(taddr, 128);
+}
+
+// ------------------------------------------------------------------ dh
+// grid (ceil(N/128), M): tile = 128 atoms at (l,m) x 128 channels; K = 5C in 64-wide blocks.
+constexpr int kDhStages = 4;
+__global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__ CUtensorMap mdq,
+                                                         const __grid_constant__ CUtensorMap mdk,
+                                                         const __grid_constant__ CUtensorMap mdv,
+                                                         const __grid_constant__ CUtensorMap mwk, TcP p,
+                                                         bf16* __restrict__ dh) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDhStages * 32768);
+  uint64_t* empty = full + kDhStages;
+  uint64_t* done = empty + kDhStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * 128, mm = blockIdx.y;
+  const int l = degree_of_row(mm);
+  const int nkb = (5 * p.C) / 64, kq = (2 * p.C) / 64;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDhStages; ++s) {
+      umma::mbar_init(&full[s], 1);
+      umma::mbar_init(&empty[s], 1);
+    }
+    umma::mbar_init(done, 1);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 128);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t taddr = *tslot;
+  if (warp == 0 && lane == 0) {  // TMA producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDhStages, round = kb / kDhStages;
+      if (round > 0) umma::mbar_wait(&empty[s], (round - 1) & 1);
+      uint8_t* A = smem + s * 32768;
+      umma::mbar_arrive_expect_tx(&full[s], 32768);
+      if (kb < kq) umma::tma_load_3d(A, &mdq, &full[s], kb * 64, mm, n0);
+      else if (kb < 2 * kq) umma::tma_load_3d(A, &mdk, &full[s], (kb - kq) * 64, mm, n0);
+      else umma::tma_load_3d(A, &mdv, &full[s], (kb - 2 * kq) * 64, mm, n0);
+      umma::tma_load_2d(A + 16384, &mwk, &full[s], kb * 64, l * p.C);
+    }
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    constexpr uint32_t idesc = umma::idesc_bf16(128, 128, 0, 0);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kDhStages, round = kb / kDhStages;
+      umma::mbar_wait(&full[s], round & 1);
+      umma::tc_fence_after();
+      const uint32_t a0 = umma::smem_u32(smem + s * 32768);
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks)
+        umma::mma_f16(taddr, umma::sdesc(a0 + ks * 32, 16, 1024), umma::sdesc(a0 + 16384 + ks * 32, 16, 1024),
+                      idesc, (kb | ks) ? 1u : 0u);
+      umma::mma_commit(&empty[s]);
+    }
+    umma::mma_commit(done);
+  }
+  umma::mbar_wait(done, 0);
+  umma::tc_fence_after();
+  const int n = n0 + warp * 32 + lane;
+  bf16* dst = dh + ((size_t)n * p.M + mm) * p.C;
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    uint32_t r[32];
+    umma::tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
+    if (n < p.N) store_row32(dst + cc * 32, r);
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(taddr, 128);
+}
+
+// ------------------------------------------------------------------ dW
+// grid (splits, 5): split-K over atoms for one degree l (R = (2l+1)*nb rows
+// per stage); D = [c 128] x [o 128]; fp32 reduction into dW.
+constexpr int kDwStages = 2;
+__global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__ CUtensorMap mh,
+                                                         const __grid_constant__ CUtensorMap mdq,
+                                                         const __grid_constant__ CUtensorMap mdk,
+                                                         const __grid_constant__ CUtensorMap mdv, TcP p, int l,
+                                                         int nb, int atoms_per_split, float* __restrict__ dW) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int R = (2 * l + 1) * nb;
+  const int half = R * 128;       // one 64-wide MN block: R rows x 128 B
+  const int stage_bytes = 4 * half;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDwStages * stage_bytes);
+  uint64_t* empty = full + kDwStages;
+  uint64_t* done = empty + kDwStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int chunk = blockIdx.y, o0 = chunk * 128;
+  const int a_begin = blockIdx.x * atoms_per_split;
+  const int a_end = min(p.N, a_begin + atoms_per_split);
+  const int nst = a_end > a_begin ? (a_end - a_begin + nb - 1) / nb : 0;
+  const CUtensorMap* mg = o0 < 2 * p.C ? &mdq : (o0 < 4 * p.C ? &mdk : &mdv);
+  const int og = o0 < 2 * p.C ? o0 : (o0 < 4 * p.C ? o0 - 2 * p.C : o0 - 4 * p.C);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDwStages; ++s) {
+      umma::mbar_init(&full[s], 1);
+      umma::mbar_init(&empty[s], 1);
+    }
+    umma::mbar_init(done, 1);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 128);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t taddr = *tslot;
+  if (nst > 0) {
+    if (warp == 0 && lane == 0) {
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kDwStages, round = it / kDwStages;
+        if (round > 0) umma::mbar_wait(&empty[s], (round - 1) & 1);
+        uint8_t* st = smem + s * stage_bytes;
+        const int na = a_begin + it * nb;
+        umma::mbar_arrive_expect_tx(&full[s], stage_bytes);
+        umma::tma_load_3d(st, &mh, &full[s], 0, l * l, na);
+        umma::tma_load_3d(st + half, &mh, &full[s], 64, l * l, na);
+        umma::tma_load_3d(st + 2 * half, mg, &full[s], og, l * l, na);
+        umma::tma_load_3d(st + 3 * half, mg, &full[s], og + 64, l * l, na);
+      }
+    } else if (warp == 1 && lane == 0) {
+      constexpr uint32_t idesc = umma::idesc_bf16(128, 128, 1, 1);
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % kDwStages, round = it / kDwStages;
+        umma::mbar_wait(&full[s], round & 1);
+        umma::tc_fence_after();
+        const uint32_t a0 = umma::smem_u32(smem + s * stage_bytes);
+        for (int ks = 0; ks < R / 16; ++ks)
+          umma::mma_f16(taddr, umma::sdesc(a0 + ks * 2048, half, 1024),
+                        umma::sdesc(a0 + 2 * half + ks * 2048, half, 1024), idesc, (it | ks) ? 1u : 0u);
+        umma::mma_commit(&empty[s]);
+      }
+      umma::mma_commit(done);
+    }
+    umma::mbar_wait(done, 0);
+    umma::tc_fence_after();
+    const int c = warp * 32 + lane;
+    float* dst = dW + ((size_t)l * p.C + c) * (5 * p.C) + o0;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t r[32];
+      umma::tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
+#pragma unroll
+      for (int t = 0; t < 32; ++t) atomicAdd(dst + cc * 32 + t, __uint_as_float(r[t]));
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(taddr, 128);
+}
+
+bool map3(CUtensorMap* m, const void* base, int inner, int M, int N, int box0, int box1, int box2) {
+  const uint64_t dims[3] = {(uint64_t)inner, (uint64_t)M, (uint64_t)N};
+  const uint64_t strides[2] = {(uint64_t)inner * 2, (uint64_t)inner * M * 2};
+  const uint32_t box[3] = {(uint32_t)box0, (uint32_t)box1, (uint32_t)box2};
+  return make_map(m, base, 3, dims, strides, box);
+}
+bool map2(CUtensorMap* m, const void* base, int inner, int rows, int box0, int box1) {
+  const uint64_t dims[2] = {(uint64_t)inner, (uint64_t)rows};
+  const uint64_t strides[1] = {(uint64_t)inner * 2};
+  const uint32_t box[2] = {(uint32_t)box0, (uint32_t)box1};
+  return make_map(m, base, 2, dims, strides, box);
+}
+
+}  // namespace
+
+bool proj_tc_supported(const ProjArgs& a) {
+  return a.dtype == ES_BF16 && a.C == 128 && a.Dq == 2 * a.C && a.Cv == a.C && encode_fn() != nullptr;
+}
+
+es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, void* q, void* k, void* v,
+                             cudaStream_t st) {
+  const int M = (a.L + 1) * (a.L + 1);
+  CUtensorMap mh, mw;
+  if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64))
+    return fail(ES_CUDA_ERROR, "proj_fwd_tc: tensor map encode failed");
+  const size_t smem = 65536 + 1024 + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(proj_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  TcP p{a.N, M, a.C, a.L};
+  dim3 grid((a.N + 127) / 128, M, 5);
+  proj_fwd_tc_kernel<<<grid, 128, smem, st>>>(mh, mw, p, (bf16*)q, (bf16*)k, (bf16*)v);
+  return cuda_status(cudaGetLastError(), "proj_fwd_tc_kernel");
+}
+
+es_status proj_bwd_tc_launch(const ProjArgs& a, const void* h, const void* W, const void* dq, const void* dk,
+                             const void* dv, void* dh, float* dW, cudaStream_t st) {
+  const int M = (a.L + 1) * (a.L + 1);
+  TcP p{a.N, M, a.C, a.L};
+  CUtensorMap mdq, mdk, mdv, mwk;
+  if (!map3(&mdq, dq, 2 * a.C, M, a.N, 64, 1, 128) || !map3(&mdk, dk, 2 * a.C, M, a.N, 64, 1, 128) ||
+      !map3(&mdv, dv, a.C, M, a.N, 64, 1, 128) || !map2(&mwk, W, 5 * a.C, (a.L + 1) * a.C, 64, 128))
+    return fail(ES_CUDA_ERROR, "proj_bwd_tc: tensor map encode failed");
+  {
+    const size_t smem = kDhStages * 32768 + 1024 + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(proj_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    dim3 grid((a.N + 127) / 128, M);
+    proj_dh_tc_kernel<<<grid, 128, smem, st>>>(mdq, mdk, mdv, mwk, p, (bf16*)dh);
+    es_status s = cuda_status(cudaGetLastError(), "proj_dh_tc_kernel");
+    if (s != ES_OK) return s;
+  }
+  if (!dW) return ES_OK;
+  cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(a.L + 1) * a.C * 5 * a.C, st);
+  static bool attr_dw = false;
+  if (!attr_dw) {
+    cudaFuncSetAttribute(proj_dw_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_dw = true;
+  }
+  for (int l = 0; l <= a.L; ++l) {
+    const int nb = l == 0 ? 64 : 16;
+    const int R = (2 * l + 1) * nb;
+    CUtensorMap mh, gq, gk, gv;
+    if (!map3(&mh, h, a.C, M, a.N, 64, 2 * l + 1, nb) || !map3(&gq, dq, 2 * a.C, M, a.N, 64, 2 * l + 1, nb) ||
+        !map3(&gk, dk, 2 * a.C, M, a.N, 64, 2 * l + 1, nb) || !map3(&gv, dv, a.C, M, a.N, 64, 2 * l + 1, nb))
+      return fail(ES_CUDA_ERROR, "proj_dw_tc: tensor map encode failed");
+    const size_t smem = (size_t)kDwStages * 4 * R * 128 + 1024 + 1024;
+    int splits = 60;
+    int per = (a.N + splits - 1) / splits;
+    per = ((per + nb - 1) / nb) * nb;
+    splits = (a.N + per - 1) / per;
+    dim3 grid(splits, 5);
+    proj_dw_tc_kernel<<<grid, 128, smem, st>>>(mh, gq, gk, gv, p, l, nb, per, dW);
+    es_status s = cuda_status(cudaGetLastError(), "proj_dw_tc_kernel");
+    if (s != ES_OK) return s;
+  }
+  return ES_OK;
+}
+
+}  // namespace es
