@@ -1,0 +1,235 @@
+// Backward of the fused equivariant attention; see attention_common.cuh.
+#include "attention_common.cuh"
+
+namespace es {
+namespace {
+
+// ------------------------------------------------------------------ backward
+// Delta_i^h = sum_{rows, head channels} dout * out.  C/2 threads per atom,
+// two channels each (same head), shuffle-reduced over the C_h/2 lanes of a head.
+template <typename T>
+__global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, int H, const T* __restrict__ out,
+                                                         const T* __restrict__ dout, float* __restrict__ delta) {
+  const int tpa = C / 2;
+  const int i = blockIdx.x * (blockDim.x / tpa) + threadIdx.x / tpa;
+  const int t = threadIdx.x % tpa;
+  if (i >= N) return;
+  float acc = 0.f;
+  for (int mm = 0; mm < M; ++mm) {
+    float a[2], b[2];
+    ldvec<2>(out + ((size_t)i * M + mm) * C + 2 * t, a);
+    ldvec<2>(dout + ((size_t)i * M + mm) * C + 2 * t, b);
+    acc = fmaf(a[0], b[0], fmaf(a[1], b[1], acc));
+  }
+  const int g = (C / H) / 2;  // threads per head (power of two <= 32)
+  for (int o = g >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (t % g == 0) delta[(size_t)i * H + (2 * t) / (C / H)] = acc;
+}
+
+// Key-centric pass: CTA per key atom j over the transposed relation; yields
+// dk_j, dv_j exclusively (no atomics) and the per-pair-head dscore.
+template <int L, int CPL, bool EAAS, typename T>
+__global__ void __launch_bounds__(256) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+                                                          const T* __restrict__ v, const double* __restrict__ pos,
+                                                          const int* __restrict__ rev_ptr,
+                                                          const int* __restrict__ rev_pair,
+                                                          const float* __restrict__ lse, const T* __restrict__ dout,
+                                                          const float* __restrict__ delta, T* __restrict__ dk,
+                                                          T* __restrict__ dv, float* __restrict__ dsbuf) {
+  using LY = Lay<L>;
+  constexpr int M = LY::M;
+  constexpr int REC = LY::REC;
+  constexpr int BP = LY::BP;
+  extern __shared__ float4 smem4[];
+  float* recs = reinterpret_cast<float*>(smem4);
+
+  const int j = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = (warp * 32 + lane) * CPL;
+  const int Ch = p.C / p.H;
+  const int lph = Ch / CPL;
+  const int head = c0 / Ch;
+  const int Dq = p.Dq;
+
+  float kr[M][2 * CPL], vr[M][CPL], dkr[M][2 * CPL], dvr[M][CPL];
+#pragma unroll
+  for (int mm = 0; mm < M; ++mm) {
+    ldvec<2 * CPL>(k + ((size_t)j * M + mm) * Dq + 2 * c0, kr[mm]);
+    ldvec<CPL>(v + ((size_t)j * M + mm) * p.C + c0, vr[mm]);
+#pragma unroll
+    for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) dvr[mm][c] = 0.f;
+  }
+  const int rs = rev_ptr[j], re = rev_ptr[j + 1];
+  for (int base = rs; base < re; base += BP) {
+    const int nb = min(BP, re - base);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+      const int pr = rev_pair[base + t];
+      const int i = pr / p.K;
+      float* rec = recs + t * REC;
+      pair_prepare<L, EAAS>(p, pos, i, j, rec);
+      rec[LY::OFF_J] = __int_as_float(i);
+      rec[LY::OFF_X] = __int_as_float(pr);
+    }
+    __syncthreads();
+    for (int e = 0; e < nb; ++e) {
+      const float* rec = recs + e * REC;
+      const int i = __float_as_int(rec[LY::OFF_J]);
+      const int pr = __float_as_int(rec[LY::OFF_X]);
+      float qv[M][2 * CPL];
+      float s = 0.f;
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm) {
+        ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qv[mm]);
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[mm][c], s);
+      }
+      for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const float P = expf(s * p.tau - lse[(size_t)i * p.H + head]);
+      const float phi = rec[LY::OFF_PHI];
+      float g[M][CPL], y[M][CPL];
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm) {
+        ldvec<CPL>(dout + ((size_t)i * M + mm) * p.C + c0, g[mm]);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) y[mm][c] = 0.f;
+      }
+      if constexpr (EAAS) {
+        eaas_apply<L, CPL, true>(rec, g, phi, y);
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) y[mm][c] = phi * g[mm][c];
+      }
+      float dp = 0.f;
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          dvr[mm][c] = fmaf(P, y[mm][c], dvr[mm][c]);
+          dp = fmaf(y[mm][c], vr[mm][c], dp);
+        }
+      for (int o = lph >> 1; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
+      const float ds = P * (dp - delta[(size_t)i * p.H + head]);
+      const float tds = p.tau * ds;
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+      if ((lane % lph) == 0) dsbuf[(size_t)pr * p.H + head] = ds;
+    }
+  }
+#pragma unroll
+  for (int mm = 0; mm < M; ++mm) {
+    stvec<2 * CPL>(dk + ((size_t)j * M + mm) * Dq + 2 * c0, dkr[mm]);
+    stvec<CPL>(dv + ((size_t)j * M + mm) * p.C + c0, dvr[mm]);
+  }
+}
+
+// Query-centric pass: dq_i = tau * sum_slot ds[i,slot,h] k_j.  Each thread
+// owns 8 consecutive q-channels of one (l,m) row (one head), loads them as
+// one vector per valid neighbour.
+template <typename T>
+__global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, int Dq, float tau,
+                                                          const T* __restrict__ k, const int* __restrict__ nbr,
+                                                          const float* __restrict__ dsbuf, T* __restrict__ dq) {
+  const int i = blockIdx.x;
+  const int dqh = Dq / H;
+  const int n = M * Dq;
+  for (int e0 = threadIdx.x * 8; e0 < n; e0 += blockDim.x * 8) {
+    const int h = (e0 % Dq) / dqh;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < K; ++s) {
+      const int j = __ldg(nbr + (size_t)i * K + s);
+      if (j < 0) continue;
+      const float ds = __ldg(dsbuf + ((size_t)i * K + s) * H + h);
+      float kv[8];
+      ldvec<4>(k + (size_t)j * n + e0, kv);
+      ldvec<4>(k + (size_t)j * n + e0 + 4, kv + 4);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[t] = fmaf(ds, kv[t], acc[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc[t] *= tau;
+    stvec<4>(dq + (size_t)i * n + e0, acc);
+    stvec<4>(dq + (size_t)i * n + e0 + 4, acc + 4);
+  }
+}
+
+
+template <int L, int CPL, bool EAAS, typename T>
+es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
+                  const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
+                  const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, float* dsbuf,
+                  cudaStream_t st) {
+  constexpr int M = Lay<L>::M;
+  {
+    const int apb = 256 / (kp.C / 2);
+    attn_delta_kernel<T><<<(kp.N + apb - 1) / apb, apb * (kp.C / 2), 0, st>>>(kp.N, M, kp.C, kp.H, (const T*)out,
+                                                                              (const T*)dout, delta);
+  }
+  es_status s = cuda_status(cudaGetLastError(), "attn_delta_kernel");
+  if (s != ES_OK) return s;
+  const int threads = kp.C / CPL;
+  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4;
+  auto fn = attn_bwd_kv_kernel<L, CPL, EAAS, T>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fn<<<kp.N, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
+                                  (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf);
+  s = cuda_status(cudaGetLastError(), "attn_bwd_kv_kernel");
+  if (s != ES_OK) return s;
+  {
+    int tq = (M * kp.Dq / 8 + 31) / 32 * 32;
+    if (tq > 1024) tq = 1024;
+    attn_bwd_q_kernel<T><<<kp.N, tq, 0, st>>>(M, kp.K, kp.H, kp.Dq, kp.tau, (const T*)k, nbr, dsbuf, (T*)dq);
+  }
+  return cuda_status(cudaGetLastError(), "attn_bwd_q_kernel");
+}
+
+KParams make_params(const AttnArgs& a) {
+  KParams kp;
+  kp.N = a.N; kp.K = a.K; kp.H = a.H; kp.C = a.C; kp.Dq = a.Dq;
+  kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
+  kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
+  kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];
+  return kp;
+}
+
+template <template <int, int, bool, typename> class Op, typename... Args>
+es_status dispatch(const AttnArgs& a, Args&&... args) {
+  const bool eaas = a.value_mode == ES_VALUE_EAAS;
+  const bool bf = a.dtype == ES_BF16;
+  const int cpl = (a.L <= 2 && a.C % 64 == 0 && (a.C / a.H) % 2 == 0) ? 2 : 1;
+#define ES_CASE(LL, CC)                                                                                  \
+  if (a.L == LL && cpl == CC) {                                                                          \
+    if (eaas) return bf ? Op<LL, CC, true, __nv_bfloat16>::run(args...) : Op<LL, CC, true, float>::run(args...); \
+    return bf ? Op<LL, CC, false, __nv_bfloat16>::run(args...) : Op<LL, CC, false, float>::run(args...);        \
+  }
+  ES_CASE(0, 2) ES_CASE(1, 2) ES_CASE(2, 2) ES_CASE(0, 1) ES_CASE(1, 1) ES_CASE(2, 1) ES_CASE(3, 1) ES_CASE(4, 1)
+#undef ES_CASE
+  return fail(ES_UNSUPPORTED, "attention: no kernel for this (L, C, H)");
+}
+
+template <int L, int CPL, bool EAAS, typename T>
+struct BwdOp {
+  template <typename... A>
+  static es_status run(A... a) { return run_bwd<L, CPL, EAAS, T>(a...); }
+};
+
+}  // namespace
+
+es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                          const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
+                          const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
+                          float* dsbuf, cudaStream_t st) {
+  es_status s = upload_tables_tu();
+  if (s != ES_OK) return s;
+  const KParams kp = make_params(a);
+  if (a.N == 0) return ES_OK;
+  return dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, st);
+}
+
+}  // namespace es

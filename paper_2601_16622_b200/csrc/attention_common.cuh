@@ -1,0 +1,374 @@
+#pragma once
+// Fused on-the-fly equivariant attention with per-pair EAAS (sm_100a) --
+// shared device code (tables, per-pair preparation, EAAS operator).
+//
+// Forward  = stream_aggregate (Alg. 1),
+// backward = stream_aggregate_backward by recomputation,
+// with the north-star value path: for every (i, j) pair the kernel builds in
+// registers/shared memory the relative direction, the SO(3)->SO(2) edge frame
+// R (R r_ij = |r_ij| e_z), the Wigner blocks D^l(R), the radial factors
+// |r|^lf Y_lf0(e_z) and applies the EAAS sparse parity re-index
+// (Def. 1 / Prop. 1) per channel:
+//     x_ij = phi(r_ij) * D^T P(|r_ij|) D v_j      (== sum over CG paths of v_j (x) R^lf(r_ij))
+// No per-edge tensor reaches HBM: the per-pair operator lives in shared
+// memory for one neighbour batch, the softmax state (mu, z, A) in registers.
+//
+// Work decomposition: one CTA per target atom (forward / dq) or per key atom
+// (dk, dv).  The CTA's WQ = C / (32*CPL) warps split the value channels
+// (CPL channels per lane, whole heads per warp), so scores reduce inside a
+// warp with shuffles.  Each neighbour batch of BP pairs is prepared by BP
+// threads in parallel (one pair per thread: frame, D^l fit, reindex
+// polynomials), then every warp streams the batch for its channels.
+#include <cuda_bf16.h>
+
+
+#include "es_internal.h"
+
+namespace es {
+namespace {
+
+// ------------------------------------------------------------------ tables
+struct DevTables {
+  float fit_pts[9][3];
+  float ainv[kMaxL + 1][81];
+  float shnorm[kMaxL + 1][kMaxL + 1];
+  float cab[kMaxL + 1][85][2][kMaxL + 1];  // [L][canonical entry][a|b][lf]
+};
+static __constant__ DevTables c_tab;
+
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int canon_entry(int lo, int li, int m) {
+  int s = 0;
+  for (int a = 0; a <= kMaxL; ++a)
+    for (int b = 0; b <= kMaxL; ++b) {
+      const int mm = cmin(a, b);
+      if (a == lo && b == li) return s + m + mm;
+      s += 2 * mm + 1;
+    }
+  return -1;
+}
+
+template <int L>
+struct Lay {
+  static constexpr int M = (L + 1) * (L + 1);
+  __host__ __device__ static constexpr int doff(int l) {
+    int s = 0;
+    for (int a = 1; a < l; ++a) s += (2 * a + 1) * (2 * a + 1);
+    return s;
+  }
+  __host__ __device__ static constexpr int eoff(int lo, int li) {
+    int s = 0;
+    for (int a = 0; a <= L; ++a)
+      for (int b = 0; b <= L; ++b) {
+        if (a == lo && b == li) return s;
+        s += 2 * cmin(a, b) + 1;
+      }
+    return s;
+  }
+  static constexpr int ND = doff(L + 1);
+  static constexpr int NE = eoff(L + 1, 0);
+  static constexpr int OFF_AB = ND;
+  static constexpr int OFF_PHI = ND + 2 * NE;
+  static constexpr int OFF_J = OFF_PHI + 1;
+  static constexpr int OFF_X = OFF_PHI + 2;  // spare (query slot in backward)
+  static constexpr int REC = ((OFF_PHI + 4) + 3) / 4 * 4;
+  static constexpr int BP = (L <= 2) ? 64 : 32;  // pairs per batch
+};
+
+inline es_status upload_tables_tu() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && done[dev]) return ES_OK;
+  const HostTables& h = host_tables();
+  DevTables t;
+  for (int k = 0; k < 9; ++k)
+    for (int a = 0; a < 3; ++a) t.fit_pts[k][a] = (float)h.fit_pts[k][a];
+  for (int l = 0; l <= kMaxL; ++l) {
+    for (int i = 0; i < 81; ++i) t.ainv[l][i] = (float)h.ainv[l][i];
+    for (int mu = 0; mu <= kMaxL; ++mu) t.shnorm[l][mu] = (float)h.shnorm[l][mu];
+  }
+  for (int L = 0; L <= kMaxL; ++L)
+    for (int e = 0; e < 85; ++e)
+      for (int f = 0; f <= kMaxL; ++f) {
+        t.cab[L][e][0][f] = (float)h.ca[L][e][f];
+        t.cab[L][e][1][f] = (float)h.cb[L][e][f];
+      }
+  cudaError_t e = cudaMemcpyToSymbol(c_tab, &t, sizeof(t));
+  if (e != cudaSuccess) return cuda_status(e, "upload_tables");
+  if (dev < 64) done[dev] = true;
+  return ES_OK;
+}
+
+// ------------------------------------------------------------------ helpers
+template <typename T>
+__device__ __forceinline__ float ldf(const T* p);
+template <>
+__device__ __forceinline__ float ldf<float>(const float* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
+
+// Load n (1, 2, 4) consecutive elements as floats.
+template <int n, typename T>
+__device__ __forceinline__ void ldvec(const T* p, float* o) {
+  if constexpr (sizeof(T) == 4) {
+    if constexpr (n == 4) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+      o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    } else if constexpr (n == 2) {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+      o[0] = v.x; o[1] = v.y;
+    } else {
+#pragma unroll
+      for (int a = 0; a < n; ++a) o[a] = ldf(p + a);
+    }
+  } else {
+    if constexpr (n == 4) {
+      const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+      const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+      o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
+    } else if constexpr (n == 2) {
+      const unsigned u = __ldg(reinterpret_cast<const unsigned*>(p));
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+      o[0] = f.x; o[1] = f.y;
+    } else {
+#pragma unroll
+      for (int a = 0; a < n; ++a) o[a] = ldf(p + a);
+    }
+  }
+}
+
+template <int n, typename T>
+__device__ __forceinline__ void stvec(T* p, const float* v) {
+  if constexpr (sizeof(T) == 4) {
+    if constexpr (n == 4) *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    else if constexpr (n == 2) *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    else {
+#pragma unroll
+      for (int a = 0; a < n; ++a) p[a] = v[a];
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < n; ++a) p[a] = __float2bfloat16_rn(v[a]);
+  }
+}
+
+// Real solid harmonics of one degree l at a point (harmonics.hpp:36-81
+// recursion; orthonormal, (-1)^m on positive m).
+template <int l>
+__device__ __forceinline__ void sh_degree(float x, float y, float z, float* out) {
+  if constexpr (l == 0) {
+    out[0] = 0.28209479177387814f;
+  } else {
+    const float r2 = x * x + y * y + z * z;
+    float a = 1.f, b = 0.f;
+#pragma unroll
+    for (int mu = 0; mu <= l; ++mu) {
+      if (mu > 0) {
+        const float an = a * x - b * y, bn = a * y + b * x;
+        a = an; b = bn;
+      }
+      float p2 = 0.f, pc = 1.f;
+#pragma unroll
+      for (int k = 2 * mu - 1; k > 1; k -= 2) pc *= (float)k;
+#pragma unroll
+      for (int ll = mu + 1; ll <= l; ++ll) {
+        const float pn = ((2 * ll - 1) * z * pc - (ll + mu - 1) * r2 * p2) * (1.f / (float)(ll - mu));
+        p2 = pc; pc = pn;
+      }
+      const float nrm = c_tab.shnorm[l][mu] * pc;
+      if (mu == 0) out[l] = nrm;
+      else {
+        out[l + mu] = ((mu & 1) ? -nrm : nrm) * a;
+        out[l - mu] = nrm * b;
+      }
+    }
+  }
+}
+
+// D^l(R) = B A^-1 with B[:,k] = Y^l(R p_k): written row-major into rec.
+template <int l>
+__device__ __forceinline__ void fit_wigner(const float (&R)[9], float* rec) {
+  constexpr int d = 2 * l + 1;
+  float acc[d * d];
+#pragma unroll
+  for (int t = 0; t < d * d; ++t) acc[t] = 0.f;
+#pragma unroll
+  for (int k = 0; k < d; ++k) {
+    const float px = c_tab.fit_pts[k][0], py = c_tab.fit_pts[k][1], pz = c_tab.fit_pts[k][2];
+    const float qx = R[0] * px + R[1] * py + R[2] * pz;
+    const float qy = R[3] * px + R[4] * py + R[5] * pz;
+    const float qz = R[6] * px + R[7] * py + R[8] * pz;
+    float y[d];
+    sh_degree<l>(qx, qy, qz, y);
+#pragma unroll
+    for (int m = 0; m < d; ++m)
+#pragma unroll
+      for (int mp = 0; mp < d; ++mp) acc[m * d + mp] = fmaf(y[m], c_tab.ainv[l][k * d + mp], acc[m * d + mp]);
+  }
+#pragma unroll
+  for (int t = 0; t < d * d; ++t) rec[t] = acc[t];
+}
+
+template <int L, int l>
+__device__ __forceinline__ void fit_all(const float (&R)[9], float* rec) {
+  if constexpr (l <= L) {
+    if constexpr (l == 1) {
+      // D^1 = Pi R Pi^T with Y^1 = c (y, z, -x): idx (1,2,0), sign (+,+,-)
+      const int idx[3] = {1, 2, 0};
+      const float sg[3] = {1.f, 1.f, -1.f};
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) rec[Lay<L>::doff(1) + a * 3 + b] = sg[a] * sg[b] * R[idx[a] * 3 + idx[b]];
+    } else {
+      fit_wigner<l>(R, rec + Lay<L>::doff(l));
+    }
+    fit_all<L, l + 1>(R, rec);
+  }
+}
+
+struct KParams {
+  int N, K, H, C, Dq;
+  int phi_mode, periodic;
+  float tau, r_cut, inv_rcut;
+  double bx, by, bz;
+};
+
+// Per-pair preparation (one thread): r_ij = pos_j - pos_i (double difference,
+// minimum image if periodic), phi, and for EAAS the frame / D^l / reindex
+// coefficients.  Gauge: R = R' P with P = diag(1,-1,-1) when u_z < 0 so that
+// the closed-form frame R' (rows e1, e2, u') is used only for u'_z >= 0 --
+// branch-stable; any gauge gives the same composite.
+template <int L, bool EAAS>
+__device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, int i, int j, float* rec) {
+  double dx = pos[3 * j] - pos[3 * i], dy = pos[3 * j + 1] - pos[3 * i + 1], dz = pos[3 * j + 2] - pos[3 * i + 2];
+  if (p.periodic) {
+    dx -= p.bx * rint(dx / p.bx);
+    dy -= p.by * rint(dy / p.by);
+    dz -= p.bz * rint(dz / p.bz);
+  }
+  const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+  const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+  float phi = 1.f;
+  if (p.phi_mode == 0) phi = rn < p.r_cut ? 0.5f * (cospif(rn * p.inv_rcut) + 1.f) : 0.f;
+  rec[Lay<L>::OFF_PHI] = phi;
+  rec[Lay<L>::OFF_J] = __int_as_float(j);
+  if constexpr (EAAS) {
+    float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+    if (rn > 1e-8f) {
+      const float inv = 1.f / rn;
+      const float ux = rx * inv;
+      const bool flip = rz < 0.f;
+      const float uy = flip ? -ry * inv : ry * inv;
+      const float uz = flip ? -rz * inv : rz * inv;
+      const float f = 1.f / (1.f + uz);
+      R[0] = 1.f - ux * ux * f; R[1] = -ux * uy * f; R[2] = -ux;
+      R[3] = -ux * uy * f;      R[4] = 1.f - uy * uy * f; R[5] = -uy;
+      R[6] = ux;                R[7] = uy;                R[8] = uz;
+      if (flip) {  // R' P: negate columns 1 and 2
+        R[1] = -R[1]; R[2] = -R[2]; R[4] = -R[4]; R[5] = -R[5]; R[7] = -R[7]; R[8] = -R[8];
+      }
+    }
+    fit_all<L, 1>(R, rec);
+    float rp[L + 1];
+    rp[0] = 1.f;
+#pragma unroll
+    for (int f = 1; f <= L; ++f) rp[f] = rp[f - 1] * rn;
+#pragma unroll
+    for (int lo = 0; lo <= L; ++lo)
+#pragma unroll
+      for (int li = 0; li <= L; ++li) {
+        const int mm = cmin(lo, li);
+#pragma unroll
+        for (int m = -mm; m <= mm; ++m) {
+          const int ce = canon_entry(lo, li, m);
+          const int e = Lay<L>::eoff(lo, li) + m + mm;
+          float a = 0.f, b = 0.f;
+#pragma unroll
+          for (int f = 0; f <= L; ++f) {
+            a = fmaf(c_tab.cab[L][ce][0][f], rp[f], a);
+            b = fmaf(c_tab.cab[L][ce][1][f], rp[f], b);
+          }
+          rec[Lay<L>::OFF_AB + 2 * e] = a;
+          rec[Lay<L>::OFF_AB + 2 * e + 1] = b;
+        }
+      }
+  }
+}
+
+// x += s * (D^T P D) v  per channel (EAAS forward value operator), or the
+// adjoint y += s * (D^T P^T D) g when ADJ.  v: [M][CPL] registers.
+template <int L, int CPL, bool ADJ>
+__device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
+                                           float (&acc)[Lay<L>::M][CPL]) {
+  constexpr int M = Lay<L>::M;
+  float vt[M][CPL];
+  // align: vt^l = D^l v^l
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) vt[0][c] = v[0][c];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    const float* D = rec + Lay<L>::doff(l);
+    const int d = 2 * l + 1;
+#pragma unroll
+    for (int m = 0; m < d; ++m)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        float t = 0.f;
+#pragma unroll
+        for (int mp = 0; mp < d; ++mp) t = fmaf(D[m * d + mp], v[l * l + mp][c], t);
+        vt[l * l + m][c] = t;
+      }
+  }
+  // sparse re-index in the aligned frame (forward P or adjoint P^T)
+  float w[M][CPL];
+#pragma unroll
+  for (int t = 0; t < M; ++t)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) w[t][c] = 0.f;
+#pragma unroll
+  for (int lo = 0; lo <= L; ++lo)
+#pragma unroll
+    for (int li = 0; li <= L; ++li) {
+      const int mm = cmin(lo, li);
+#pragma unroll
+      for (int m = -mm; m <= mm; ++m) {
+        const int e = Lay<L>::eoff(lo, li) + m + mm;
+        const float a = rec[Lay<L>::OFF_AB + 2 * e];
+        const float b = rec[Lay<L>::OFF_AB + 2 * e + 1];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          if constexpr (!ADJ) {
+            w[lo * lo + lo + m][c] = fmaf(a, vt[li * li + li + m][c], w[lo * lo + lo + m][c]);
+            if (m != 0) w[lo * lo + lo + m][c] = fmaf(b, vt[li * li + li - m][c], w[lo * lo + lo + m][c]);
+          } else {
+            w[li * li + li + m][c] = fmaf(a, vt[lo * lo + lo + m][c], w[li * li + li + m][c]);
+            if (m != 0) w[li * li + li - m][c] = fmaf(b, vt[lo * lo + lo + m][c], w[li * li + li - m][c]);
+          }
+        }
+      }
+    }
+  // un-align and accumulate: acc^l += s * D^l^T w^l
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[0][c] = fmaf(s, w[0][c], acc[0][c]);
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    const float* D = rec + Lay<L>::doff(l);
+    const int d = 2 * l + 1;
+#pragma unroll
+    for (int m = 0; m < d; ++m)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        float t = 0.f;
+#pragma unroll
+        for (int mp = 0; mp < d; ++mp) t = fmaf(D[mp * d + m], w[l * l + mp][c], t);
+        acc[l * l + m][c] = fmaf(s, t, acc[l * l + m][c]);
+      }
+  }
+}
+
+}  // namespace
+}  // namespace es

@@ -1,0 +1,161 @@
+// Forward of the fused equivariant attention; see attention_common.cuh.
+#include "attention_common.cuh"
+
+namespace es {
+namespace {
+
+// ------------------------------------------------------------------ forward
+template <int L, int CPL, bool EAAS, typename T>
+__global__ void __launch_bounds__(256) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+                                                       const T* __restrict__ v, const double* __restrict__ pos,
+                                                       const int* __restrict__ nbr, T* __restrict__ out,
+                                                       float* __restrict__ lse) {
+  using LY = Lay<L>;
+  constexpr int M = LY::M;
+  constexpr int REC = LY::REC;
+  constexpr int BP = LY::BP;
+  extern __shared__ float4 smem4[];
+  float* recs = reinterpret_cast<float*>(smem4);
+  float* sc = recs + BP * REC;  // [BP][H]
+
+  const int i = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = (warp * 32 + lane) * CPL;  // first value channel of this lane
+  const int Ch = p.C / p.H;                 // value channels per head
+  const int lph = Ch / CPL;                 // lanes per head
+  const int head = c0 / Ch;
+  const int Dq = p.Dq;
+
+  float qr[M][2 * CPL];
+#pragma unroll
+  for (int mm = 0; mm < M; ++mm) ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qr[mm]);
+  float A[M][CPL];
+#pragma unroll
+  for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) A[mm][c] = 0.f;
+  float mu = -INFINITY, z = 0.f;
+
+  for (int base = 0; base < p.K; base += BP) {
+    const int nb = min(BP, p.K - base);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+      const int j = nbr[(size_t)i * p.K + base + t];
+      float* rec = recs + t * REC;
+      if (j >= 0) pair_prepare<L, EAAS>(p, pos, i, j, rec);
+      else rec[LY::OFF_J] = __int_as_float(-1);
+    }
+    __syncthreads();
+    // phase A: scores of this warp's heads for the whole batch
+    for (int e = 0; e < nb; ++e) {
+      const int j = __float_as_int(recs[e * REC + LY::OFF_J]);
+      if (j < 0) continue;
+      float s = 0.f;
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm) {
+        float kv[2 * CPL];
+        ldvec<2 * CPL>(k + ((size_t)j * M + mm) * Dq + 2 * c0, kv);
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qr[mm][c], kv[c], s);
+      }
+      for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if ((lane % lph) == 0) sc[e * p.H + head] = s * p.tau;
+    }
+    __syncwarp();
+    float bm = -INFINITY;
+    for (int e = 0; e < nb; ++e)
+      if (__float_as_int(recs[e * REC + LY::OFF_J]) >= 0) bm = fmaxf(bm, sc[e * p.H + head]);
+    if (bm == -INFINITY) continue;
+    const float mu2 = fmaxf(mu, bm);
+    const float scale = __expf(mu - mu2);  // mu = -inf -> 0
+    z *= scale;
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) A[mm][c] *= scale;
+    mu = mu2;
+    // phase B: values
+    for (int e = 0; e < nb; ++e) {
+      const float* rec = recs + e * REC;
+      const int j = __float_as_int(rec[LY::OFF_J]);
+      if (j < 0) continue;
+      const float pr = expf(sc[e * p.H + head] - mu);
+      z += pr;
+      const float s = pr * rec[LY::OFF_PHI];
+      float vv[M][CPL];
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm) ldvec<CPL>(v + ((size_t)j * M + mm) * p.C + c0, vv[mm]);
+      if constexpr (EAAS) {
+        eaas_apply<L, CPL, false>(rec, vv, s, A);
+      } else {
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) A[mm][c] = fmaf(s, vv[mm][c], A[mm][c]);
+      }
+    }
+  }
+  const float inv = z > 0.f ? 1.f / z : 0.f;
+#pragma unroll
+  for (int mm = 0; mm < M; ++mm) {
+    float o[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) o[c] = A[mm][c] * inv;
+    stvec<CPL>(out + ((size_t)i * M + mm) * p.C + c0, o);
+  }
+  if ((lane % lph) == 0) lse[(size_t)i * p.H + head] = z > 0.f ? mu + logf(z) : -INFINITY;
+}
+
+
+template <int L, int CPL, bool EAAS, typename T>
+es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
+                  const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
+  const int threads = kp.C / CPL;
+  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)Lay<L>::BP * kp.H * 4;
+  auto fn = attn_fwd_kernel<L, CPL, EAAS, T>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  fn<<<kp.N, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
+  return cuda_status(cudaGetLastError(), "attn_fwd_kernel");
+}
+
+KParams make_params(const AttnArgs& a) {
+  KParams kp;
+  kp.N = a.N; kp.K = a.K; kp.H = a.H; kp.C = a.C; kp.Dq = a.Dq;
+  kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
+  kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
+  kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];
+  return kp;
+}
+
+template <template <int, int, bool, typename> class Op, typename... Args>
+es_status dispatch(const AttnArgs& a, Args&&... args) {
+  const bool eaas = a.value_mode == ES_VALUE_EAAS;
+  const bool bf = a.dtype == ES_BF16;
+  const int cpl = (a.L <= 2 && a.C % 64 == 0 && (a.C / a.H) % 2 == 0) ? 2 : 1;
+#define ES_CASE(LL, CC)                                                                                  \
+  if (a.L == LL && cpl == CC) {                                                                          \
+    if (eaas) return bf ? Op<LL, CC, true, __nv_bfloat16>::run(args...) : Op<LL, CC, true, float>::run(args...); \
+    return bf ? Op<LL, CC, false, __nv_bfloat16>::run(args...) : Op<LL, CC, false, float>::run(args...);        \
+  }
+  ES_CASE(0, 2) ES_CASE(1, 2) ES_CASE(2, 2) ES_CASE(0, 1) ES_CASE(1, 1) ES_CASE(2, 1) ES_CASE(3, 1) ES_CASE(4, 1)
+#undef ES_CASE
+  return fail(ES_UNSUPPORTED, "attention: no kernel for this (L, C, H)");
+}
+
+template <int L, int CPL, bool EAAS, typename T>
+struct FwdOp {
+  template <typename... A>
+  static es_status run(A... a) { return run_fwd<L, CPL, EAAS, T>(a...); }
+};
+}  // namespace
+
+es_status attn_fwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                          const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
+  es_status s = upload_tables_tu();
+  if (s != ES_OK) return s;
+  const KParams kp = make_params(a);
+  if (a.N == 0) return ES_OK;
+  return dispatch<FwdOp>(a, kp, q, k, v, pos, nbr, out, lse, st);
+}
+
+}  // namespace es

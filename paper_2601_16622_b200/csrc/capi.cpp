@@ -45,7 +45,7 @@ es_status check_attn(const es_attn_desc* d) {
     return fail(ES_INVALID_ARGUMENT, "attn: periodic box must be positive");
   const int ch = d->C / d->H;
   if (d->C % 32 != 0 || d->C > 256) return fail(ES_UNSUPPORTED, "attn: C must be a multiple of 32 and <= 256");
-  if (ch > 32 || (32 % ch != 0 && ch % 32 != 0)) return fail(ES_UNSUPPORTED, "attn: C/H must divide 32");
+  if (ch > 32 || 32 % ch != 0 || ch < 4) return fail(ES_UNSUPPORTED, "attn: C/H must be 4, 8, 16 or 32");
   if (d->H > 64) return fail(ES_UNSUPPORTED, "attn: H <= 64");
   return ES_OK;
 }

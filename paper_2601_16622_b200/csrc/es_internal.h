@@ -51,7 +51,7 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
                           const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
                           float* dsbuf, cudaStream_t st);
-es_status upload_tables();
+
 
 struct NbrArgs {
   int N, K, nseg, periodic;
