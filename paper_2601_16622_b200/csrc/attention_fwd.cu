@@ -1,4 +1,6 @@
 // Forward of the fused equivariant attention; see attention_common.cuh.
+#include <cstdlib>
+
 #include "attention_common.cuh"
 
 namespace es {
@@ -155,6 +157,12 @@ es_status attn_fwd_launch(const AttnArgs& a, const void* q, const void* k, const
   if (s != ES_OK) return s;
   const KParams kp = make_params(a);
   if (a.N == 0) return ES_OK;
+  static int force_simt = -1;
+  if (force_simt < 0) {
+    const char* e = getenv("ES_ATTN_SIMT");
+    force_simt = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!force_simt && attn_tc_supported(a)) return attn_fwd_tc_launch(a, q, k, v, pos, nbr, out, lse, st);
   return dispatch<FwdOp>(a, kp, q, k, v, pos, nbr, out, lse, st);
 }
 

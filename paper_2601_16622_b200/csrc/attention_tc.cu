@@ -1,0 +1,510 @@
+// Tensor-core (tcgen05 / TMEM / TMA) fused equivariant attention, forward,
+// bf16 storage, L = 2, C = 128, H = 8 (C_h = 16, d_k = 288) -- the shape of
+// BASELINE configs 2, 3 and 5.
+//
+// Formulation (exact; same map as the per-pair EAAS kernel, Prop. 1):
+//   x_ij = phi_ij sum_f Y^f(r_ij) G_f v_j,   G_f[o, i'] = C^{o}_{i', f}
+// (the CG coupling of v_j with the solid harmonic basis function f, summed
+// over the path set).  Per head h, with P_ij = exp(tau s_ij - lse_i):
+//   out_i[(o,c)] = sum_{(f,j)} Wt[i,(f,j)] Vg[(f,j),(o,c)]
+//   Wt[i,(f,j)]  = P_ij phi_ij Y^f(r_ij)          (9 scalars per pair: the only per-pair work)
+//   Vg[(f,j),(o,c)] = sum_i' G_f[o,i'] v_j[i',c]   (per-key source coupling, 137 non-zeros)
+// so both contractions run on the tensor cores:
+//   S  = Q_h K_h^T            M=128 queries, N=16 keys,  K=288   (TMA, 64B swizzle)
+//   O += Wt . Vg^T            M=128 queries, N=144 (o,c), K=144 (f,j)   (no-swizzle core matrices)
+// A CTA owns a tile of 128 consecutive query atoms; key chunks of 16 atoms
+// are the non-empty entries of the tile-skip mask.  Softmax in two passes
+// (statistics, then exact normalised P) so the TMEM accumulator never needs
+// rescaling.  Invalid (non-neighbour) pairs get Wt = 0; pair validity comes
+// from the neighbour index itself (never re-tested in fp32).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cmath>
+
+#include <cub/cub.cuh>
+
+#include "es_internal.h"
+#include "umma.cuh"
+
+namespace es {
+
+namespace {
+
+using bf16 = __nv_bfloat16;
+
+constexpr int TQ = 128;      // queries per tile (MMA M)
+constexpr int KC = 16;       // keys per chunk (S MMA N)
+constexpr int HD = 16;       // value channels per head
+constexpr int DH = 32;       // q/k channels per head per (l,m) row
+constexpr int MM = 9;        // (L+1)^2, L = 2
+constexpr int KV = MM * KC;  // 144: value MMA K  ((f, j))
+constexpr int NV = MM * HD;  // 144: value MMA N  ((o, c))
+constexpr int KMAX = 64;     // neighbour slots per atom held in shared memory
+
+// shared memory map (bytes)
+constexpr int SM_Q = 0;                                // 9 x [128 x 32] bf16, SW64     73728
+constexpr int SM_K = SM_Q + MM * TQ * DH * 2;          // 2 x 9 x [16 x 32] bf16, SW64  18432
+constexpr int SM_VST = SM_K + 2 * MM * KC * DH * 2;    // 2 x [16 keys][9][16] bf16      9216
+constexpr int SM_VT = SM_VST + 2 * KC * MM * HD * 2;   // [9][16 c][16 keys] bf16        4608
+constexpr int SM_WT = SM_VT + MM * HD * KC * 2;        // [128 x 144] core-matrix        36864
+constexpr int SM_VG = SM_WT + TQ * KV * 2;             // [144 x 144] core-matrix        41472
+constexpr int SM_NB = SM_VG + NV * KV * 2;             // [128][64] int32               32768
+constexpr int SM_BAR = SM_NB + TQ * KMAX * 4;
+constexpr int SM_TOTAL = SM_BAR + 128;
+
+struct TcTab {
+  float ycoef[4];        // Y0, c1, c2, c20
+  unsigned char ent_i[160];
+  float ent_c[160];
+  int ofs[MM * MM + 1];  // (o, f) -> entry range
+};
+__constant__ TcTab c_tc;
+
+struct TcArgs {
+  int N, K;
+  float tau, r_cut, inv_rcut;
+  int phi_mode, periodic;
+  double bx, by, bz;
+};
+
+__device__ __forceinline__ void solid_l2(float x, float y, float z, float* Y) {
+  const float r2 = x * x + y * y + z * z;
+  const float c1 = c_tc.ycoef[1], c2 = c_tc.ycoef[2], c20 = c_tc.ycoef[3];
+  Y[0] = c_tc.ycoef[0];
+  Y[1] = c1 * y; Y[2] = c1 * z; Y[3] = -c1 * x;
+  Y[4] = c2 * x * y; Y[5] = c2 * y * z; Y[6] = c20 * (1.5f * z * z - 0.5f * r2);
+  Y[7] = -c2 * x * z; Y[8] = 0.5f * c2 * (x * x - y * y);
+}
+
+// no-swizzle K-major core-matrix layout: element (r, k) of an R x KV operand
+__device__ __forceinline__ uint32_t cm_off(int r, int k) {
+  return (uint32_t)((((r >> 3) * (KV / 8) + (k >> 3)) << 7) + ((r & 7) << 4) + ((k & 7) << 1));
+}
+
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  uint4 u;
+  __nv_bfloat162 t;
+  t = __floats2bfloat162_rn(v[0], v[1]); u.x = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(v[2], v[3]); u.y = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(v[4], v[5]); u.z = *reinterpret_cast<uint32_t*>(&t);
+  t = __floats2bfloat162_rn(v[6], v[7]); u.w = *reinterpret_cast<uint32_t*>(&t);
+  return u;
+}
+
+__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mq,
+                                                             const __grid_constant__ CUtensorMap mk,
+                                                             const __grid_constant__ CUtensorMap mv, TcArgs a,
+                                                             const double* __restrict__ pos,
+                                                             const int* __restrict__ nbr,
+                                                             const int* __restrict__ cptr,
+                                                             const int* __restrict__ clist, bf16* __restrict__ out,
+                                                             float* __restrict__ lse) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sm + SM_BAR);
+  uint64_t* bar_ld = bar_q + 1;  // [2]
+  uint64_t* bar_s = bar_q + 3;
+  uint64_t* bar_v = bar_q + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_q + 5);
+  int* nbs = reinterpret_cast<int*>(sm + SM_NB);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q0 = blockIdx.x * TQ;
+  const int qi = q0 + tid;
+  const bool qvalid = qi < a.N;
+  const int c_begin = cptr[blockIdx.x], c_end = cptr[blockIdx.x + 1];
+
+  if (tid == 0) {
+    umma::prefetch_tmap(&mq);
+    umma::prefetch_tmap(&mk);
+    umma::prefetch_tmap(&mv);
+    umma::mbar_init(bar_q, 1);
+    umma::mbar_init(&bar_ld[0], 1);
+    umma::mbar_init(&bar_ld[1], 1);
+    umma::mbar_init(bar_s, 1);
+    umma::mbar_init(bar_v, 1);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 256);
+  // this query's neighbours, ascending j (the kernel consumes the index, it
+  // never re-tests the cutoff)
+  int nn = 0;
+  int* my = nbs + tid * KMAX;
+  if (qvalid) {
+    for (int s = 0; s < a.K && s < KMAX; ++s) {
+      const int j = nbr[(size_t)qi * a.K + s];
+      if (j < 0) continue;
+      int p = nn++;
+      while (p > 0 && my[p - 1] > j) { my[p] = my[p - 1]; --p; }
+      my[p] = j;
+    }
+  }
+  double pix = 0, piy = 0, piz = 0;
+  if (qvalid) { pix = pos[3 * qi]; piy = pos[3 * qi + 1]; piz = pos[3 * qi + 2]; }
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t t_out = tmem;          // cols [0, 144)
+  const uint32_t t_s = tmem + 192;      // cols [192, 208)
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+
+  constexpr uint32_t idesc_s = umma::idesc_bf16(128, KC, 0, 0);
+  constexpr uint32_t idesc_v = umma::idesc_bf16(128, NV, 0, 0);
+  uint32_t ph_q = 0, ph_ld[2] = {0, 0}, ph_s = 0, ph_v = 0;
+  int ld_use = 0;  // loads issued (buffer = ld_use & 1)
+
+  // geometry of (qi, j): r, phi, Y^f
+  auto pair_geo = [&](int j, float* w) {
+    double dx = pos[3 * j] - pix, dy = pos[3 * j + 1] - piy, dz = pos[3 * j + 2] - piz;
+    if (a.periodic) {
+      dx -= a.bx * rint(dx / a.bx);
+      dy -= a.by * rint(dy / a.by);
+      dz -= a.bz * rint(dz / a.bz);
+    }
+    const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+    const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+    float phi = 1.f;
+    if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
+    solid_l2(rx, ry, rz, w);
+#pragma unroll
+    for (int f = 0; f < MM; ++f) w[f] *= phi;
+  };
+
+  for (int h = 0; h < 8; ++h) {
+    // ---- Q_h tile: 9 boxes of [128 atoms x 32 ch]
+    if (tid == 0) {
+      umma::mbar_arrive_expect_tx(bar_q, MM * TQ * DH * 2);
+      for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(sm + SM_Q + mm * TQ * DH * 2, &mq, bar_q, DH * h, mm, q0);
+    }
+    umma::mbar_wait(bar_q, ph_q);
+    ph_q ^= 1;
+
+    float lse_h = -INFINITY;
+    for (int pass = 0; pass < 2; ++pass) {
+      float mu = -INFINITY, z = 0.f;
+      int ptr = 0;
+      for (int ci = c_begin; ci < c_end; ++ci) {
+        const int k0 = clist[ci] * KC;
+        const int buf = ld_use & 1;
+        // ---- load K_h (and V_h in pass 2) chunk, S MMA
+        if (tid == 0) {
+          uint8_t* kb = sm + SM_K + buf * (MM * KC * DH * 2);
+          const uint32_t bytes = MM * KC * DH * 2 + (pass ? KC * MM * HD * 2 : 0);
+          umma::mbar_arrive_expect_tx(&bar_ld[buf], bytes);
+          for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &bar_ld[buf], DH * h, mm, k0);
+          if (pass) umma::tma_load_3d(sm + SM_VST + buf * (KC * MM * HD * 2), &mv, &bar_ld[buf], HD * h, 0, k0);
+          umma::mbar_wait(&bar_ld[buf], ph_ld[buf]);
+          umma::tc_fence_after();
+          const uint32_t qa = umma::smem_u32(sm + SM_Q), ka = umma::smem_u32(kb);
+#pragma unroll
+          for (int s = 0; s < 2 * MM; ++s) {
+            const int mm = s >> 1, kk = s & 1;
+            umma::mma_f16(t_s, umma::sdesc(qa + mm * TQ * DH * 2 + kk * 32, 16, 512, 4),
+                          umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
+          }
+          umma::mma_commit(bar_s);
+        } else {
+          // keep the per-buffer phase in sync on all threads (only tid 0 waits)
+        }
+        ph_ld[buf] ^= 1;
+        ++ld_use;
+
+        if (pass == 1) {
+          // previous value MMA must be done before Wt / Vg are overwritten
+          if (ci > c_begin) {
+            umma::mbar_wait(bar_v, ph_v);
+            ph_v ^= 1;
+          }
+          // V chunk: wait for its bytes (bar_ld[buf] completed: tid 0 waited; all threads need the data)
+          umma::mbar_wait(&bar_ld[buf], ph_ld[buf] ^ 1);
+          // transpose V stage [key][mm][c] -> Vt [mm][c][key]
+          const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + buf * (KC * MM * HD * 2));
+          bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
+          for (int e = tid; e < KC * MM * HD; e += 128) {
+            const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, c = rem % HD;
+            vt[(mm * HD + c) * KC + key] = vst[e];
+          }
+          __syncthreads();
+          // Vg[(o,c), (f,j)] = sum_i' G_f[o,i'] v_j[i',c]: warp w handles o = w, w+4, w+8
+          {
+            const int c = lane & 15, j0 = (lane >> 4) * 8;
+            for (int o = warp; o < MM; o += 4) {
+              for (int f = 0; f < MM; ++f) {
+                float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int e = c_tc.ofs[o * MM + f]; e < c_tc.ofs[o * MM + f + 1]; ++e) {
+                  const int ip = c_tc.ent_i[e];
+                  const float cf = c_tc.ent_c[e];
+                  const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
+                  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+                  for (int t = 0; t < 4; ++t) {
+                    const float2 fv = __bfloat1622float2(b2[t]);
+                    acc[2 * t] = fmaf(cf, fv.x, acc[2 * t]);
+                    acc[2 * t + 1] = fmaf(cf, fv.y, acc[2 * t + 1]);
+                  }
+                }
+                *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc);
+              }
+            }
+          }
+        }
+        // ---- scores of this chunk
+        umma::mbar_wait(bar_s, ph_s);
+        ph_s ^= 1;
+        umma::tc_fence_after();
+        uint32_t sr[16];
+        umma::tmem_ld16(t_s + lane_base, sr);
+        // valid keys of this query in [k0, k0+16)
+        unsigned vmask = 0;
+        while (ptr < nn && my[ptr] < k0) ++ptr;
+        int p2 = ptr;
+        while (p2 < nn && my[p2] < k0 + KC) { vmask |= 1u << (my[p2] - k0); ++p2; }
+        if (pass == 0) {
+          for (int t = 0; t < KC; ++t)
+            if (vmask >> t & 1) {
+              const float sv = a.tau * __uint_as_float(sr[t]);
+              const float m2 = fmaxf(mu, sv);
+              z = z * __expf(mu - m2) + __expf(sv - m2);
+              mu = m2;
+            }
+          ptr = p2;
+        } else {
+          // Wt row: P phi Y^f for the valid keys, 0 elsewhere; two halves of 8 keys
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float w[MM][8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              const int kk = half * 8 + t;
+              if (vmask >> kk & 1) {
+                float y[MM];
+                pair_geo(k0 + kk, y);
+                const float P = __expf(a.tau * __uint_as_float(sr[kk]) - lse_h);
+#pragma unroll
+                for (int f = 0; f < MM; ++f) w[f][t] = P * y[f];
+              } else {
+#pragma unroll
+                for (int f = 0; f < MM; ++f) w[f][t] = 0.f;
+              }
+            }
+#pragma unroll
+            for (int f = 0; f < MM; ++f)
+              *reinterpret_cast<uint4*>(sm + SM_WT + cm_off(tid, f * KC + half * 8)) = pack8(w[f]);
+          }
+          ptr = p2;
+        }
+        umma::fence_proxy_async();
+        umma::tc_fence_before();
+        __syncthreads();
+        if (pass == 1 && tid == 0) {
+          umma::tc_fence_after();
+          const uint32_t wa = umma::smem_u32(sm + SM_WT), va = umma::smem_u32(sm + SM_VG);
+#pragma unroll
+          for (int s = 0; s < MM; ++s)  // K = 144 = 9 steps of 16 = 2 core columns each
+            umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
+                          umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v,
+                          (ci > c_begin || s > 0) ? 1u : 0u);
+          umma::mma_commit(bar_v);
+        }
+      }
+      if (pass == 0) {
+        lse_h = z > 0.f ? mu + __logf(z) : -INFINITY;
+        if (qvalid) lse[(size_t)qi * 8 + h] = lse_h;
+      }
+    }
+    // ---- epilogue: O_h rows from TMEM
+    const bool any = c_end > c_begin;
+    if (any) {
+      umma::mbar_wait(bar_v, ph_v);
+      ph_v ^= 1;
+      umma::tc_fence_after();
+    }
+#pragma unroll
+    for (int cc = 0; cc < NV / 16; ++cc) {  // 9 x 16 columns = one o row of 16 channels
+      uint32_t r[16];
+      if (any) umma::tmem_ld16(t_out + lane_base + cc * 16, r);
+      float v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) v[t] = (any && lse_h > -INFINITY) ? __uint_as_float(r[t]) : 0.f;
+      if (qvalid) {
+        uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)qi * MM + cc) * 128 + HD * h);
+        dst[0] = pack8(v);
+        dst[1] = pack8(v + 8);
+      }
+    }
+    umma::tc_fence_before();
+    __syncthreads();
+    umma::tc_fence_after();
+  }
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, 256);
+}
+
+// ---------------------------------------------------------------- tile chunk lists
+__global__ void tc_count_kernel(int ntiles, int words, const uint32_t* __restrict__ mask, int* __restrict__ cnt) {
+  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  int c = 0;
+  for (int w = lane; w < words; w += 32) c += __popc(mask[(size_t)t * words + w]);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[t] = c;
+}
+
+__global__ void tc_fill_kernel(int ntiles, int words, const uint32_t* __restrict__ mask, const int* __restrict__ ptr,
+                               int* __restrict__ list) {
+  const int t = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  int base = ptr[t];
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    const uint32_t m = w < words ? mask[(size_t)t * words + w] : 0u;
+    const int c = __popc(m);
+    int incl = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    int pos = base + incl - c;
+    uint32_t mm = m;
+    while (mm) {
+      const int b = __ffs(mm) - 1;
+      list[pos++] = w * 32 + b;
+      mm &= mm - 1;
+    }
+    base += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+bool map3(CUtensorMap* m, const void* base, int inner, int mid, int outer, int b0, int b1, int b2,
+          CUtensorMapSwizzle sw) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t gd[3] = {(cuuint64_t)inner, (cuuint64_t)mid, (cuuint64_t)outer};
+  cuuint64_t gs[2] = {(cuuint64_t)inner * 2, (cuuint64_t)inner * mid * 2};
+  cuuint32_t bd[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
+  cuuint32_t es_[3] = {1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gd, gs, bd, es_,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+es_status upload_tc_tables() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && done[dev]) return ES_OK;
+  TcTab t;
+  t.ycoef[0] = 0.28209479177387814f;
+  t.ycoef[1] = (float)std::sqrt(3.0 / (4.0 * M_PI));
+  t.ycoef[2] = (float)std::sqrt(15.0 / (4.0 * M_PI));
+  t.ycoef[3] = (float)std::sqrt(5.0 / (4.0 * M_PI));
+  // G_f[o, i'] for the path set of L = 2 (every degree <= 2), grouped by (o, f)
+  int n = 0;
+  for (int o = 0; o < MM; ++o)
+    for (int f = 0; f < MM; ++f) {
+      t.ofs[o * MM + f] = n;
+      const int lo = o < 1 ? 0 : (o < 4 ? 1 : 2), mo = o - lo * lo - lo;
+      const int lf = f < 1 ? 0 : (f < 4 ? 1 : 2), mf = f - lf * lf - lf;
+      for (int ip = 0; ip < MM; ++ip) {
+        const int li = ip < 1 ? 0 : (ip < 4 ? 1 : 2), mi = ip - li * li - li;
+        const double c = real_cg(li, mi, lf, mf, lo, mo);
+        if (std::fabs(c) > 1e-12) {
+          if (n >= 160) return fail(ES_CUDA_ERROR, "attn_tc: CG table overflow");
+          t.ent_i[n] = (unsigned char)ip;
+          t.ent_c[n] = (float)c;
+          ++n;
+        }
+      }
+    }
+  t.ofs[MM * MM] = n;
+  const cudaError_t e = cudaMemcpyToSymbol(c_tc, &t, sizeof(t));
+  if (e != cudaSuccess) return cuda_status(e, "attn_tc tables");
+  if (dev < 64) done[dev] = true;
+  return ES_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace
+
+bool attn_tc_supported(const AttnArgs& a) {
+  return a.dtype == ES_BF16 && a.value_mode == ES_VALUE_EAAS && a.L == 2 && a.C == 128 && a.H == 8 &&
+         a.K <= KMAX && encode_fn() != nullptr;
+}
+
+// Scratch (tile mask + chunk lists, O(N/128 * N/512) words) is stream-ordered
+// library-owned memory: cudaMallocAsync / cudaFreeAsync on `st`.
+es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                             const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
+  es_status s = upload_tc_tables();
+  if (s != ES_OK) return s;
+  if (a.N == 0) return ES_OK;
+  const int ntiles = (a.N + TQ - 1) / TQ;
+  const int nkb = (a.N + KC - 1) / KC;
+  const int words = (nkb + 31) / 32;
+  const size_t per_tile = (size_t)(nkb < TQ * KMAX ? nkb : TQ * KMAX);
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, ntiles + 1);
+  const size_t bytes = align256((size_t)ntiles * words * 4) + 2 * align256((size_t)(ntiles + 1) * 4) +
+                       align256((size_t)ntiles * per_tile * 4) + align256(cub_bytes);
+  char* base = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&base, bytes, st);
+  if (e != cudaSuccess) return cuda_status(e, "attn_fwd_tc: scratch");
+  uint32_t* mask = (uint32_t*)base;
+  size_t off = align256((size_t)ntiles * words * 4);
+  int* cnt = (int*)(base + off);
+  off += align256((size_t)(ntiles + 1) * 4);
+  int* cptr = (int*)(base + off);
+  off += align256((size_t)(ntiles + 1) * 4);
+  int* clist = (int*)(base + off);
+  off += align256((size_t)ntiles * per_tile * 4);
+  void* cub_ws = base + off;
+  cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
+  cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
+  s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, mask, st);
+  if (s != ES_OK) return s;
+  tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
+  e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
+  if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
+  tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
+
+  CUtensorMap mq, mk, mv;
+  if (!map3(&mq, q, 256, MM, a.N, DH, 1, TQ, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mk, k, 256, MM, a.N, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mv, v, 128, MM, a.N, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return fail(ES_CUDA_ERROR, "attn_fwd_tc: tensor map encode failed");
+  TcArgs ta;
+  ta.N = a.N; ta.K = a.K; ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
+  ta.phi_mode = a.phi_mode; ta.periodic = a.periodic;
+  ta.bx = a.box[0]; ta.by = a.box[1]; ta.bz = a.box[2];
+  const int smem = SM_TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  attn_fwd_tc_kernel<<<ntiles, 128, smem, st>>>(mq, mk, mv, ta, pos, nbr, cptr, clist, (bf16*)out, lse);
+  s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
+  cudaFreeAsync(base, st);
+  return s;
+}
+
+}  // namespace es

@@ -278,3 +278,30 @@ def test_full_size_properties_config2(es):
     assert torch.isfinite(o12).all()
     cnt = idx.count.cpu().numpy()
     assert 10 < cnt.mean() < 20
+
+
+@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc"])
+def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
+    """The tcgen05 path (bf16, L=2, C=128, H=8) over many 128-query tiles and
+    key chunks: molecule batch, one bulk system, a periodic box."""
+    L, C, H = 2, 128, 8
+    box = None
+    if kind == "batch":
+        b = S.molecule_batch(12, 40, 60, 5)
+        pos, seg = b.pos, b.seg_ptr
+    elif kind == "bulk":
+        pos, seg = S.gen_fcc_system(700, 3.8, 6), None
+    else:
+        b = S.periodic_box(500, 4, 3.8, 7)
+        pos, seg, box = b.pos, None, b.box
+    N = len(pos)
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0, seg_ptr=seg, box=box)
+    h = S.random_features(N, L, C, 8)
+    W = S.random_weights(L, C, 8)
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in po.project(h, W, L))
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
+    rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
+    out, lse, _ = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box)
+    assert rel(out.float().cpu(), rout) < BF16_TOL
+    fin = np.isfinite(rlse)
+    assert rel(lse.cpu().numpy()[fin], rlse[fin]) < 1e-3
