@@ -292,7 +292,7 @@ def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     elif kind == "bulk":
         pos, seg = S.gen_fcc_system(700, 3.8, 6), None
     else:
-        b = S.periodic_box(500, 4, 3.8, 7)
+        b = S.periodic_box(480, 5, 3.8, 7)
         pos, seg, box = b.pos, None, b.box
     N = len(pos)
     nbr, _, _ = po.build_neighbors(pos, 64, 6.0, seg_ptr=seg, box=box)
