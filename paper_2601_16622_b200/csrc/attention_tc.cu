@@ -92,7 +92,11 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
-__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mq,
+// 256 threads: warps 0-3 own the 128 query rows (scores from TMEM, online
+// softmax with lazy rescale, Wt rows, epilogue); warps 4-7 build the per-key
+// source coupling Vg; thread 0 also drives TMA and the tcgen05 MMAs.  Chunk
+// g+1's TMA is in flight while chunk g is processed.
+__global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mq,
                                                              const __grid_constant__ CUtensorMap mk,
                                                              const __grid_constant__ CUtensorMap mv, TcArgs a,
                                                              const double* __restrict__ pos,
@@ -110,10 +114,12 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_consta
   int* nbs = reinterpret_cast<int*>(sm + SM_NB);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool row_warp = warp < 4;
   const int q0 = blockIdx.x * TQ;
-  const int qi = q0 + tid;
-  const bool qvalid = qi < a.N;
+  const int qi = q0 + (tid & 127);
+  const bool qvalid = row_warp && qi < a.N;
   const int c_begin = cptr[blockIdx.x], c_end = cptr[blockIdx.x + 1];
+  const int nch = c_end - c_begin;
 
   if (tid == 0) {
     umma::prefetch_tmap(&mq);
@@ -127,11 +133,9 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_consta
     umma::fence_barrier_init();
   }
   if (warp == 0) umma::tmem_alloc(tslot, 256);
-  // this query's neighbours, ascending j (the kernel consumes the index, it
-  // never re-tests the cutoff)
   int nn = 0;
-  int* my = nbs + tid * KMAX;
-  if (qvalid) {
+  int* my = nbs + (tid & 127) * KMAX;
+  if (qvalid) {  // this query's neighbours, ascending j (the index is consumed, never re-tested)
     for (int s = 0; s < a.K && s < KMAX; ++s) {
       const int j = nbr[(size_t)qi * a.K + s];
       if (j < 0) continue;
@@ -146,199 +150,181 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_consta
   __syncthreads();
   umma::tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t t_out = tmem;          // cols [0, 144)
-  const uint32_t t_s = tmem + 192;      // cols [192, 208)
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-
+  const uint32_t t_out = tmem;      // cols [0, 144)
+  const uint32_t t_s = tmem + 192;  // cols [192, 208)
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
   constexpr uint32_t idesc_s = umma::idesc_bf16(128, KC, 0, 0);
   constexpr uint32_t idesc_v = umma::idesc_bf16(128, NV, 0, 0);
-  uint32_t ph_q = 0, ph_ld[2] = {0, 0}, ph_s = 0, ph_v = 0;
-  int ld_use = 0;  // loads issued (buffer = ld_use & 1)
+  constexpr uint32_t KBYTES = MM * KC * DH * 2, VBYTES = KC * MM * HD * 2;
 
-  // geometry of (qi, j): r, phi, Y^f
-  auto pair_geo = [&](int j, float* w) {
-    double dx = pos[3 * j] - pix, dy = pos[3 * j + 1] - piy, dz = pos[3 * j + 2] - piz;
-    if (a.periodic) {
-      dx -= a.bx * rint(dx / a.bx);
-      dy -= a.by * rint(dy / a.by);
-      dz -= a.bz * rint(dz / a.bz);
-    }
-    const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
-    const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
-    float phi = 1.f;
-    if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
-    solid_l2(rx, ry, rz, w);
-#pragma unroll
-    for (int f = 0; f < MM; ++f) w[f] *= phi;
+  auto issue_load = [&](int g, int ci, int h) {  // chunk ci (global chunk counter g) -> buffer g & 1
+    const int b = g & 1;
+    const int k0 = clist[ci] * KC;
+    uint8_t* kb = sm + SM_K + b * KBYTES;
+    umma::mbar_arrive_expect_tx(&bar_ld[b], KBYTES + VBYTES);
+    for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &bar_ld[b], DH * h, mm, k0);
+    umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &bar_ld[b], HD * h, 0, k0);
   };
 
+  int g0 = 0;  // global chunk counter at the start of this head
   for (int h = 0; h < 8; ++h) {
-    // ---- Q_h tile: 9 boxes of [128 atoms x 32 ch]
     if (tid == 0) {
       umma::mbar_arrive_expect_tx(bar_q, MM * TQ * DH * 2);
       for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(sm + SM_Q + mm * TQ * DH * 2, &mq, bar_q, DH * h, mm, q0);
+      if (nch > 0) issue_load(g0, c_begin, h);
     }
-    umma::mbar_wait(bar_q, ph_q);
-    ph_q ^= 1;
-
-    float lse_h = -INFINITY;
-    for (int pass = 0; pass < 2; ++pass) {
-      float mu = -INFINITY, z = 0.f;
-      int ptr = 0;
-      for (int ci = c_begin; ci < c_end; ++ci) {
-        const int k0 = clist[ci] * KC;
-        const int buf = ld_use & 1;
-        // ---- load K_h (and V_h in pass 2) chunk, S MMA
-        if (tid == 0) {
-          uint8_t* kb = sm + SM_K + buf * (MM * KC * DH * 2);
-          const uint32_t bytes = MM * KC * DH * 2 + (pass ? KC * MM * HD * 2 : 0);
-          umma::mbar_arrive_expect_tx(&bar_ld[buf], bytes);
-          for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &bar_ld[buf], DH * h, mm, k0);
-          if (pass) umma::tma_load_3d(sm + SM_VST + buf * (KC * MM * HD * 2), &mv, &bar_ld[buf], HD * h, 0, k0);
-          umma::mbar_wait(&bar_ld[buf], ph_ld[buf]);
-          umma::tc_fence_after();
-          const uint32_t qa = umma::smem_u32(sm + SM_Q), ka = umma::smem_u32(kb);
+    umma::mbar_wait(bar_q, h & 1);
+    float mu = -INFINITY, z = 0.f;
+    int ptr = 0;
+    for (int it = 0; it < nch; ++it) {
+      const int g = g0 + it, b = g & 1;
+      const int ci = c_begin + it;
+      const int k0 = clist[ci] * KC;
+      if (tid == 0) {
+        umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
+        umma::tc_fence_after();
+        const uint32_t qa = umma::smem_u32(sm + SM_Q), ka = umma::smem_u32(sm + SM_K + b * KBYTES);
 #pragma unroll
-          for (int s = 0; s < 2 * MM; ++s) {
-            const int mm = s >> 1, kk = s & 1;
-            umma::mma_f16(t_s, umma::sdesc(qa + mm * TQ * DH * 2 + kk * 32, 16, 512, 4),
-                          umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
-          }
-          umma::mma_commit(bar_s);
-        } else {
-          // keep the per-buffer phase in sync on all threads (only tid 0 waits)
+        for (int s = 0; s < 2 * MM; ++s) {
+          const int mm = s >> 1, kk = s & 1;
+          umma::mma_f16(t_s, umma::sdesc(qa + mm * TQ * DH * 2 + kk * 32, 16, 512, 4),
+                        umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
         }
-        ph_ld[buf] ^= 1;
-        ++ld_use;
-
-        if (pass == 1) {
-          // previous value MMA must be done before Wt / Vg are overwritten
-          if (ci > c_begin) {
-            umma::mbar_wait(bar_v, ph_v);
-            ph_v ^= 1;
-          }
-          // V chunk: wait for its bytes (bar_ld[buf] completed: tid 0 waited; all threads need the data)
-          umma::mbar_wait(&bar_ld[buf], ph_ld[buf] ^ 1);
-          // transpose V stage [key][mm][c] -> Vt [mm][c][key]
-          const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + buf * (KC * MM * HD * 2));
-          bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
-          for (int e = tid; e < KC * MM * HD; e += 128) {
-            const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, c = rem % HD;
-            vt[(mm * HD + c) * KC + key] = vst[e];
-          }
-          __syncthreads();
-          // Vg[(o,c), (f,j)] = sum_i' G_f[o,i'] v_j[i',c]: warp w handles o = w, w+4, w+8
-          {
-            const int c = lane & 15, j0 = (lane >> 4) * 8;
-            for (int o = warp; o < MM; o += 4) {
-              for (int f = 0; f < MM; ++f) {
-                float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int e = c_tc.ofs[o * MM + f]; e < c_tc.ofs[o * MM + f + 1]; ++e) {
-                  const int ip = c_tc.ent_i[e];
-                  const float cf = c_tc.ent_c[e];
-                  const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
-                  const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        umma::mma_commit(bar_s);
+        if (it + 1 < nch) issue_load(g + 1, ci + 1, h);  // prefetch next chunk into the other buffer
+      }
+      if (it > 0) umma::mbar_wait(bar_v, (g - 1) & 1);  // Wt / Vg / Vt free again
+      if (!row_warp) {
+        // ---- Vg[(o,c),(f,j)] = sum_i' G_f[o,i'] v_j[i',c]  (warps 4-7)
+        umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
+        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
+        bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
+        for (int e = tid - 128; e < KC * MM * HD; e += 128) {
+          const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, c = rem % HD;
+          vt[(mm * HD + c) * KC + key] = vst[e];
+        }
+        umma::named_bar(1, 128);
+        const int c = lane & 15, j0 = (lane >> 4) * 8;
+        for (int o = warp - 4; o < MM; o += 4) {
+          for (int f = 0; f < MM; ++f) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int e = c_tc.ofs[o * MM + f]; e < c_tc.ofs[o * MM + f + 1]; ++e) {
+              const int ip = c_tc.ent_i[e];
+              const float cf = c_tc.ent_c[e];
+              const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
+              const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
 #pragma unroll
-                  for (int t = 0; t < 4; ++t) {
-                    const float2 fv = __bfloat1622float2(b2[t]);
-                    acc[2 * t] = fmaf(cf, fv.x, acc[2 * t]);
-                    acc[2 * t + 1] = fmaf(cf, fv.y, acc[2 * t + 1]);
-                  }
-                }
-                *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc);
+              for (int t = 0; t < 4; ++t) {
+                const float2 fv = __bfloat1622float2(b2[t]);
+                acc[2 * t] = fmaf(cf, fv.x, acc[2 * t]);
+                acc[2 * t + 1] = fmaf(cf, fv.y, acc[2 * t + 1]);
               }
             }
+            *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc);
           }
         }
-        // ---- scores of this chunk
-        umma::mbar_wait(bar_s, ph_s);
-        ph_s ^= 1;
+      } else {
+        // ---- scores -> online softmax (lazy rescale) -> Wt row  (warps 0-3)
+        umma::mbar_wait(bar_s, g & 1);
         umma::tc_fence_after();
         uint32_t sr[16];
         umma::tmem_ld16(t_s + lane_base, sr);
-        // valid keys of this query in [k0, k0+16)
         unsigned vmask = 0;
         while (ptr < nn && my[ptr] < k0) ++ptr;
-        int p2 = ptr;
-        while (p2 < nn && my[p2] < k0 + KC) { vmask |= 1u << (my[p2] - k0); ++p2; }
-        if (pass == 0) {
-          for (int t = 0; t < KC; ++t)
-            if (vmask >> t & 1) {
-              const float sv = a.tau * __uint_as_float(sr[t]);
-              const float m2 = fmaxf(mu, sv);
-              z = z * __expf(mu - m2) + __expf(sv - m2);
-              mu = m2;
-            }
-          ptr = p2;
-        } else {
-          // Wt row: P phi Y^f for the valid keys, 0 elsewhere; two halves of 8 keys
+        while (ptr < nn && my[ptr] < k0 + KC) { vmask |= 1u << (my[ptr] - k0); ++ptr; }
+        float mc = -INFINITY;
+        for (int t = 0; t < KC; ++t)
+          if (vmask >> t & 1) mc = fmaxf(mc, a.tau * __uint_as_float(sr[t]));
+        // rescale only when the running max grows by more than e^5 (rows are independent)
+        const bool need = (mu > -INFINITY) && (mc > mu + 5.f);
+        float factor = 1.f;
+        if (mu == -INFINITY && mc > -INFINITY) mu = mc;
+        else if (need) { factor = __expf(mu - mc); mu = mc; z *= factor; }
+        if (__any_sync(0xffffffffu, need)) {  // warp-collective TMEM read-modify-write
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            float w[MM][8];
+          for (int cc = 0; cc < NV / 16; ++cc) {
+            uint32_t r[16];
+            umma::tmem_ld16(t_out + lane_base + cc * 16, r);
 #pragma unroll
-            for (int t = 0; t < 8; ++t) {
-              const int kk = half * 8 + t;
-              if (vmask >> kk & 1) {
-                float y[MM];
-                pair_geo(k0 + kk, y);
-                const float P = __expf(a.tau * __uint_as_float(sr[kk]) - lse_h);
-#pragma unroll
-                for (int f = 0; f < MM; ++f) w[f][t] = P * y[f];
-              } else {
-#pragma unroll
-                for (int f = 0; f < MM; ++f) w[f][t] = 0.f;
-              }
-            }
-#pragma unroll
-            for (int f = 0; f < MM; ++f)
-              *reinterpret_cast<uint4*>(sm + SM_WT + cm_off(tid, f * KC + half * 8)) = pack8(w[f]);
+            for (int t = 0; t < 16; ++t) r[t] = __float_as_uint(__uint_as_float(r[t]) * factor);
+            umma::tmem_st16(t_out + lane_base + cc * 16, r);
           }
-          ptr = p2;
         }
-        umma::fence_proxy_async();
-        umma::tc_fence_before();
-        __syncthreads();
-        if (pass == 1 && tid == 0) {
-          umma::tc_fence_after();
-          const uint32_t wa = umma::smem_u32(sm + SM_WT), va = umma::smem_u32(sm + SM_VG);
 #pragma unroll
-          for (int s = 0; s < MM; ++s)  // K = 144 = 9 steps of 16 = 2 core columns each
-            umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
-                          umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v,
-                          (ci > c_begin || s > 0) ? 1u : 0u);
-          umma::mma_commit(bar_v);
+        for (int half = 0; half < 2; ++half) {
+          float w[MM][8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int kk = half * 8 + t;
+            if (vmask >> kk & 1) {
+              const int j = k0 + kk;
+              double dx = pos[3 * j] - pix, dy = pos[3 * j + 1] - piy, dz = pos[3 * j + 2] - piz;
+              if (a.periodic) {
+                dx -= a.bx * rint(dx / a.bx);
+                dy -= a.by * rint(dy / a.by);
+                dz -= a.bz * rint(dz / a.bz);
+              }
+              const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+              const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+              float phi = 1.f;
+              if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
+              const float P = __expf(a.tau * __uint_as_float(sr[kk]) - mu);
+              z += P;
+              float y[MM];
+              solid_l2(rx, ry, rz, y);
+              const float pp = P * phi;
+#pragma unroll
+              for (int f = 0; f < MM; ++f) w[f][t] = pp * y[f];
+            } else {
+#pragma unroll
+              for (int f = 0; f < MM; ++f) w[f][t] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int f = 0; f < MM; ++f)
+            *reinterpret_cast<uint4*>(sm + SM_WT + cm_off(tid, f * KC + half * 8)) = pack8(w[f]);
         }
       }
-      if (pass == 0) {
-        lse_h = z > 0.f ? mu + __logf(z) : -INFINITY;
-        if (qvalid) lse[(size_t)qi * 8 + h] = lse_h;
+      umma::fence_proxy_async();
+      umma::tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        umma::tc_fence_after();
+        const uint32_t wa = umma::smem_u32(sm + SM_WT), va = umma::smem_u32(sm + SM_VG);
+#pragma unroll
+        for (int s = 0; s < MM; ++s)  // K = 144 = 9 steps of 16 (2 core-matrix columns each)
+          umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
+                        umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (it > 0 || s > 0) ? 1u : 0u);
+        umma::mma_commit(bar_v);
       }
     }
-    // ---- epilogue: O_h rows from TMEM
-    const bool any = c_end > c_begin;
-    if (any) {
-      umma::mbar_wait(bar_v, ph_v);
-      ph_v ^= 1;
+    // ---- epilogue (rows): O_h / z
+    if (nch > 0) {
+      umma::mbar_wait(bar_v, (g0 + nch - 1) & 1);
       umma::tc_fence_after();
     }
+    if (row_warp) {
+      const float inv = z > 0.f ? 1.f / z : 0.f;
+      if (qvalid) lse[(size_t)qi * 8 + h] = z > 0.f ? mu + __logf(z) : -INFINITY;
 #pragma unroll
-    for (int cc = 0; cc < NV / 16; ++cc) {  // 9 x 16 columns = one o row of 16 channels
-      uint32_t r[16];
-      if (any) umma::tmem_ld16(t_out + lane_base + cc * 16, r);
-      float v[16];
+      for (int cc = 0; cc < NV / 16; ++cc) {
+        uint32_t r[16];
+        if (nch > 0) umma::tmem_ld16(t_out + lane_base + cc * 16, r);
+        float v[16];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) v[t] = (any && lse_h > -INFINITY) ? __uint_as_float(r[t]) : 0.f;
-      if (qvalid) {
-        uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)qi * MM + cc) * 128 + HD * h);
-        dst[0] = pack8(v);
-        dst[1] = pack8(v + 8);
+        for (int t = 0; t < 16; ++t) v[t] = nch > 0 ? __uint_as_float(r[t]) * inv : 0.f;
+        if (qvalid) {
+          uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)qi * MM + cc) * 128 + HD * h);
+          dst[0] = pack8(v);
+          dst[1] = pack8(v + 8);
+        }
       }
     }
+    g0 += nch;
     umma::tc_fence_before();
     __syncthreads();
     umma::tc_fence_after();
   }
-  __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 256);
 }
 
@@ -501,7 +487,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
     cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_fwd_tc_kernel<<<ntiles, 128, smem, st>>>(mq, mk, mv, ta, pos, nbr, cptr, clist, (bf16*)out, lse);
+  attn_fwd_tc_kernel<<<ntiles, 256, smem, st>>>(mq, mk, mv, ta, pos, nbr, cptr, clist, (bf16*)out, lse);
   s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
   cudaFreeAsync(base, st);
   return s;
