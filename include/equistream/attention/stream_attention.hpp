@@ -48,6 +48,7 @@ struct AttentionProblem {
   double r_cut = 6.0;
   bool periodic = false;
   double box[3] = {0, 0, 0};
+  int32_t row0 = 0, n_keys = 0;  // query-row sharding (0 = unsharded)
 
   es_attn_desc desc() const {
     es_attn_desc d{};
@@ -58,6 +59,8 @@ struct AttentionProblem {
     d.r_cut = r_cut;
     d.periodic = periodic ? 1 : 0;
     for (int a = 0; a < 3; ++a) d.box[a] = box[a];
+    d.row0 = row0;
+    d.Nk = n_keys;
     return d;
   }
 };
@@ -77,8 +80,10 @@ inline void build_neighbors(const double* pos, int32_t N, int32_t K, double r_cu
   check(es_neighbors_build(&d, pos, seg_ptr, idx.table, idx.distances, idx.count, workspace, ws_bytes, stream),
         "build_neighbors");
 }
-inline void transpose(NeighborIndex& idx, void* workspace, std::size_t ws_bytes, void* stream = nullptr) {
-  check(es_neighbors_transpose(idx.N, idx.K, idx.table, idx.rev_ptr, idx.rev_pair, workspace, ws_bytes, stream),
+inline void transpose(NeighborIndex& idx, void* workspace, std::size_t ws_bytes, void* stream = nullptr,
+                      int32_t n_keys = 0) {
+  check(es_neighbors_transpose(idx.N, idx.K, n_keys > 0 ? n_keys : idx.N, idx.table, idx.rev_ptr, idx.rev_pair,
+                               workspace, ws_bytes, stream),
         "neighbors_transpose");
 }
 

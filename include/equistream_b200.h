@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 1
+#define ES_ABI_VERSION 2
 
 typedef enum {
   ES_OK = 0,
@@ -83,10 +83,16 @@ typedef struct {
   double r_cut;
   int32_t periodic;   /* 1: minimum image in box[] */
   double box[3];
+  /* Query-row sharding (one large system over several GPUs): the N query
+   * rows are atoms row0 .. row0+N-1 of a system of Nk atoms; q, out, lse,
+   * dout, dq and nbr hold the N local rows, k, v, pos, dk and dv all Nk atoms
+   * (nbr entries index [0, Nk)).  Nk = 0 means Nk = N, row0 = 0. */
+  int32_t row0, Nk;
 } es_attn_desc;
 
-/* Compiled kernel set: L in [0, 4]; C in {32, 64, 128, 256}; C/H in
- * {8, 16, 32, ...} with C/H >= 2 (L <= 2) or >= 1 (L >= 3). */
+/* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in
+ * {4, 8, 16, 32}.  bf16 + EAAS + L=2 + C=128 + H=8 + K<=64 runs on the
+ * tcgen05 tensor-core kernel, everything else on the SIMT kernels. */
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, void* out, float* lse, void* stream);
 
@@ -116,12 +122,13 @@ size_t es_neighbors_workspace_size(const es_nbr_desc* d);
 es_status es_neighbors_build(const es_nbr_desc* d, const double* pos, const int32_t* seg_ptr, int32_t* nbr,
                              float* dist, int32_t* count, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Transposed (key-major) relation of nbr: for key j, entries
- * rev_pair[rev_ptr[j] .. rev_ptr[j+1]) hold i*K + slot with nbr[i][slot] == j,
- * ascending (deterministic).  rev_ptr: [N+1], rev_pair: [N*K]. */
-size_t es_neighbors_transpose_workspace_size(int32_t N, int32_t K);
-es_status es_neighbors_transpose(int32_t N, int32_t K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair,
-                                 void* workspace, size_t workspace_bytes, void* stream);
+/* Transposed (key-major) relation of nbr [N][K] over Nk key atoms (Nk = N
+ * for one unsharded system): for key j, entries rev_pair[rev_ptr[j] ..
+ * rev_ptr[j+1]) hold i*K + slot with nbr[i][slot] == j, ascending
+ * (deterministic).  rev_ptr: [Nk+1], rev_pair: [N*K]. */
+size_t es_neighbors_transpose_workspace_size(int32_t N, int32_t K, int32_t Nk);
+es_status es_neighbors_transpose(int32_t N, int32_t K, int32_t Nk, const int32_t* nbr, int32_t* rev_ptr,
+                                 int32_t* rev_pair, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Tile-skip mask: bit (qb, kb) of mask[qb * ceil(nkb/32) + kb/32] is set iff
  * some atom of query block qb (tq atoms) lists a neighbour in key block kb

@@ -20,7 +20,8 @@ ES_PHI_COSINE, ES_PHI_ONE = 0, 1
 class AttnDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("H", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32),
                 ("value_mode", ct.c_int32), ("phi_mode", ct.c_int32), ("dtype", ct.c_int32),
-                ("r_cut", ct.c_double), ("periodic", ct.c_int32), ("box", ct.c_double * 3)]
+                ("r_cut", ct.c_double), ("periodic", ct.c_int32), ("box", ct.c_double * 3),
+                ("row0", ct.c_int32), ("Nk", ct.c_int32)]
 
 
 class NbrDesc(ct.Structure):
@@ -69,8 +70,8 @@ def lib() -> ct.CDLL:
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]
         L.es_neighbors_workspace_size.argtypes = [ct.POINTER(NbrDesc)]
         L.es_neighbors_workspace_size.restype = sz
-        L.es_neighbors_transpose.argtypes = [i32, i32, vp, vp, vp, vp, sz, vp]
-        L.es_neighbors_transpose_workspace_size.argtypes = [i32, i32]
+        L.es_neighbors_transpose.argtypes = [i32, i32, i32, vp, vp, vp, vp, sz, vp]
+        L.es_neighbors_transpose_workspace_size.argtypes = [i32, i32, i32]
         L.es_neighbors_transpose_workspace_size.restype = sz
         L.es_tile_mask.argtypes = [i32, i32, vp, i32, i32, vp, vp]
         L.es_project_fwd.argtypes = [ct.POINTER(ProjDesc)] + [vp] * 6
@@ -81,6 +82,8 @@ def lib() -> ct.CDLL:
         L.es_cg_real.argtypes = [i32] * 6
         L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
         L.es_wigner_d_host.argtypes = [i32, dp, dp]
+        if L.es_abi_version() != 2:
+            raise EsError("libequistream_b200.so ABI mismatch: rebuild (python -m paper_2601_16622_b200.build)")
         _lib = L
     return _lib
 

@@ -72,9 +72,10 @@ class NeighborIndex:
     def K(self) -> int:
         return self.table.shape[1]
 
-    def transpose(self):
-        if self._rev is None:
-            self._rev = neighbors_transpose(self.table)
+    def transpose(self, n_keys: int | None = None):
+        nk = self.N if n_keys is None else int(n_keys)
+        if self._rev is None or self._rev[0].numel() != nk + 1:
+            self._rev = neighbors_transpose(self.table, nk)
         return self._rev
 
 
@@ -109,15 +110,17 @@ def build_neighbors(pos: torch.Tensor, K: int, r_cut: float, seg_ptr: torch.Tens
     return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box))
 
 
-def neighbors_transpose(table: torch.Tensor):
-    """Key-major relation: (rev_ptr [N+1], rev_pair [N*K]) with
-    rev_pair[rev_ptr[j]:rev_ptr[j+1]] = sorted {i*K+slot : table[i,slot] == j}."""
+def neighbors_transpose(table: torch.Tensor, n_keys: int | None = None):
+    """Key-major relation over n_keys key atoms (default N): (rev_ptr [Nk+1],
+    rev_pair [N*K]) with rev_pair[rev_ptr[j]:rev_ptr[j+1]] = sorted
+    {i*K+slot : table[i,slot] == j}."""
     table = _need(table, "table", torch.int32)
     N, K = table.shape
-    rev_ptr = torch.empty(N + 1, dtype=torch.int32, device=table.device)
+    Nk = N if n_keys is None else int(n_keys)
+    rev_ptr = torch.empty(Nk + 1, dtype=torch.int32, device=table.device)
     rev_pair = torch.empty(max(N * K, 1), dtype=torch.int32, device=table.device)
-    ws = _workspace(lib().es_neighbors_transpose_workspace_size(N, K), table.device)
-    check(lib().es_neighbors_transpose(N, K, _ptr(table), _ptr(rev_ptr), _ptr(rev_pair), _ptr(ws), ws.numel(),
+    ws = _workspace(lib().es_neighbors_transpose_workspace_size(N, K, Nk), table.device)
+    check(lib().es_neighbors_transpose(N, K, Nk, _ptr(table), _ptr(rev_ptr), _ptr(rev_pair), _ptr(ws), ws.numel(),
                                        _stream()), "es_neighbors_transpose")
     return rev_ptr, rev_pair
 
@@ -182,7 +185,7 @@ class AttentionConfig:
     phi: str = "cosine"
     box: tuple | None = None
 
-    def desc(self, N: int, K: int, C: int, dtype: torch.dtype) -> _lib.AttnDesc:
+    def desc(self, N: int, K: int, C: int, dtype: torch.dtype, row0: int = 0, Nk: int = 0) -> _lib.AttnDesc:
         if self.value_mode not in _VALUE:
             raise EsInvalidArgument(f"value_mode must be one of {list(_VALUE)}")
         if self.phi not in _PHI:
@@ -197,6 +200,7 @@ class AttentionConfig:
         if self.box is not None:
             for a in range(3):
                 d.box[a] = float(self.box[a])
+        d.row0, d.Nk = int(row0), int(Nk)
         return d
 
 
@@ -211,31 +215,40 @@ class SavedAttention:
     out: torch.Tensor
     lse: torch.Tensor
     cfg: AttentionConfig
+    row0: int = 0
 
 
-def _check_qkv(q, k, v, pos, idx, cfg):
+def _check_qkv(q, k, v, pos, idx, cfg, row0=0):
+    """q (and idx, out, lse): the N local query rows; k, v, pos: all Nk atoms."""
     if q.dtype not in _DT:
         raise EsInvalidArgument("q: dtype must be float32 or bfloat16")
     M = (cfg.L + 1) ** 2
     _need(v, "v", q.dtype)
     if v.dim() != 3 or v.shape[1] != M:
-        raise EsInvalidArgument(f"v: expected [N, {M}, C]")
-    N, _, C = v.shape
-    _need(q, "q", q.dtype, (N, M, 2 * C))
-    _need(k, "k", q.dtype, (N, M, 2 * C))
-    _need(pos, "pos", torch.float64, (N, 3))
+        raise EsInvalidArgument(f"v: expected [Nk, {M}, C]")
+    Nk, _, C = v.shape
+    _need(q, "q", q.dtype)
+    if q.dim() != 3 or tuple(q.shape[1:]) != (M, 2 * C):
+        raise EsInvalidArgument(f"q: expected [N, {M}, {2 * C}]")
+    N = q.shape[0]
+    _need(k, "k", q.dtype, (Nk, M, 2 * C))
+    _need(pos, "pos", torch.float64, (Nk, 3))
     _need(idx.table, "idx.table", torch.int32)
     if idx.table.shape[0] != N:
-        raise EsInvalidArgument("idx: row count != N")
-    return N, C
+        raise EsInvalidArgument("idx: row count != number of query rows")
+    if row0 < 0 or row0 + N > Nk:
+        raise EsInvalidArgument("row0 + N > Nk")
+    return N, C, Nk
 
 
-def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig):
-    """stream_aggregate (SPEC.md:275; Alg. 1): returns (m [N][M][C], lse [N][H] f32)."""
-    N, C = _check_qkv(q, k, v, pos, idx, cfg)
-    out = torch.empty_like(v)
+def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row0: int = 0):
+    """stream_aggregate (SPEC.md:275; Alg. 1): returns (m [N][M][C], lse [N][H] f32).
+    With row0 / k, v, pos longer than q: the query rows are atoms row0..row0+N-1
+    of the Nk-atom system (query-row sharding)."""
+    N, C, Nk = _check_qkv(q, k, v, pos, idx, cfg, row0)
+    out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
-    d = cfg.desc(N, idx.K, C, q.dtype)
+    d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
     check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
                             _ptr(lse), _stream()), "es_attn_fwd")
     return out, lse
@@ -245,10 +258,10 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention):
     """stream_aggregate_backward (SPEC.md:293): (grad_q, grad_k, grad_v) of
     sum <grad_m, m>, by recomputation (no O(N*K*C) buffer)."""
     s = saved
-    N, C = _check_qkv(s.q, s.k, s.v, s.pos, s.idx, s.cfg)
-    grad_m = _need(grad_m.contiguous(), "grad_m", s.q.dtype, tuple(s.v.shape))
-    rev_ptr, rev_pair = s.idx.transpose()
-    d = s.cfg.desc(N, s.idx.K, C, s.q.dtype)
+    N, C, Nk = _check_qkv(s.q, s.k, s.v, s.pos, s.idx, s.cfg, s.row0)
+    grad_m = _need(grad_m.contiguous(), "grad_m", s.q.dtype, tuple(s.out.shape))
+    rev_ptr, rev_pair = s.idx.transpose(Nk)
+    d = s.cfg.desc(N, s.idx.K, C, s.q.dtype, s.row0, Nk)
     ws = _workspace(lib().es_attn_bwd_workspace_size(ct.byref(d)), s.q.device)
     dq = torch.empty_like(s.q)
     dk = torch.empty_like(s.k)

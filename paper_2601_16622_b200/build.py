@@ -54,8 +54,22 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def gen_tables() -> None:
+    """Generate csrc/_gen_cg.h from the library's own so3 tables (g++ host tool)."""
+    out = os.path.join(CSRC, "_gen_cg.h")
+    tool_src = [os.path.join(HERE, "tools", "gen_tables.cpp"), os.path.join(CSRC, "so3_tables.cpp")]
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(x) for x in tool_src):
+        return
+    exe = os.path.join(BUILD, "gen_tables")
+    cuda_inc = os.path.join(os.path.dirname(os.path.dirname(nvcc())), "include")
+    subprocess.check_call(["g++", "-std=c++17", "-O1", "-I", INCLUDE, "-I", CSRC, "-I", cuda_inc, *tool_src,
+                           "-o", exe])
+    subprocess.check_call([exe, out])
+
+
 def build(verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    gen_tables()
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))

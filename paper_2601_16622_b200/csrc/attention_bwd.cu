@@ -177,7 +177,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4;
   auto fn = attn_bwd_kv_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fn<<<kp.N, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
+  fn<<<kp.Nk, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
                                   (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf);
   s = cuda_status(cudaGetLastError(), "attn_bwd_kv_kernel");
   if (s != ES_OK) return s;
@@ -192,6 +192,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
 KParams make_params(const AttnArgs& a) {
   KParams kp;
   kp.N = a.N; kp.K = a.K; kp.H = a.H; kp.C = a.C; kp.Dq = a.Dq;
+  kp.row0 = a.row0; kp.Nk = a.Nk;
   kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
   kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
   kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];

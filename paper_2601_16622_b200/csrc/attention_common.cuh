@@ -232,6 +232,7 @@ __device__ __forceinline__ void fit_all(const float (&R)[9], float* rec) {
 
 struct KParams {
   int N, K, H, C, Dq;
+  int row0, Nk;  // query i <-> atom row0 + i (pos); keys j index k/v/pos in [0, Nk)
   int phi_mode, periodic;
   float tau, r_cut, inv_rcut;
   double bx, by, bz;
@@ -244,7 +245,8 @@ struct KParams {
 // branch-stable; any gauge gives the same composite.
 template <int L, bool EAAS>
 __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, int i, int j, float* rec) {
-  double dx = pos[3 * j] - pos[3 * i], dy = pos[3 * j + 1] - pos[3 * i + 1], dz = pos[3 * j + 2] - pos[3 * i + 2];
+  const int ia = p.row0 + i;
+  double dx = pos[3 * j] - pos[3 * ia], dy = pos[3 * j + 1] - pos[3 * ia + 1], dz = pos[3 * j + 2] - pos[3 * ia + 2];
   if (p.periodic) {
     dx -= p.bx * rint(dx / p.bx);
     dy -= p.by * rint(dy / p.by);

@@ -123,6 +123,7 @@ es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v
 KParams make_params(const AttnArgs& a) {
   KParams kp;
   kp.N = a.N; kp.K = a.K; kp.H = a.H; kp.C = a.C; kp.Dq = a.Dq;
+  kp.row0 = a.row0; kp.Nk = a.Nk;
   kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
   kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
   kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];

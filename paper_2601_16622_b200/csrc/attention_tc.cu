@@ -24,6 +24,7 @@
 
 #include <cub/cub.cuh>
 
+#include "_gen_cg.h"
 #include "es_internal.h"
 #include "umma.cuh"
 
@@ -62,7 +63,7 @@ struct TcTab {
 __constant__ TcTab c_tc;
 
 struct TcArgs {
-  int N, K;
+  int N, K, row0, Nk;
   float tau, r_cut, inv_rcut;
   int phi_mode, periodic;
   double bx, by, bz;
@@ -145,7 +146,10 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
     }
   }
   double pix = 0, piy = 0, piz = 0;
-  if (qvalid) { pix = pos[3 * qi]; piy = pos[3 * qi + 1]; piz = pos[3 * qi + 2]; }
+  if (qvalid) {
+    const int qa = a.row0 + qi;
+    pix = pos[3 * qa]; piy = pos[3 * qa + 1]; piz = pos[3 * qa + 2];
+  }
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
@@ -194,36 +198,18 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
         if (it + 1 < nch) issue_load(g + 1, ci + 1, h);  // prefetch next chunk into the other buffer
       }
       if (it > 0) umma::mbar_wait(bar_v, (g - 1) & 1);  // Wt / Vg / Vt free again
-      if (!row_warp) {
-        // ---- Vg[(o,c),(f,j)] = sum_i' G_f[o,i'] v_j[i',c]  (warps 4-7)
-        umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
+      // ---- V chunk -> Vt [mm][c][key] (all warps), then the per-key source coupling
+      umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
+      {
         const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
         bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
-        for (int e = tid - 128; e < KC * MM * HD; e += 128) {
+        for (int e = tid; e < KC * MM * HD; e += 256) {
           const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, c = rem % HD;
           vt[(mm * HD + c) * KC + key] = vst[e];
         }
-        umma::named_bar(1, 128);
-        const int c = lane & 15, j0 = (lane >> 4) * 8;
-        for (int o = warp - 4; o < MM; o += 4) {
-          for (int f = 0; f < MM; ++f) {
-            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int e = c_tc.ofs[o * MM + f]; e < c_tc.ofs[o * MM + f + 1]; ++e) {
-              const int ip = c_tc.ent_i[e];
-              const float cf = c_tc.ent_c[e];
-              const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
-              const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const float2 fv = __bfloat1622float2(b2[t]);
-                acc[2 * t] = fmaf(cf, fv.x, acc[2 * t]);
-                acc[2 * t + 1] = fmaf(cf, fv.y, acc[2 * t + 1]);
-              }
-            }
-            *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc);
-          }
-        }
-      } else {
+      }
+      __syncthreads();
+      if (row_warp) {
         // ---- scores -> online softmax (lazy rescale) -> Wt row  (warps 0-3)
         umma::mbar_wait(bar_s, g & 1);
         umma::tc_fence_after();
@@ -283,6 +269,40 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
 #pragma unroll
           for (int f = 0; f < MM; ++f)
             *reinterpret_cast<uint4*>(sm + SM_WT + cm_off(tid, f * KC + half * 8)) = pack8(w[f]);
+        }
+      }
+      {
+        // Vg[(o,c),(f,j)] = sum_i' G_f[o,i'] v_j[i',c]; o split over the 8 warps
+        // (rows: o = 0..3, others: o = 4..8), compile-time sparsity (_gen_cg.h)
+        const int c = lane & 15, j0 = (lane >> 4) * 8;
+        const bf16* vt = reinterpret_cast<const bf16*>(sm + SM_VT);
+        float v8[MM][8];
+#pragma unroll
+        for (int ip = 0; ip < MM; ++ip) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 fv = __bfloat1622float2(b2[t]);
+            v8[ip][2 * t] = fv.x;
+            v8[ip][2 * t + 1] = fv.y;
+          }
+        }
+        auto emit = [&](int o, const float (&acc)[MM][8]) {
+#pragma unroll
+          for (int f = 0; f < MM; ++f)
+            *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc[f]);
+        };
+        float acc[MM][8];
+        switch (warp) {
+          case 0: es_vg_o0(v8, acc); emit(0, acc); break;
+          case 1: es_vg_o1(v8, acc); emit(1, acc); break;
+          case 2: es_vg_o2(v8, acc); emit(2, acc); break;
+          case 3: es_vg_o3(v8, acc); emit(3, acc); break;
+          case 4: es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
+          case 5: es_vg_o5(v8, acc); emit(5, acc); break;
+          case 6: es_vg_o6(v8, acc); emit(6, acc); break;
+          default: es_vg_o7(v8, acc); emit(7, acc); break;
         }
       }
       umma::fence_proxy_async();
@@ -444,7 +464,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   if (s != ES_OK) return s;
   if (a.N == 0) return ES_OK;
   const int ntiles = (a.N + TQ - 1) / TQ;
-  const int nkb = (a.N + KC - 1) / KC;
+  const int nkb = (a.Nk + KC - 1) / KC;
   const int words = (nkb + 31) / 32;
   const size_t per_tile = (size_t)(nkb < TQ * KMAX ? nkb : TQ * KMAX);
   size_t cub_bytes = 0;
@@ -465,7 +485,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   void* cub_ws = base + off;
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
-  s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, mask, st);
+  s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
   if (s != ES_OK) return s;
   tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
   e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
@@ -474,11 +494,11 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
 
   CUtensorMap mq, mk, mv;
   if (!map3(&mq, q, 256, MM, a.N, DH, 1, TQ, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !map3(&mk, k, 256, MM, a.N, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !map3(&mv, v, 128, MM, a.N, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
+      !map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mv, v, 128, MM, a.Nk, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
     return fail(ES_CUDA_ERROR, "attn_fwd_tc: tensor map encode failed");
   TcArgs ta;
-  ta.N = a.N; ta.K = a.K; ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
+  ta.N = a.N; ta.K = a.K; ta.row0 = a.row0; ta.Nk = a.Nk; ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
   ta.phi_mode = a.phi_mode; ta.periodic = a.periodic;
   ta.bx = a.box[0]; ta.by = a.box[1]; ta.bz = a.box[2];
   const int smem = SM_TOTAL + 1024;

@@ -47,12 +47,16 @@ es_status check_attn(const es_attn_desc* d) {
   if (d->C % 32 != 0 || d->C > 256) return fail(ES_UNSUPPORTED, "attn: C must be a multiple of 32 and <= 256");
   if (ch > 32 || 32 % ch != 0 || ch < 4) return fail(ES_UNSUPPORTED, "attn: C/H must be 4, 8, 16 or 32");
   if (d->H > 64) return fail(ES_UNSUPPORTED, "attn: H <= 64");
+  if (d->Nk < 0 || d->row0 < 0) return fail(ES_INVALID_ARGUMENT, "attn: row0, Nk >= 0");
+  if (d->Nk > 0 && d->row0 + d->N > d->Nk) return fail(ES_INVALID_ARGUMENT, "attn: row0 + N > Nk");
   return ES_OK;
 }
 
 AttnArgs to_args(const es_attn_desc* d) {
   AttnArgs a;
   a.N = d->N; a.K = d->K; a.H = d->H; a.L = d->L; a.C = d->C; a.Dq = 2 * d->C;
+  a.Nk = d->Nk > 0 ? d->Nk : d->N;
+  a.row0 = d->Nk > 0 ? d->row0 : 0;
   a.value_mode = d->value_mode; a.phi_mode = d->phi_mode; a.dtype = d->dtype; a.periodic = d->periodic;
   const int M = (d->L + 1) * (d->L + 1);
   a.tau = (float)(1.0 / std::sqrt((double)M * (a.Dq / d->H)));
@@ -199,19 +203,19 @@ es_status es_neighbors_build(const es_nbr_desc* d, const double* pos, const int3
   });
 }
 
-size_t es_neighbors_transpose_workspace_size(int32_t N, int32_t K) {
-  if (N < 0 || K < 1) return 0;
-  return transpose_workspace_bytes(N, K);
+size_t es_neighbors_transpose_workspace_size(int32_t N, int32_t K, int32_t Nk) {
+  if (N < 0 || K < 1 || Nk < 0) return 0;
+  return transpose_workspace_bytes(N, K, Nk);
 }
 
-es_status es_neighbors_transpose(int32_t N, int32_t K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair,
-                                 void* workspace, size_t workspace_bytes, void* stream) {
+es_status es_neighbors_transpose(int32_t N, int32_t K, int32_t Nk, const int32_t* nbr, int32_t* rev_ptr,
+                                 int32_t* rev_pair, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
-    if (N < 0 || K < 1) return fail(ES_INVALID_ARGUMENT, "neighbors_transpose: N >= 0, K >= 1");
+    if (N < 0 || K < 1 || Nk < 0) return fail(ES_INVALID_ARGUMENT, "neighbors_transpose: N >= 0, K >= 1, Nk >= 0");
     if ((size_t)N * K >= (size_t)1 << 31) return fail(ES_UNSUPPORTED, "neighbors_transpose: N*K >= 2^31");
     if (N > 0 && (!nbr || !rev_ptr || !rev_pair || !workspace))
       return fail(ES_INVALID_ARGUMENT, "neighbors_transpose: null buffer");
-    return nbr_transpose_launch(N, K, nbr, rev_ptr, rev_pair, workspace, workspace_bytes, (cudaStream_t)stream);
+    return nbr_transpose_launch(N, K, Nk, nbr, rev_ptr, rev_pair, workspace, workspace_bytes, (cudaStream_t)stream);
   });
 }
 
@@ -220,7 +224,7 @@ es_status es_tile_mask(int32_t N, int32_t K, const int32_t* nbr, int32_t tq, int
   return guarded([&] {
     if (N < 0 || K < 1) return fail(ES_INVALID_ARGUMENT, "tile_mask: N >= 0, K >= 1");
     if (N > 0 && (!nbr || !mask)) return fail(ES_INVALID_ARGUMENT, "tile_mask: null buffer");
-    return tile_mask_launch(N, K, nbr, tq, tk, mask, (cudaStream_t)stream);
+    return tile_mask_launch(N, K, nbr, tq, tk, (N + tk - 1) / tk, mask, (cudaStream_t)stream);
   });
 }
 

@@ -40,6 +40,7 @@ int entry_index(int lo, int li, int m);
 // ---------------------------------------------------------------- launchers
 struct AttnArgs {
   int N, K, H, L, C, Dq;
+  int row0, Nk;
   int value_mode, phi_mode, dtype, periodic;
   float tau, r_cut;
   double box[3];
@@ -64,10 +65,11 @@ struct NbrArgs {
 size_t nbr_workspace_bytes(const NbrArgs& a);
 es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* seg_ptr, int32_t* nbr, float* dist,
                            int32_t* count, void* ws, size_t ws_bytes, cudaStream_t st);
-size_t transpose_workspace_bytes(int N, int K);
-es_status nbr_transpose_launch(int N, int K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair, void* ws,
-                               size_t ws_bytes, cudaStream_t st);
-es_status tile_mask_launch(int N, int K, const int32_t* nbr, int tq, int tk, uint32_t* mask, cudaStream_t st);
+size_t transpose_workspace_bytes(int N, int K, int Nk);
+es_status nbr_transpose_launch(int N, int K, int Nk, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair,
+                               void* ws, size_t ws_bytes, cudaStream_t st);
+es_status tile_mask_launch(int N, int K, const int32_t* nbr, int tq, int tk, int nkb, uint32_t* mask,
+                           cudaStream_t st);
 
 struct ProjArgs {
   int N, L, C, Dq, Cv, dtype;

@@ -274,12 +274,12 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
 }
 
 // ---------------------------------------------------------------- transpose
-__global__ void tr_keys_kernel(int N, int K, const int32_t* __restrict__ nbr, unsigned* __restrict__ key,
+__global__ void tr_keys_kernel(int N, int K, int Nk, const int32_t* __restrict__ nbr, unsigned* __restrict__ key,
                                int* __restrict__ val, int* __restrict__ cnt) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (size_t)N * K) return;
   const int j = nbr[t];
-  key[t] = j >= 0 ? (unsigned)j : (unsigned)N;
+  key[t] = j >= 0 ? (unsigned)j : (unsigned)Nk;
   val[t] = (int)t;
   if (j >= 0) atomicAdd(&cnt[j], 1);
 }
@@ -288,18 +288,18 @@ namespace {
 struct TrWs {
   size_t key, skey, val, cnt, cub, total, cub_sort, cub_scan;
 };
-TrWs tr_ws(int N, int K) {
+TrWs tr_ws(int N, int K, int Nk) {
   TrWs w{};
   const int n = N * K;
   size_t cs = 0, cc = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, cs, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
                                   (int*)nullptr, n);
-  cub::DeviceScan::ExclusiveSum(nullptr, cc, (int*)nullptr, (int*)nullptr, N + 1);
+  cub::DeviceScan::ExclusiveSum(nullptr, cc, (int*)nullptr, (int*)nullptr, Nk + 1);
   size_t o = 0;
   w.key = o; o += align256(sizeof(unsigned) * n);
   w.skey = o; o += align256(sizeof(unsigned) * n);
   w.val = o; o += align256(sizeof(int) * n);
-  w.cnt = o; o += align256(sizeof(int) * (N + 1));
+  w.cnt = o; o += align256(sizeof(int) * (Nk + 1));
   w.cub = o; o += align256(cs > cc ? cs : cc);
   w.cub_sort = cs; w.cub_scan = cc;
   w.total = o;
@@ -307,28 +307,31 @@ TrWs tr_ws(int N, int K) {
 }
 }  // namespace
 
-size_t transpose_workspace_bytes(int N, int K) { return tr_ws(N, K).total; }
+size_t transpose_workspace_bytes(int N, int K, int Nk) { return tr_ws(N, K, Nk).total; }
 
-es_status nbr_transpose_launch(int N, int K, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair, void* ws,
-                               size_t ws_bytes, cudaStream_t st) {
-  const TrWs w = tr_ws(N, K);
+es_status nbr_transpose_launch(int N, int K, int Nk, const int32_t* nbr, int32_t* rev_ptr, int32_t* rev_pair,
+                               void* ws, size_t ws_bytes, cudaStream_t st) {
+  const TrWs w = tr_ws(N, K, Nk);
   if (ws_bytes < w.total) return fail(ES_INVALID_ARGUMENT, "neighbors_transpose: workspace too small");
-  if (N == 0) return ES_OK;
+  if (N == 0 || Nk == 0) {
+    if (Nk >= 0) cudaMemsetAsync(rev_ptr, 0, sizeof(int) * (Nk + 1), st);
+    return ES_OK;
+  }
   char* base = (char*)ws;
   unsigned* key = (unsigned*)(base + w.key);
   unsigned* skey = (unsigned*)(base + w.skey);
   int* val = (int*)(base + w.val);
   int* cnt = (int*)(base + w.cnt);
   const int n = N * K;
-  cudaMemsetAsync(cnt, 0, sizeof(int) * (N + 1), st);
-  tr_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(N, K, nbr, key, val, cnt);
+  cudaMemsetAsync(cnt, 0, sizeof(int) * (Nk + 1), st);
+  tr_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(N, K, Nk, nbr, key, val, cnt);
   int bits = 1;
-  while ((1u << bits) <= (unsigned)N) ++bits;
+  while ((1u << bits) <= (unsigned)Nk) ++bits;
   size_t cb = w.cub_sort;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(base + w.cub, cb, key, skey, val, (int*)rev_pair, n, 0, bits, st);
   if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: sort");
   cb = w.cub_scan;
-  e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, N + 1, st);
+  e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, Nk + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: scan");
   return cuda_status(cudaGetLastError(), "neighbors_transpose");
 }
@@ -345,10 +348,10 @@ __global__ void tile_mask_kernel(int N, int K, const int32_t* __restrict__ nbr, 
   atomicOr(&mask[(size_t)qb * words + kb / 32], 1u << (kb % 32));
 }
 
-es_status tile_mask_launch(int N, int K, const int32_t* nbr, int tq, int tk, uint32_t* mask, cudaStream_t st) {
+es_status tile_mask_launch(int N, int K, const int32_t* nbr, int tq, int tk, int nkb, uint32_t* mask,
+                           cudaStream_t st) {
   if (tq <= 0 || tk <= 0) return fail(ES_INVALID_ARGUMENT, "tile_mask: tile sizes must be positive");
   if (N == 0) return ES_OK;
-  const int nkb = (N + tk - 1) / tk;
   const int words = (nkb + 31) / 32;
   const size_t n = (size_t)N * K;
   tile_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, K, nbr, tq, tk, words, mask);

@@ -305,3 +305,43 @@ def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     assert rel(out.float().cpu(), rout) < BF16_TOL
     fin = np.isfinite(rlse)
     assert rel(lse.cpu().numpy()[fin], rlse[fin]) < 1e-3
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_row_sharded_attention_matches_unsharded(es, dtype):
+    """Query-row sharding (config 5 layout) simulated on one GPU: each shard
+    runs its rows against all keys (row0 / Nk); outputs concatenate and the
+    partial dk / dv sum to the unsharded gradients (what the NCCL
+    reduce-scatter of paper_2601_16622_b200.distributed does)."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    L, C, H = 2, 128, 8
+    b = S.periodic_box(700, 6, 3.8, 3)
+    pos = dev(b.pos)
+    N = len(b.pos)
+    idx = es.build_neighbors(pos, 64, 6.0, box=b.box)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q = torch.randn(N, 9, 2 * C, device="cuda", generator=g).to(dtype)
+    k = torch.randn(N, 9, 2 * C, device="cuda", generator=g).to(dtype)
+    v = torch.randn(N, 9, C, device="cuda", generator=g).to(dtype)
+    go = torch.randn(N, 9, C, device="cuda", generator=g).to(dtype)
+    cfg = AttentionConfig(heads=H, L=L, box=tuple(b.box))
+    out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
+    dq, dk, dv = es.stream_aggregate_backward(go, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
+    cuts = [0, 250, 520, N]
+    outs, dqs = [], []
+    dk_sum = torch.zeros_like(dk, dtype=torch.float32)
+    dv_sum = torch.zeros_like(dv, dtype=torch.float32)
+    for a0, a1 in zip(cuts[:-1], cuts[1:]):
+        li = NeighborIndex(idx.table[a0:a1].contiguous(), None, idx.count[a0:a1], 6.0)
+        o_, l_ = es.stream_aggregate(q[a0:a1].contiguous(), k, v, pos, li, cfg, row0=a0)
+        saved = SavedAttention(q[a0:a1].contiguous(), k, v, pos, li, o_, l_, cfg, row0=a0)
+        dq_, dk_, dv_ = es.stream_aggregate_backward(go[a0:a1].contiguous(), saved)
+        outs.append(o_)
+        dqs.append(dq_)
+        dk_sum += dk_.float()
+        dv_sum += dv_.float()
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    assert rel(torch.cat(outs).float().cpu(), out.float().cpu()) < tol
+    assert rel(torch.cat(dqs).float().cpu(), dq.float().cpu()) < tol
+    assert rel(dk_sum.cpu(), dk.float().cpu()) < tol
+    assert rel(dv_sum.cpu(), dv.float().cpu()) < tol
