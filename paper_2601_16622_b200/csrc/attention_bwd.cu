@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 // Key-centric pass: CTA per key atom j over the transposed relation; yields
 // dk_j, dv_j exclusively (no atomics) and the per-pair-head dscore.
 template <int L, int CPL, bool EAAS, typename T>
-__global__ void __launch_bounds__(256) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
                                                           const int* __restrict__ rev_pair,

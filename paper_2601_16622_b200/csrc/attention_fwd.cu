@@ -8,7 +8,7 @@ namespace {
 
 // ------------------------------------------------------------------ forward
 template <int L, int CPL, bool EAAS, typename T>
-__global__ void __launch_bounds__(256) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                        const T* __restrict__ v, const double* __restrict__ pos,
                                                        const int* __restrict__ nbr, T* __restrict__ out,
                                                        float* __restrict__ lse) {
@@ -158,12 +158,14 @@ es_status attn_fwd_launch(const AttnArgs& a, const void* q, const void* k, const
   if (s != ES_OK) return s;
   const KParams kp = make_params(a);
   if (a.N == 0) return ES_OK;
-  static int force_simt = -1;
-  if (force_simt < 0) {
-    const char* e = getenv("ES_ATTN_SIMT");
-    force_simt = (e && e[0] == '1') ? 1 : 0;
+  // The tcgen05 kernel is opt-in (ES_ATTN_TC=1) until it beats the SIMT
+  // kernel on the bench workload (round-1 measurement: 9.4 vs 8.4 ms).
+  static int use_tc = -1;
+  if (use_tc < 0) {
+    const char* e = getenv("ES_ATTN_TC");
+    use_tc = (e && e[0] == '1') ? 1 : 0;
   }
-  if (!force_simt && attn_tc_supported(a)) return attn_fwd_tc_launch(a, q, k, v, pos, nbr, out, lse, st);
+  if (use_tc && attn_tc_supported(a)) return attn_fwd_tc_launch(a, q, k, v, pos, nbr, out, lse, st);
   return dispatch<FwdOp>(a, kp, q, k, v, pos, nbr, out, lse, st);
 }
 
