@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 // Key-centric pass: CTA per key atom j over the transposed relation; yields
 // dk_j, dv_j exclusively (no atomics) and the per-pair-head dscore.
 template <int L, int CPL, bool EAAS, typename T>
-__global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
                                                           const int* __restrict__ rev_pair,
@@ -51,11 +51,13 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KPar
   const int head = c0 / Ch;
   const int Dq = p.Dq;
 
-  float kr[M][2 * CPL], vr[M][CPL], dkr[M][2 * CPL], dvr[M][CPL];
+  // k_j / v_j are re-read per pair from L1 (one row per CTA) instead of
+  // being held in registers: halves the live state, doubles occupancy
+  float dkr[M][2 * CPL], dvr[M][CPL];
+  const T* kj = k + (size_t)j * M * Dq + 2 * c0;
+  const T* vj = v + (size_t)j * M * p.C + c0;
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
-    ldvec<2 * CPL>(k + ((size_t)j * M + mm) * Dq + 2 * c0, kr[mm]);
-    ldvec<CPL>(v + ((size_t)j * M + mm) * p.C + c0, vr[mm]);
 #pragma unroll
     for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = 0.f;
 #pragma unroll
@@ -84,7 +86,10 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KPar
       for (int mm = 0; mm < M; ++mm) {
         ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qv[mm]);
 #pragma unroll
-        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[mm][c], s);
+        float kr[2 * CPL];
+        ldvec<2 * CPL>(kj + (size_t)mm * Dq, kr);
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[c], s);
       }
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       const float P = expf(s * p.tau - lse[(size_t)i * p.H + head]);
@@ -106,12 +111,15 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KPar
       }
       float dp = 0.f;
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm)
+      for (int mm = 0; mm < M; ++mm) {
+        float vr[CPL];
+        ldvec<CPL>(vj + (size_t)mm * p.C, vr);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           dvr[mm][c] = fmaf(P, y[mm][c], dvr[mm][c]);
-          dp = fmaf(y[mm][c], vr[mm][c], dp);
+          dp = fmaf(y[mm][c], vr[c], dp);
         }
+      }
       for (int o = lph >> 1; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
       const float ds = P * (dp - delta[(size_t)i * p.H + head]);
       const float tds = p.tau * ds;
