@@ -43,16 +43,20 @@ constexpr int KV = MM * KC;  // 144: value MMA K  ((f, j))
 constexpr int NV = MM * HD;  // 144: value MMA N  ((o, c))
 constexpr int KMAX = 64;     // neighbour slots per atom held in shared memory
 
-// shared memory map (bytes)
-constexpr int SM_Q = 0;                                // 9 x [128 x 32] bf16, SW64     73728
-constexpr int SM_K = SM_Q + MM * TQ * DH * 2;          // 2 x 9 x [16 x 32] bf16, SW64  18432
-constexpr int SM_VST = SM_K + 2 * MM * KC * DH * 2;    // 2 x [16 keys][9][16] bf16      9216
-constexpr int SM_VT = SM_VST + 2 * KC * MM * HD * 2;   // [9][16 c][16 keys] bf16        4608
-constexpr int SM_WT = SM_VT + MM * HD * KC * 2;        // [128 x 144] core-matrix        36864
-constexpr int SM_VG = SM_WT + TQ * KV * 2;             // [144 x 144] core-matrix        41472
-constexpr int SM_NB = SM_VG + NV * KV * 2;             // [128][64] int32               32768
+// shared memory map (bytes), double-buffered K/V stages, Wt and Vg
+constexpr int KBYTES = MM * KC * DH * 2;               // 9 x [16 x 32] bf16 SW64   9216
+constexpr int VBYTES = KC * MM * HD * 2;               // [16 keys][9][16] bf16     4608
+constexpr int WBYTES = TQ * KV * 2;                    // [128 x 144] core-matrix   36864
+constexpr int GBYTES = NV * KV * 2;                    // [144 x 144] core-matrix   41472
+constexpr int SM_K = 0;                                // 2 x KBYTES
+constexpr int SM_VST = SM_K + 2 * KBYTES;              // 2 x VBYTES
+constexpr int SM_VT = SM_VST + 2 * VBYTES;             // VBYTES (transposed [9][16 c][16 keys])
+constexpr int SM_WT = 32768;                           // 2 x WBYTES
+constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
+constexpr int SM_NB = SM_VG + 2 * GBYTES;              // [128][64] int32
 constexpr int SM_BAR = SM_NB + TQ * KMAX * 4;
-constexpr int SM_TOTAL = SM_BAR + 128;
+constexpr int SM_TOTAL = SM_BAR + 256;
+static_assert(SM_VT + VBYTES <= SM_WT, "smem map overlap");
 
 struct TcTab {
   float ycoef[4];        // Y0, c1, c2, c20
@@ -93,50 +97,66 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
-// 256 threads: warps 0-3 own the 128 query rows (scores from TMEM, online
-// softmax with lazy rescale, Wt rows, epilogue); warps 4-7 build the per-key
-// source coupling Vg; thread 0 also drives TMA and the tcgen05 MMAs.  Chunk
-// g+1's TMA is in flight while chunk g is processed.
-__global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mq,
-                                                             const __grid_constant__ CUtensorMap mk,
-                                                             const __grid_constant__ CUtensorMap mv, TcArgs a,
-                                                             const double* __restrict__ pos,
-                                                             const int* __restrict__ nbr,
-                                                             const int* __restrict__ cptr,
-                                                             const int* __restrict__ clist, bf16* __restrict__ out,
-                                                             float* __restrict__ lse) {
+// Warp-specialised, double-buffered pipeline (288 threads):
+//   warp 0, one lane : TMA producer (K, V chunks) + tcgen05 MMA issuer
+//   warps 1-4        : the 128 query rows -- Q_h into TMEM, scores from TMEM,
+//                      online softmax with lazy rescale, Wt rows, epilogue
+//   warps 5-8        : per-key source coupling Vg
+// Q_h lives in tensor memory (the S MMA's A operand), which frees the shared
+// memory for two Wt/Vg buffers: chunk c+1's SIMT work overlaps chunk c's
+// value MMA.  TMEM: Q [0,144), O [160,304), S[2] [320,336) / [352,368).
+constexpr int TC_THREADS = 288;
+
+__global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
+    const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
+    const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
+    const int* __restrict__ cptr, const int* __restrict__ clist, bf16* __restrict__ out, float* __restrict__ lse) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar_q = reinterpret_cast<uint64_t*>(sm + SM_BAR);
-  uint64_t* bar_ld = bar_q + 1;  // [2]
-  uint64_t* bar_s = bar_q + 3;
-  uint64_t* bar_v = bar_q + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_q + 5);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
+  uint64_t* full_kv = bars + 0;   // [2] TMA landed (tx)
+  uint64_t* empty_kv = bars + 2;  // [2] S MMA done with K + Vg warps done with V (2 arrivals)
+  uint64_t* s_full = bars + 4;    // [2] S MMA committed
+  uint64_t* s_free = bars + 6;    // [2] rows read S (128)
+  uint64_t* wt_full = bars + 8;   // [2] rows wrote Wt (128)
+  uint64_t* vg_full = bars + 10;  // [2] Vg warps wrote Vg (128)
+  uint64_t* wv_free = bars + 12;  // [2] value MMA committed (Wt / Vg free, O updated)
+  uint64_t* q_ready = bars + 14;  // rows stored Q_h into TMEM (128)
+  uint64_t* acc_done = bars + 15; // last value MMA of the head committed
+  uint64_t* epi_done = bars + 16; // rows finished reading O (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 17);
   int* nbs = reinterpret_cast<int*>(sm + SM_NB);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool row_warp = warp < 4;
   const int q0 = blockIdx.x * TQ;
-  const int qi = q0 + (tid & 127);
-  const bool qvalid = row_warp && qi < a.N;
-  const int c_begin = cptr[blockIdx.x], c_end = cptr[blockIdx.x + 1];
-  const int nch = c_end - c_begin;
+  const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
+  const bool is_row = warp >= 1 && warp <= 4, is_vg = warp >= 5;
+  const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
+  const int qi = q0 + row;
+  const bool qvalid = is_row && qi < a.N;
 
   if (tid == 0) {
-    umma::prefetch_tmap(&mq);
     umma::prefetch_tmap(&mk);
     umma::prefetch_tmap(&mv);
-    umma::mbar_init(bar_q, 1);
-    umma::mbar_init(&bar_ld[0], 1);
-    umma::mbar_init(&bar_ld[1], 1);
-    umma::mbar_init(bar_s, 1);
-    umma::mbar_init(bar_v, 1);
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&full_kv[b], 1);
+      umma::mbar_init(&empty_kv[b], 2);
+      umma::mbar_init(&s_full[b], 1);
+      umma::mbar_init(&s_free[b], 128);
+      umma::mbar_init(&wt_full[b], 128);
+      umma::mbar_init(&vg_full[b], 128);
+      umma::mbar_init(&wv_free[b], 1);
+    }
+    umma::mbar_init(q_ready, 128);
+    umma::mbar_init(acc_done, 1);
+    umma::mbar_init(epi_done, 128);
     umma::fence_barrier_init();
   }
-  if (warp == 0) umma::tmem_alloc(tslot, 256);
+  if (warp == 0) umma::tmem_alloc(tslot, 512);
   int nn = 0;
-  int* my = nbs + (tid & 127) * KMAX;
-  if (qvalid) {  // this query's neighbours, ascending j (the index is consumed, never re-tested)
+  int* my = nbs + row * KMAX;
+  double pix = 0, piy = 0, piz = 0;
+  if (qvalid) {  // neighbours of this query, ascending j (the index is consumed, never re-tested)
     for (int s = 0; s < a.K && s < KMAX; ++s) {
       const int j = nbr[(size_t)qi * a.K + s];
       if (j < 0) continue;
@@ -144,9 +164,6 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
       while (p > 0 && my[p - 1] > j) { my[p] = my[p - 1]; --p; }
       my[p] = j;
     }
-  }
-  double pix = 0, piy = 0, piz = 0;
-  if (qvalid) {
     const int qa = a.row0 + qi;
     pix = pos[3 * qa]; piy = pos[3 * qa + 1]; piz = pos[3 * qa + 2];
   }
@@ -154,79 +171,111 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
   __syncthreads();
   umma::tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t t_out = tmem;      // cols [0, 144)
-  const uint32_t t_s = tmem + 192;  // cols [192, 208)
-  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t t_q = tmem, t_out = tmem + 160, t_s0 = tmem + 320;
   constexpr uint32_t idesc_s = umma::idesc_bf16(128, KC, 0, 0);
   constexpr uint32_t idesc_v = umma::idesc_bf16(128, NV, 0, 0);
-  constexpr uint32_t KBYTES = MM * KC * DH * 2, VBYTES = KC * MM * HD * 2;
 
-  auto issue_load = [&](int g, int ci, int h) {  // chunk ci (global chunk counter g) -> buffer g & 1
-    const int b = g & 1;
-    const int k0 = clist[ci] * KC;
-    uint8_t* kb = sm + SM_K + b * KBYTES;
-    umma::mbar_arrive_expect_tx(&bar_ld[b], KBYTES + VBYTES);
-    for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &bar_ld[b], DH * h, mm, k0);
-    umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &bar_ld[b], HD * h, 0, k0);
-  };
-
-  int g0 = 0;  // global chunk counter at the start of this head
-  for (int h = 0; h < 8; ++h) {
-    if (tid == 0) {
-      umma::mbar_arrive_expect_tx(bar_q, MM * TQ * DH * 2);
-      for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(sm + SM_Q + mm * TQ * DH * 2, &mq, bar_q, DH * h, mm, q0);
-      if (nch > 0) issue_load(g0, c_begin, h);
-    }
-    umma::mbar_wait(bar_q, h & 1);
-    float mu = -INFINITY, z = 0.f;
-    int ptr = 0;
-    for (int it = 0; it < nch; ++it) {
-      const int g = g0 + it, b = g & 1;
-      const int ci = c_begin + it;
-      const int k0 = clist[ci] * KC;
-      if (tid == 0) {
-        umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= producer + MMA issuer =================
+      auto load = [&](int g, int ci, int h) {
+        const int b = g & 1;
+        if (g >= 2) umma::mbar_wait(&empty_kv[b], ((g >> 1) - 1) & 1);
+        const int k0 = clist[ci] * KC;
+        uint8_t* kb = sm + SM_K + b * KBYTES;
+        umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES);
+        for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[b], DH * h, mm, k0);
+        umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &full_kv[b], HD * h, 0, k0);
+      };
+      auto value_mma = [&](int g, int c, int h) {
+        const int b = g & 1;
+        umma::mbar_wait(&wt_full[b], (g >> 1) & 1);
+        umma::mbar_wait(&vg_full[b], (g >> 1) & 1);
+        if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);  // O of the previous head read out
         umma::tc_fence_after();
-        const uint32_t qa = umma::smem_u32(sm + SM_Q), ka = umma::smem_u32(sm + SM_K + b * KBYTES);
+        const uint32_t wa = umma::smem_u32(sm + SM_WT + b * WBYTES), va = umma::smem_u32(sm + SM_VG + b * GBYTES);
 #pragma unroll
-        for (int s = 0; s < 2 * MM; ++s) {
-          const int mm = s >> 1, kk = s & 1;
-          umma::mma_f16(t_s, umma::sdesc(qa + mm * TQ * DH * 2 + kk * 32, 16, 512, 4),
-                        umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
+        for (int s = 0; s < MM; ++s)
+          umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
+                        umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
+        umma::mma_commit(&wv_free[b]);
+      };
+      int g0 = 0;
+      for (int h = 0; h < 8; ++h) {
+        if (nch > 0) load(g0, c_begin, h);
+        if (nch > 1) load(g0 + 1, c_begin + 1, h);
+        umma::mbar_wait(q_ready, h & 1);
+        for (int c = 0; c < nch; ++c) {
+          const int g = g0 + c, b = g & 1;
+          umma::mbar_wait(&full_kv[b], (g >> 1) & 1);
+          if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
+          umma::tc_fence_after();
+          const uint32_t ka = umma::smem_u32(sm + SM_K + b * KBYTES);
+#pragma unroll
+          for (int s = 0; s < 2 * MM; ++s) {
+            const int mm = s >> 1, kk = s & 1;
+            umma::mma_f16_ts(t_s0 + 32 * b, t_q + 8 * s,
+                             umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
+          }
+          umma::mma_commit(&s_full[b]);
+          umma::mma_commit(&empty_kv[b]);
+          if (c >= 1) value_mma(g - 1, c - 1, h);
+          if (c + 2 < nch) load(g + 2, c_begin + c + 2, h);
         }
-        umma::mma_commit(bar_s);
-        if (it + 1 < nch) issue_load(g + 1, ci + 1, h);  // prefetch next chunk into the other buffer
-      }
-      if (it > 0) umma::mbar_wait(bar_v, (g - 1) & 1);  // Wt / Vg / Vt free again
-      // ---- V chunk -> Vt [mm][c][key] (all warps), then the per-key source coupling
-      umma::mbar_wait(&bar_ld[b], (g >> 1) & 1);
-      {
-        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
-        bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
-        for (int e = tid; e < KC * MM * HD; e += 256) {
-          const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, c = rem % HD;
-          vt[(mm * HD + c) * KC + key] = vst[e];
+        if (nch > 0) {
+          value_mma(g0 + nch - 1, nch - 1, h);
+          umma::mma_commit(acc_done);
+        } else {
+          umma::mbar_arrive(acc_done);
         }
+        g0 += nch;
       }
-      __syncthreads();
-      if (row_warp) {
-        // ---- scores -> online softmax (lazy rescale) -> Wt row  (warps 0-3)
-        umma::mbar_wait(bar_s, g & 1);
+    }
+  } else if (is_row) {
+    // ================= query rows =================
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const bf16* qrow = q + (size_t)(qvalid ? qi : 0) * MM * 256;
+    int g0 = 0;
+    for (int h = 0; h < 8; ++h) {
+      // Q_h row -> TMEM (A operand): block mm = 16 columns of packed bf16 pairs
+#pragma unroll
+      for (int mm = 0; mm < MM; ++mm) {
+        uint32_t r[16];
+        const uint4* src = reinterpret_cast<const uint4*>(qrow + mm * 256 + DH * h);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint4 u = qvalid ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
+          r[4 * t] = u.x; r[4 * t + 1] = u.y; r[4 * t + 2] = u.z; r[4 * t + 3] = u.w;
+        }
+        umma::tmem_st16(t_q + lane_base + 16 * mm, r);
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(q_ready);
+      float mu = -INFINITY, z = 0.f;
+      int ptr = 0;
+      for (int c = 0; c < nch; ++c) {
+        const int g = g0 + c, b = g & 1;
+        const int k0 = clist[c_begin + c] * KC;
+        umma::mbar_wait(&s_full[b], (g >> 1) & 1);
         umma::tc_fence_after();
         uint32_t sr[16];
-        umma::tmem_ld16(t_s + lane_base, sr);
+        umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
+        umma::tc_fence_before();
+        umma::mbar_arrive(&s_free[b]);
         unsigned vmask = 0;
         while (ptr < nn && my[ptr] < k0) ++ptr;
         while (ptr < nn && my[ptr] < k0 + KC) { vmask |= 1u << (my[ptr] - k0); ++ptr; }
         float mc = -INFINITY;
         for (int t = 0; t < KC; ++t)
           if (vmask >> t & 1) mc = fmaxf(mc, a.tau * __uint_as_float(sr[t]));
-        // rescale only when the running max grows by more than e^5 (rows are independent)
         const bool need = (mu > -INFINITY) && (mc > mu + 5.f);
         float factor = 1.f;
         if (mu == -INFINITY && mc > -INFINITY) mu = mc;
         else if (need) { factor = __expf(mu - mc); mu = mc; z *= factor; }
-        if (__any_sync(0xffffffffu, need)) {  // warp-collective TMEM read-modify-write
+        if (__any_sync(0xffffffffu, need)) {
+          // O must be quiescent: every value MMA up to chunk c-1 complete (c >= 1 here)
+          umma::mbar_wait(&wv_free[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          umma::tc_fence_after();
 #pragma unroll
           for (int cc = 0; cc < NV / 16; ++cc) {
             uint32_t r[16];
@@ -235,7 +284,10 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
             for (int t = 0; t < 16; ++t) r[t] = __float_as_uint(__uint_as_float(r[t]) * factor);
             umma::tmem_st16(t_out + lane_base + cc * 16, r);
           }
+          umma::tc_fence_before();
         }
+        if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
+        uint8_t* wt = sm + SM_WT + b * WBYTES;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           float w[MM][8];
@@ -268,62 +320,14 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
           }
 #pragma unroll
           for (int f = 0; f < MM; ++f)
-            *reinterpret_cast<uint4*>(sm + SM_WT + cm_off(tid, f * KC + half * 8)) = pack8(w[f]);
+            *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + half * 8)) = pack8(w[f]);
         }
+        umma::fence_proxy_async();
+        umma::mbar_arrive(&wt_full[b]);
       }
-      {
-        // Vg[(o,c),(f,j)] = sum_i' G_f[o,i'] v_j[i',c]; o split over the 8 warps
-        // (rows: o = 0..3, others: o = 4..8), compile-time sparsity (_gen_cg.h)
-        const int c = lane & 15, j0 = (lane >> 4) * 8;
-        const bf16* vt = reinterpret_cast<const bf16*>(sm + SM_VT);
-        float v8[MM][8];
-#pragma unroll
-        for (int ip = 0; ip < MM; ++ip) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c) * KC + j0);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float2 fv = __bfloat1622float2(b2[t]);
-            v8[ip][2 * t] = fv.x;
-            v8[ip][2 * t + 1] = fv.y;
-          }
-        }
-        auto emit = [&](int o, const float (&acc)[MM][8]) {
-#pragma unroll
-          for (int f = 0; f < MM; ++f)
-            *reinterpret_cast<uint4*>(sm + SM_VG + cm_off(o * HD + c, f * KC + j0)) = pack8(acc[f]);
-        };
-        float acc[MM][8];
-        switch (warp) {
-          case 0: es_vg_o0(v8, acc); emit(0, acc); break;
-          case 1: es_vg_o1(v8, acc); emit(1, acc); break;
-          case 2: es_vg_o2(v8, acc); emit(2, acc); break;
-          case 3: es_vg_o3(v8, acc); emit(3, acc); break;
-          case 4: es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
-          case 5: es_vg_o5(v8, acc); emit(5, acc); break;
-          case 6: es_vg_o6(v8, acc); emit(6, acc); break;
-          default: es_vg_o7(v8, acc); emit(7, acc); break;
-        }
-      }
-      umma::fence_proxy_async();
-      umma::tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        umma::tc_fence_after();
-        const uint32_t wa = umma::smem_u32(sm + SM_WT), va = umma::smem_u32(sm + SM_VG);
-#pragma unroll
-        for (int s = 0; s < MM; ++s)  // K = 144 = 9 steps of 16 (2 core-matrix columns each)
-          umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
-                        umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (it > 0 || s > 0) ? 1u : 0u);
-        umma::mma_commit(bar_v);
-      }
-    }
-    // ---- epilogue (rows): O_h / z
-    if (nch > 0) {
-      umma::mbar_wait(bar_v, (g0 + nch - 1) & 1);
+      // ---- epilogue: O_h / z
+      umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
-    }
-    if (row_warp) {
       const float inv = z > 0.f ? 1.f / z : 0.f;
       if (qvalid) lse[(size_t)qi * 8 + h] = z > 0.f ? mu + __logf(z) : -INFINITY;
 #pragma unroll
@@ -339,13 +343,63 @@ __global__ void __launch_bounds__(256, 1) attn_fwd_tc_kernel(const __grid_consta
           dst[1] = pack8(v + 8);
         }
       }
+      umma::tc_fence_before();
+      umma::mbar_arrive(epi_done);
+      g0 += nch;
     }
-    g0 += nch;
-    umma::tc_fence_before();
-    __syncthreads();
-    umma::tc_fence_after();
+  } else {
+    // ================= per-key source coupling (warps 5-8) =================
+    const int vw = warp - 5;
+    const int c16 = lane & 15, j0 = (lane >> 4) * 8;
+    int g0 = 0;
+    for (int h = 0; h < 8; ++h) {
+      for (int c = 0; c < nch; ++c) {
+        const int g = g0 + c, b = g & 1;
+        umma::mbar_wait(&full_kv[b], (g >> 1) & 1);
+        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
+        bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
+        for (int e = tid - 160; e < KC * MM * HD; e += 128) {
+          const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, cc = rem % HD;
+          vt[(mm * HD + cc) * KC + key] = vst[e];
+        }
+        umma::named_bar(1, 128);
+        if (tid == 160) umma::mbar_arrive(&empty_kv[b]);  // V stage b consumed
+        float v8[MM][8];
+#pragma unroll
+        for (int ip = 0; ip < MM; ++ip) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c16) * KC + j0);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float2 fv = __bfloat1622float2(b2[t]);
+            v8[ip][2 * t] = fv.x;
+            v8[ip][2 * t + 1] = fv.y;
+          }
+        }
+        umma::named_bar(1, 128);  // Vt reusable by the next chunk
+        if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Vg buffer b free
+        uint8_t* vg = sm + SM_VG + b * GBYTES;
+        auto emit = [&](int o, const float (&acc)[MM][8]) {
+#pragma unroll
+          for (int f = 0; f < MM; ++f)
+            *reinterpret_cast<uint4*>(vg + cm_off(o * HD + c16, f * KC + j0)) = pack8(acc[f]);
+        };
+        float acc[MM][8];
+        switch (vw) {  // o split: {0,4,8} {1,5} {2,6} {3,7}
+          case 0: es_vg_o0(v8, acc); emit(0, acc); es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
+          case 1: es_vg_o1(v8, acc); emit(1, acc); es_vg_o5(v8, acc); emit(5, acc); break;
+          case 2: es_vg_o2(v8, acc); emit(2, acc); es_vg_o6(v8, acc); emit(6, acc); break;
+          default: es_vg_o3(v8, acc); emit(3, acc); es_vg_o7(v8, acc); emit(7, acc); break;
+        }
+        umma::fence_proxy_async();
+        umma::mbar_arrive(&vg_full[b]);
+      }
+      g0 += nch;
+    }
   }
-  if (warp == 0) umma::tmem_dealloc(tmem, 256);
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, 512);
 }
 
 // ---------------------------------------------------------------- tile chunk lists
@@ -492,9 +546,8 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
 
-  CUtensorMap mq, mk, mv;
-  if (!map3(&mq, q, 256, MM, a.N, DH, 1, TQ, CU_TENSOR_MAP_SWIZZLE_64B) ||
-      !map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
+  CUtensorMap mk, mv;
+  if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
       !map3(&mv, v, 128, MM, a.Nk, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
     return fail(ES_CUDA_ERROR, "attn_fwd_tc: tensor map encode failed");
   TcArgs ta;
@@ -507,7 +560,8 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
     cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_fwd_tc_kernel<<<ntiles, 256, smem, st>>>(mq, mk, mv, ta, pos, nbr, cptr, clist, (bf16*)out, lse);
+  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, (bf16*)out,
+                                                        lse);
   s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
   cudaFreeAsync(base, st);
   return s;
