@@ -97,22 +97,23 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
-// Warp-specialised, double-buffered pipeline (288 threads):
-//   warp 0, one lane : TMA producer (K, V chunks) + tcgen05 MMA issuer
+// Warp-specialised, double-buffered pipeline (320 threads):
+//   warp 0, one lane : TMA producer (K, V chunks)
+//   warp 9, one lane : tcgen05 MMA issuer
 //   warps 1-4        : the 128 query rows -- Q_h into TMEM, scores from TMEM,
 //                      online softmax with lazy rescale, Wt rows, epilogue
 //   warps 5-8        : per-key source coupling Vg
 // Q_h lives in tensor memory (the S MMA's A operand), which frees the shared
 // memory for two Wt/Vg buffers: chunk c+1's SIMT work overlaps chunk c's
 // value MMA.  TMEM: Q [0,144), O [160,304), S[2] [320,336) / [352,368).
-constexpr int TC_THREADS = 288;
+constexpr int TC_THREADS = 320;
 
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
     const int* __restrict__ cptr, const int* __restrict__ clist, bf16* __restrict__ out, float* __restrict__ lse) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
   uint64_t* full_kv = bars + 0;   // [2] TMA landed (tx)
   uint64_t* empty_kv = bars + 2;  // [2] S MMA done with K + Vg warps done with V (2 arrivals)
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * TQ;
   const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
-  const bool is_row = warp >= 1 && warp <= 4, is_vg = warp >= 5;
+  const bool is_row = warp >= 1 && warp <= 4;
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
   const int qi = q0 + row;
   const bool qvalid = is_row && qi < a.N;
@@ -177,16 +178,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
 
   if (warp == 0) {
     if (lane == 0) {
-      // ================= producer + MMA issuer =================
-      auto load = [&](int g, int ci, int h) {
-        const int b = g & 1;
-        if (g >= 2) umma::mbar_wait(&empty_kv[b], ((g >> 1) - 1) & 1);
-        const int k0 = clist[ci] * KC;
-        uint8_t* kb = sm + SM_K + b * KBYTES;
-        umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES);
-        for (int mm = 0; mm < MM; ++mm) umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[b], DH * h, mm, k0);
-        umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &full_kv[b], HD * h, 0, k0);
-      };
+      // ================= TMA producer =================
+      int g0 = 0;
+      for (int h = 0; h < 8; ++h) {
+        for (int c = 0; c < nch; ++c) {
+          const int g = g0 + c, b = g & 1;
+          if (g >= 2) umma::mbar_wait(&empty_kv[b], ((g >> 1) - 1) & 1);
+          const int k0 = clist[c_begin + c] * KC;
+          uint8_t* kb = sm + SM_K + b * KBYTES;
+          umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES);
+          for (int mm = 0; mm < MM; ++mm)
+            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[b], DH * h, mm, k0);
+          umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &full_kv[b], HD * h, 0, k0);
+        }
+        g0 += nch;
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      // ================= MMA issuer =================
       auto value_mma = [&](int g, int c, int h) {
         const int b = g & 1;
         umma::mbar_wait(&wt_full[b], (g >> 1) & 1);
@@ -202,8 +212,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       };
       int g0 = 0;
       for (int h = 0; h < 8; ++h) {
-        if (nch > 0) load(g0, c_begin, h);
-        if (nch > 1) load(g0 + 1, c_begin + 1, h);
         umma::mbar_wait(q_ready, h & 1);
         for (int c = 0; c < nch; ++c) {
           const int g = g0 + c, b = g & 1;
@@ -220,7 +228,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           umma::mma_commit(&s_full[b]);
           umma::mma_commit(&empty_kv[b]);
           if (c >= 1) value_mma(g - 1, c - 1, h);
-          if (c + 2 < nch) load(g + 2, c_begin + c + 2, h);
         }
         if (nch > 0) {
           value_mma(g0 + nch - 1, nch - 1, h);
@@ -358,7 +365,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::mbar_wait(&full_kv[b], (g >> 1) & 1);
         const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
         bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
-        for (int e = tid - 160; e < KC * MM * HD; e += 128) {
+        for (int e = tid - 160; e < KC * MM * HD; e += 128) {  // warps 5-8: tid 160..287
           const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, cc = rem % HD;
           vt[(mm * HD + cc) * KC + key] = vst[e];
         }

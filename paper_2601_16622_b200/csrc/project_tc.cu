@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(128) proj_fwd_tc_kernel(const __grid_constant_
                                                           bf16* __restrict__ q, bf16* __restrict__ k,
                                                           bf16* __restrict__ v) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
   uint8_t* Bs = smem + 32768;         // [2 kb][2 nb][64 k-rows][64] bf16, 8 KB each
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 65536);
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap mwk, TcP p,
                                                          bf16* __restrict__ dh) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDhStages * 32768);
   uint64_t* empty = full + kDhStages;
   uint64_t* done = empty + kDhStages;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__
                                                          const __grid_constant__ CUtensorMap mdv, TcP p, int l,
                                                          int nb, int atoms_per_split, float* __restrict__ dW) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   const int R = (2 * l + 1) * nb;
   const int half = R * 128;       // one 64-wide MN block: R rows x 128 B
   const int stage_bytes = 4 * half;
