@@ -51,12 +51,14 @@ constexpr int GBYTES = NV * KV * 2;                    // [144 x 144] core-matri
 constexpr int SM_K = 0;                                // 2 x KBYTES
 constexpr int SM_VST = SM_K + 2 * KBYTES;              // 2 x VBYTES
 constexpr int SM_VT = SM_VST + 2 * VBYTES;             // VBYTES (transposed [9][16 c][16 keys])
-constexpr int SM_WT = 32768;                           // 2 x WBYTES
+constexpr int SM_POS = SM_VT + VBYTES;                 // 2 x [16 keys][3] f64 (chunk key positions)
+constexpr int SM_WT = 33792;                           // 2 x WBYTES
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
-constexpr int SM_NB = SM_VG + 2 * GBYTES;              // [128][64] int32
-constexpr int SM_BAR = SM_NB + TQ * KMAX * 4;
+constexpr int NB_STRIDE = KMAX + 1;                    // padded: conflict-free per-row walks
+constexpr int SM_NB = SM_VG + 2 * GBYTES;              // [128][65] int32
+constexpr int SM_BAR = SM_NB + TQ * NB_STRIDE * 4;
 constexpr int SM_TOTAL = SM_BAR + 256;
-static_assert(SM_VT + VBYTES <= SM_WT, "smem map overlap");
+static_assert(SM_POS + 2 * KC * 24 <= SM_WT, "smem map overlap");
 
 struct TcTab {
   float ycoef[4];        // Y0, c1, c2, c20
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
   uint64_t* full_kv = bars + 0;   // [2] TMA landed (tx)
-  uint64_t* empty_kv = bars + 2;  // [2] S MMA done with K + Vg warps done with V (2 arrivals)
+  uint64_t* empty_kv = bars + 2;  // [2] S MMA done with K + Vg warps done with V + rows done with key pos (130)
   uint64_t* s_full = bars + 4;    // [2] S MMA committed
   uint64_t* s_free = bars + 6;    // [2] rows read S (128)
   uint64_t* wt_full = bars + 8;   // [2] rows wrote Wt (128)
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     umma::prefetch_tmap(&mv);
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&full_kv[b], 1);
-      umma::mbar_init(&empty_kv[b], 2);
+      umma::mbar_init(&empty_kv[b], 2 + 128);
       umma::mbar_init(&s_full[b], 1);
       umma::mbar_init(&s_free[b], 128);
       umma::mbar_init(&wt_full[b], 128);
@@ -155,7 +157,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
   int nn = 0;
-  int* my = nbs + row * KMAX;
+  int* my = nbs + row * NB_STRIDE;
   double pix = 0, piy = 0, piz = 0;
   if (qvalid) {  // neighbours of this query, ascending j (the index is consumed, never re-tested)
     for (int s = 0; s < a.K && s < KMAX; ++s) {
@@ -186,10 +188,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           if (g >= 2) umma::mbar_wait(&empty_kv[b], ((g >> 1) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           uint8_t* kb = sm + SM_K + b * KBYTES;
-          umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES);
+          const int nkeys = min(KC, a.Nk - k0);
+          const uint32_t pbytes = (uint32_t)((nkeys * 24 + 15) & ~15);  // chunk key positions (contiguous atoms)
+          umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES + pbytes);
           for (int mm = 0; mm < MM; ++mm)
             umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[b], DH * h, mm, k0);
           umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &full_kv[b], HD * h, 0, k0);
+          umma::bulk_load(sm + SM_POS + b * (KC * 24), pos + 3 * (size_t)k0, pbytes, &full_kv[b]);
         }
         g0 += nch;
       }
@@ -264,7 +269,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         const int g = g0 + c, b = g & 1;
         const int k0 = clist[c_begin + c] * KC;
         umma::mbar_wait(&s_full[b], (g >> 1) & 1);
+        umma::mbar_wait(&full_kv[b], (g >> 1) & 1);  // chunk key positions landed (already complete)
         umma::tc_fence_after();
+        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + b * (KC * 24));
         uint32_t sr[16];
         umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
         umma::tc_fence_before();
@@ -302,8 +309,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           for (int t = 0; t < 8; ++t) {
             const int kk = half * 8 + t;
             if (vmask >> kk & 1) {
-              const int j = k0 + kk;
-              double dx = pos[3 * j] - pix, dy = pos[3 * j + 1] - piy, dz = pos[3 * j + 2] - piz;
+              double dx = kpos[3 * kk] - pix, dy = kpos[3 * kk + 1] - piy, dz = kpos[3 * kk + 2] - piz;
               if (a.periodic) {
                 dx -= a.bx * rint(dx / a.bx);
                 dy -= a.by * rint(dy / a.by);
@@ -331,6 +337,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         }
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
+        umma::mbar_arrive(&empty_kv[b]);  // done with this stage's key positions
       }
       // ---- epilogue: O_h / z
       umma::mbar_wait(acc_done, h & 1);
