@@ -21,6 +21,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include <cub/cub.cuh>
 
@@ -43,22 +44,22 @@ constexpr int KV = MM * KC;  // 144: value MMA K  ((f, j))
 constexpr int NV = MM * HD;  // 144: value MMA N  ((o, c))
 constexpr int KMAX = 64;     // neighbour slots per atom held in shared memory
 
-// shared memory map (bytes), double-buffered K/V stages, Wt and Vg
+// shared memory map (bytes): 3 K/V/pos stages, double-buffered Wt and Vg
+constexpr int NSTAGE = 3;
 constexpr int KBYTES = MM * KC * DH * 2;               // 9 x [16 x 32] bf16 SW64   9216
 constexpr int VBYTES = KC * MM * HD * 2;               // [16 keys][9][16] bf16     4608
+constexpr int PBYTES = KC * 24;                        // [16 keys][3] f64          384
 constexpr int WBYTES = TQ * KV * 2;                    // [128 x 144] core-matrix   36864
 constexpr int GBYTES = NV * KV * 2;                    // [144 x 144] core-matrix   41472
-constexpr int SM_K = 0;                                // 2 x KBYTES
-constexpr int SM_VST = SM_K + 2 * KBYTES;              // 2 x VBYTES
-constexpr int SM_VT = SM_VST + 2 * VBYTES;             // VBYTES (transposed [9][16 c][16 keys])
-constexpr int SM_POS = SM_VT + VBYTES;                 // 2 x [16 keys][3] f64 (chunk key positions)
-constexpr int SM_WT = 33792;                           // 2 x WBYTES
+constexpr int SM_K = 0;                                // NSTAGE x KBYTES
+constexpr int SM_VST = SM_K + NSTAGE * KBYTES;         // NSTAGE x VBYTES
+constexpr int SM_VT = SM_VST + NSTAGE * VBYTES;        // VBYTES (transposed [9][16 c][16 keys])
+constexpr int SM_POS = SM_VT + VBYTES;                 // NSTAGE x PBYTES (chunk key positions)
+constexpr int SM_WT = 48128;                           // 2 x WBYTES
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
-constexpr int NB_STRIDE = KMAX + 1;                    // padded: conflict-free per-row walks
-constexpr int SM_NB = SM_VG + 2 * GBYTES;              // [128][65] int32
-constexpr int SM_BAR = SM_NB + TQ * NB_STRIDE * 4;
+constexpr int SM_BAR = SM_VG + 2 * GBYTES;
 constexpr int SM_TOTAL = SM_BAR + 256;
-static_assert(SM_POS + 2 * KC * 24 <= SM_WT, "smem map overlap");
+static_assert(SM_POS + NSTAGE * PBYTES <= SM_WT, "smem map overlap");
 
 struct TcTab {
   float ycoef[4];        // Y0, c1, c2, c20
@@ -70,6 +71,7 @@ __constant__ TcTab c_tc;
 
 struct TcArgs {
   int N, K, row0, Nk;
+  int dbg;  // profiling switches (ES_TC_DBG): 1 skip Vg math, 2 skip Wt math, 4 skip value MMA, 8 skip S MMA
   float tau, r_cut, inv_rcut;
   int phi_mode, periodic;
   double bx, by, bz;
@@ -99,36 +101,36 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
-// Warp-specialised, double-buffered pipeline (320 threads):
-//   warp 0, one lane : TMA producer (K, V chunks)
+// Warp-specialised pipeline (320 threads):
+//   warp 0, one lane : TMA producer (K, V, key positions; 3 stages)
 //   warp 9, one lane : tcgen05 MMA issuer
 //   warps 1-4        : the 128 query rows -- Q_h into TMEM, scores from TMEM,
 //                      online softmax with lazy rescale, Wt rows, epilogue
 //   warps 5-8        : per-key source coupling Vg
-// Q_h lives in tensor memory (the S MMA's A operand), which frees the shared
-// memory for two Wt/Vg buffers: chunk c+1's SIMT work overlaps chunk c's
-// value MMA.  TMEM: Q [0,144), O [160,304), S[2] [320,336) / [352,368).
+// Q_h lives in tensor memory (the S MMA's A operand); Wt and Vg are double
+// buffered, so chunk c+1's SIMT work overlaps chunk c's value MMA.
+// TMEM: Q [0,144), O [160,304), S[2] [320,336) / [352,368).
 constexpr int TC_THREADS = 320;
 
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
-    const int* __restrict__ cptr, const int* __restrict__ clist, bf16* __restrict__ out, float* __restrict__ lse) {
+    const int* __restrict__ cptr, const int* __restrict__ clist, int* __restrict__ nsort, bf16* __restrict__ out,
+    float* __restrict__ lse) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
-  uint64_t* full_kv = bars + 0;   // [2] TMA landed (tx)
-  uint64_t* empty_kv = bars + 2;  // [2] S MMA done with K + Vg warps done with V + rows done with key pos (130)
-  uint64_t* s_full = bars + 4;    // [2] S MMA committed
-  uint64_t* s_free = bars + 6;    // [2] rows read S (128)
-  uint64_t* wt_full = bars + 8;   // [2] rows wrote Wt (128)
-  uint64_t* vg_full = bars + 10;  // [2] Vg warps wrote Vg (128)
-  uint64_t* wv_free = bars + 12;  // [2] value MMA committed (Wt / Vg free, O updated)
-  uint64_t* q_ready = bars + 14;  // rows stored Q_h into TMEM (128)
-  uint64_t* acc_done = bars + 15; // last value MMA of the head committed
-  uint64_t* epi_done = bars + 16; // rows finished reading O (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 17);
-  int* nbs = reinterpret_cast<int*>(sm + SM_NB);
+  uint64_t* full_kv = bars + 0;    // [3] TMA landed (tx)
+  uint64_t* empty_kv = bars + 3;   // [3] S MMA done with K + Vg warps with V + rows with key pos (130)
+  uint64_t* s_full = bars + 6;     // [2] S MMA committed
+  uint64_t* s_free = bars + 8;     // [2] rows read S (128)
+  uint64_t* wt_full = bars + 10;   // [2] rows wrote Wt (128)
+  uint64_t* vg_full = bars + 12;   // [2] Vg warps wrote Vg (128)
+  uint64_t* wv_free = bars + 14;   // [2] value MMA committed (Wt / Vg free, O updated)
+  uint64_t* q_ready = bars + 16;   // rows stored Q_h into TMEM (128)
+  uint64_t* acc_done = bars + 17;  // last value MMA of the head committed
+  uint64_t* epi_done = bars + 18;  // rows finished reading O (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 19);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * TQ;
@@ -141,9 +143,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   if (tid == 0) {
     umma::prefetch_tmap(&mk);
     umma::prefetch_tmap(&mv);
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NSTAGE; ++b) {
       umma::mbar_init(&full_kv[b], 1);
       umma::mbar_init(&empty_kv[b], 2 + 128);
+    }
+    for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&s_full[b], 1);
       umma::mbar_init(&s_free[b], 128);
       umma::mbar_init(&wt_full[b], 128);
@@ -157,9 +161,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
   int nn = 0;
-  int* my = nbs + row * NB_STRIDE;
+  int* my = nsort + (size_t)qi * KMAX;  // this query's neighbours, ascending j (global scratch, L1-resident)
   double pix = 0, piy = 0, piz = 0;
-  if (qvalid) {  // neighbours of this query, ascending j (the index is consumed, never re-tested)
+  if (qvalid) {
     for (int s = 0; s < a.K && s < KMAX; ++s) {
       const int j = nbr[(size_t)qi * a.K + s];
       if (j < 0) continue;
@@ -184,17 +188,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       int g0 = 0;
       for (int h = 0; h < 8; ++h) {
         for (int c = 0; c < nch; ++c) {
-          const int g = g0 + c, b = g & 1;
-          if (g >= 2) umma::mbar_wait(&empty_kv[b], ((g >> 1) - 1) & 1);
+          const int g = g0 + c, st = g % NSTAGE;
+          if (g >= NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
-          uint8_t* kb = sm + SM_K + b * KBYTES;
           const int nkeys = min(KC, a.Nk - k0);
-          const uint32_t pbytes = (uint32_t)((nkeys * 24 + 15) & ~15);  // chunk key positions (contiguous atoms)
-          umma::mbar_arrive_expect_tx(&full_kv[b], KBYTES + VBYTES + pbytes);
+          const uint32_t pbytes = (uint32_t)((nkeys * 24 + 15) & ~15);
+          uint8_t* kb = sm + SM_K + st * KBYTES;
+          umma::mbar_arrive_expect_tx(&full_kv[st], KBYTES + VBYTES + pbytes);
           for (int mm = 0; mm < MM; ++mm)
-            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[b], DH * h, mm, k0);
-          umma::tma_load_3d(sm + SM_VST + b * VBYTES, &mv, &full_kv[b], HD * h, 0, k0);
-          umma::bulk_load(sm + SM_POS + b * (KC * 24), pos + 3 * (size_t)k0, pbytes, &full_kv[b]);
+            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
+          umma::tma_load_3d(sm + SM_VST + st * VBYTES, &mv, &full_kv[st], HD * h, 0, k0);
+          umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
         }
         g0 += nch;
       }
@@ -209,29 +213,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);  // O of the previous head read out
         umma::tc_fence_after();
         const uint32_t wa = umma::smem_u32(sm + SM_WT + b * WBYTES), va = umma::smem_u32(sm + SM_VG + b * GBYTES);
+        if (!(a.dbg & 4))
 #pragma unroll
-        for (int s = 0; s < MM; ++s)
-          umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
-                        umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
+          for (int s = 0; s < MM; ++s)
+            umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
+                          umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
         umma::mma_commit(&wv_free[b]);
       };
       int g0 = 0;
       for (int h = 0; h < 8; ++h) {
         umma::mbar_wait(q_ready, h & 1);
         for (int c = 0; c < nch; ++c) {
-          const int g = g0 + c, b = g & 1;
-          umma::mbar_wait(&full_kv[b], (g >> 1) & 1);
+          const int g = g0 + c, b = g & 1, st = g % NSTAGE;
+          umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
           if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
           umma::tc_fence_after();
-          const uint32_t ka = umma::smem_u32(sm + SM_K + b * KBYTES);
+          const uint32_t ka = umma::smem_u32(sm + SM_K + st * KBYTES);
+          if (!(a.dbg & 8))
 #pragma unroll
-          for (int s = 0; s < 2 * MM; ++s) {
-            const int mm = s >> 1, kk = s & 1;
-            umma::mma_f16_ts(t_s0 + 32 * b, t_q + 8 * s,
-                             umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
-          }
+            for (int s = 0; s < 2 * MM; ++s) {
+              const int mm = s >> 1, kk = s & 1;
+              umma::mma_f16_ts(t_s0 + 32 * b, t_q + 8 * s,
+                               umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
+            }
           umma::mma_commit(&s_full[b]);
-          umma::mma_commit(&empty_kv[b]);
+          umma::mma_commit(&empty_kv[st]);
           if (c >= 1) value_mma(g - 1, c - 1, h);
         }
         if (nch > 0) {
@@ -249,37 +255,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const bf16* qrow = q + (size_t)(qvalid ? qi : 0) * MM * 256;
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
-      // Q_h row -> TMEM (A operand): block mm = 16 columns of packed bf16 pairs
+      // Q_h row -> TMEM (A operand): block mm = 16 columns of packed bf16 pairs; 3 batches of loads
 #pragma unroll
-      for (int mm = 0; mm < MM; ++mm) {
-        uint32_t r[16];
-        const uint4* src = reinterpret_cast<const uint4*>(qrow + mm * 256 + DH * h);
+      for (int m0 = 0; m0 < MM; m0 += 3) {
+        uint32_t r[3][16];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const uint4 u = qvalid ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
-          r[4 * t] = u.x; r[4 * t + 1] = u.y; r[4 * t + 2] = u.z; r[4 * t + 3] = u.w;
+        for (int d = 0; d < 3; ++d) {
+          const uint4* src = reinterpret_cast<const uint4*>(qrow + (m0 + d) * 256 + DH * h);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint4 u = qvalid ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
+            r[d][4 * t] = u.x; r[d][4 * t + 1] = u.y; r[d][4 * t + 2] = u.z; r[d][4 * t + 3] = u.w;
+          }
         }
-        umma::tmem_st16(t_q + lane_base + 16 * mm, r);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) umma::tmem_st16(t_q + lane_base + 16 * (m0 + d), r[d]);
       }
       umma::tc_fence_before();
       umma::mbar_arrive(q_ready);
       float mu = -INFINITY, z = 0.f;
       int ptr = 0;
       for (int c = 0; c < nch; ++c) {
-        const int g = g0 + c, b = g & 1;
+        const int g = g0 + c, b = g & 1, st = g % NSTAGE;
         const int k0 = clist[c_begin + c] * KC;
         umma::mbar_wait(&s_full[b], (g >> 1) & 1);
-        umma::mbar_wait(&full_kv[b], (g >> 1) & 1);  // chunk key positions landed (already complete)
+        umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);  // key positions landed (already complete)
         umma::tc_fence_after();
-        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + b * (KC * 24));
+        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
         uint32_t sr[16];
         umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
         unsigned vmask = 0;
-        while (ptr < nn && my[ptr] < k0) ++ptr;
-        while (ptr < nn && my[ptr] < k0 + KC) { vmask |= 1u << (my[ptr] - k0); ++ptr; }
+        while (ptr < nn && __ldg(my + ptr) < k0) ++ptr;
+        while (ptr < nn) {
+          const int j = __ldg(my + ptr);
+          if (j >= k0 + KC) break;
+          vmask |= 1u << (j - k0);
+          ++ptr;
+        }
         float mc = -INFINITY;
+#pragma unroll
         for (int t = 0; t < KC; ++t)
           if (vmask >> t & 1) mc = fmaxf(mc, a.tau * __uint_as_float(sr[t]));
         const bool need = (mu > -INFINITY) && (mc > mu + 5.f);
@@ -302,42 +318,39 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         }
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
         uint8_t* wt = sm + SM_WT + b * WBYTES;
+        // zero row, then scatter the (few) valid pairs: the warp iterates
+        // max-popcount times instead of over all 16 keys
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float w[MM][8];
-#pragma unroll
-          for (int t = 0; t < 8; ++t) {
-            const int kk = half * 8 + t;
-            if (vmask >> kk & 1) {
-              double dx = kpos[3 * kk] - pix, dy = kpos[3 * kk + 1] - piy, dz = kpos[3 * kk + 2] - piz;
-              if (a.periodic) {
-                dx -= a.bx * rint(dx / a.bx);
-                dy -= a.by * rint(dy / a.by);
-                dz -= a.bz * rint(dz / a.bz);
-              }
-              const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
-              const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
-              float phi = 1.f;
-              if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
-              const float P = __expf(a.tau * __uint_as_float(sr[kk]) - mu);
-              z += P;
-              float y[MM];
-              solid_l2(rx, ry, rz, y);
-              const float pp = P * phi;
-#pragma unroll
-              for (int f = 0; f < MM; ++f) w[f][t] = pp * y[f];
-            } else {
-#pragma unroll
-              for (int f = 0; f < MM; ++f) w[f][t] = 0.f;
-            }
+        for (int f = 0; f < MM; ++f) {
+          *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC)) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8)) = make_uint4(0, 0, 0, 0);
+        }
+        unsigned m = (a.dbg & 2) ? 0u : vmask;
+        while (m) {
+          const int kk = __ffs(m) - 1;
+          m &= m - 1;
+          double dx = kpos[3 * kk] - pix, dy = kpos[3 * kk + 1] - piy, dz = kpos[3 * kk + 2] - piz;
+          if (a.periodic) {
+            dx -= a.bx * rint(dx / a.bx);
+            dy -= a.by * rint(dy / a.by);
+            dz -= a.bz * rint(dz / a.bz);
           }
+          const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+          const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+          float phi = 1.f;
+          if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
+          const float P = __expf(a.tau * __uint_as_float(sr[kk]) - mu);
+          z += P;
+          float y[MM];
+          solid_l2(rx, ry, rz, y);
+          const float pp = P * phi;
 #pragma unroll
           for (int f = 0; f < MM; ++f)
-            *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + half * 8)) = pack8(w[f]);
+            *reinterpret_cast<bf16*>(wt + cm_off(row, f * KC + kk)) = __float2bfloat16_rn(pp * y[f]);
         }
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
-        umma::mbar_arrive(&empty_kv[b]);  // done with this stage's key positions
+        umma::mbar_arrive(&empty_kv[st]);  // done with this stage's key positions
       }
       // ---- epilogue: O_h / z
       umma::mbar_wait(acc_done, h & 1);
@@ -363,21 +376,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     }
   } else {
     // ================= per-key source coupling (warps 5-8) =================
-    const int vw = warp - 5;
+    const int vw = warp - 5, vt_id = tid - 160;
     const int c16 = lane & 15, j0 = (lane >> 4) * 8;
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
       for (int c = 0; c < nch; ++c) {
-        const int g = g0 + c, b = g & 1;
-        umma::mbar_wait(&full_kv[b], (g >> 1) & 1);
-        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + b * VBYTES);
+        const int g = g0 + c, b = g & 1, st = g % NSTAGE;
+        umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
+        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + st * VBYTES);
         bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
-        for (int e = tid - 160; e < KC * MM * HD; e += 128) {  // warps 5-8: tid 160..287
-          const int key = e / (MM * HD), rem = e % (MM * HD), mm = rem / HD, cc = rem % HD;
-          vt[(mm * HD + cc) * KC + key] = vst[e];
+        // transpose [key][mm][c] -> [mm][c][key]: one (key, mm) row of 16 channels per thread
+        for (int r2 = vt_id; r2 < KC * MM; r2 += 128) {
+          const int key = r2 / MM, mm = r2 - key * MM;
+          const uint4 u0 = *reinterpret_cast<const uint4*>(vst + r2 * HD);
+          const uint4 u1 = *reinterpret_cast<const uint4*>(vst + r2 * HD + 8);
+          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+          unsigned short* vts = reinterpret_cast<unsigned short*>(vt);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            vts[(mm * HD + 2 * cc) * KC + key] = (unsigned short)(w[cc] & 0xffffu);
+            vts[(mm * HD + 2 * cc + 1) * KC + key] = (unsigned short)(w[cc] >> 16);
+          }
         }
         umma::named_bar(1, 128);
-        if (tid == 160) umma::mbar_arrive(&empty_kv[b]);  // V stage b consumed
+        if (vt_id == 0) umma::mbar_arrive(&empty_kv[st]);  // V stage consumed
         float v8[MM][8];
 #pragma unroll
         for (int ip = 0; ip < MM; ++ip) {
@@ -399,11 +421,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             *reinterpret_cast<uint4*>(vg + cm_off(o * HD + c16, f * KC + j0)) = pack8(acc[f]);
         };
         float acc[MM][8];
-        switch (vw) {  // o split: {0,4,8} {1,5} {2,6} {3,7}
-          case 0: es_vg_o0(v8, acc); emit(0, acc); es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
-          case 1: es_vg_o1(v8, acc); emit(1, acc); es_vg_o5(v8, acc); emit(5, acc); break;
-          case 2: es_vg_o2(v8, acc); emit(2, acc); es_vg_o6(v8, acc); emit(6, acc); break;
-          default: es_vg_o3(v8, acc); emit(3, acc); es_vg_o7(v8, acc); emit(7, acc); break;
+        if (a.dbg & 1) {
+#pragma unroll
+          for (int x = 0; x < MM; ++x)
+#pragma unroll
+            for (int t = 0; t < 8; ++t) acc[x][t] = v8[x][t];
+          emit(vw, acc);
+        } else {
+          switch (vw) {  // o split: {0,4,8} {1,5} {2,6} {3,7}
+            case 0: es_vg_o0(v8, acc); emit(0, acc); es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
+            case 1: es_vg_o1(v8, acc); emit(1, acc); es_vg_o5(v8, acc); emit(5, acc); break;
+            case 2: es_vg_o2(v8, acc); emit(2, acc); es_vg_o6(v8, acc); emit(6, acc); break;
+            default: es_vg_o3(v8, acc); emit(3, acc); es_vg_o7(v8, acc); emit(7, acc); break;
+          }
         }
         umma::fence_proxy_async();
         umma::mbar_arrive(&vg_full[b]);
@@ -538,7 +568,8 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   size_t cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, ntiles + 1);
   const size_t bytes = align256((size_t)ntiles * words * 4) + 2 * align256((size_t)(ntiles + 1) * 4) +
-                       align256((size_t)ntiles * per_tile * 4) + align256(cub_bytes);
+                       align256((size_t)ntiles * per_tile * 4) + align256(cub_bytes) +
+                       align256((size_t)ntiles * TQ * KMAX * 4);
   char* base = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&base, bytes, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_fwd_tc: scratch");
@@ -551,6 +582,8 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   int* clist = (int*)(base + off);
   off += align256((size_t)ntiles * per_tile * 4);
   void* cub_ws = base + off;
+  off += align256(cub_bytes);
+  int* nsort = (int*)(base + off);
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
   s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
@@ -565,7 +598,11 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
       !map3(&mv, v, 128, MM, a.Nk, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
     return fail(ES_CUDA_ERROR, "attn_fwd_tc: tensor map encode failed");
   TcArgs ta;
-  ta.N = a.N; ta.K = a.K; ta.row0 = a.row0; ta.Nk = a.Nk; ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
+  ta.N = a.N; ta.K = a.K; ta.row0 = a.row0; ta.Nk = a.Nk;
+  {
+    const char* e = getenv("ES_TC_DBG");
+    ta.dbg = e ? atoi(e) : 0;
+  } ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
   ta.phi_mode = a.phi_mode; ta.periodic = a.periodic;
   ta.bx = a.box[0]; ta.by = a.box[1]; ta.bz = a.box[2];
   const int smem = SM_TOTAL + 1024;
@@ -574,8 +611,8 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
     cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, (bf16*)out,
-                                                        lse);
+  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, nsort,
+                                                        (bf16*)out, lse);
   s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
   cudaFreeAsync(base, st);
   return s;
