@@ -109,7 +109,8 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 //   warps 5-8        : per-key source coupling Vg
 // Q_h lives in tensor memory (the S MMA's A operand); Wt and Vg are double
 // buffered, so chunk c+1's SIMT work overlaps chunk c's value MMA.
-// TMEM: Q [0,144), O [160,304), S[2] [320,336) / [352,368).
+// TMEM: Q[2] [0,144) / [144,288) (next head's Q is loaded by the Vg warps
+// while the current head runs), O [288,432), S[2] [448,464) / [480,496).
 constexpr int TC_THREADS = 320;
 
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
@@ -127,10 +128,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   uint64_t* wt_full = bars + 10;   // [2] rows wrote Wt (128)
   uint64_t* vg_full = bars + 12;   // [2] Vg warps wrote Vg (128)
   uint64_t* wv_free = bars + 14;   // [2] value MMA committed (Wt / Vg free, O updated)
-  uint64_t* q_ready = bars + 16;   // rows stored Q_h into TMEM (128)
   uint64_t* acc_done = bars + 17;  // last value MMA of the head committed
   uint64_t* epi_done = bars + 18;  // rows finished reading O (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 19);
+  uint64_t* q_ready = bars + 19;   // [2] Q_h stored into TMEM buffer h&1 (128, Vg warps)
+  uint64_t* q_free = bars + 21;    // [2] last S MMA reading Q buffer committed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 23);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * TQ;
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
   const int qi = q0 + row;
   const bool qvalid = is_row && qi < a.N;
+  const bool qin = qi < a.N;  // row exists (Vg warps load Q rows too)
 
   if (tid == 0) {
     umma::prefetch_tmap(&mk);
@@ -154,7 +157,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       umma::mbar_init(&vg_full[b], 128);
       umma::mbar_init(&wv_free[b], 1);
     }
-    umma::mbar_init(q_ready, 128);
+    umma::mbar_init(&q_ready[0], 128);
+    umma::mbar_init(&q_ready[1], 128);
+    umma::mbar_init(&q_free[0], 1);
+    umma::mbar_init(&q_free[1], 1);
     umma::mbar_init(acc_done, 1);
     umma::mbar_init(epi_done, 128);
     umma::fence_barrier_init();
@@ -178,7 +184,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   __syncthreads();
   umma::tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t t_q = tmem, t_out = tmem + 160, t_s0 = tmem + 320;
+  const uint32_t t_q0 = tmem, t_out = tmem + 288, t_s0 = tmem + 448;  // Q[2] at 0 / 144
   constexpr uint32_t idesc_s = umma::idesc_bf16(128, KC, 0, 0);
   constexpr uint32_t idesc_v = umma::idesc_bf16(128, NV, 0, 0);
 
@@ -220,59 +226,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
                           umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
         umma::mma_commit(&wv_free[b]);
       };
+      auto issue_s = [&](int g, int h, bool last) {
+        const int b = g & 1, st = g % NSTAGE;
+        umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
+        if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
+        umma::tc_fence_after();
+        const uint32_t ka = umma::smem_u32(sm + SM_K + st * KBYTES);
+        const uint32_t tq = t_q0 + 144 * (h & 1);
+        if (!(a.dbg & 8))
+#pragma unroll
+          for (int s = 0; s < 2 * MM; ++s) {
+            const int mm = s >> 1, kk = s & 1;
+            umma::mma_f16_ts(t_s0 + 32 * b, tq + 8 * s, umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4),
+                             idesc_s, s > 0 ? 1u : 0u);
+          }
+        umma::mma_commit(&s_full[b]);
+        umma::mma_commit(&empty_kv[st]);
+        if (last) umma::mma_commit(&q_free[h & 1]);
+      };
       int g0 = 0;
       for (int h = 0; h < 8; ++h) {
-        umma::mbar_wait(q_ready, h & 1);
+        umma::mbar_wait(&q_ready[h & 1], (h >> 1) & 1);
+        if (nch > 0) issue_s(g0, h, nch == 1);
+        else umma::mbar_arrive(&q_free[h & 1]);
         for (int c = 0; c < nch; ++c) {
-          const int g = g0 + c, b = g & 1, st = g % NSTAGE;
-          umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
-          if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
-          umma::tc_fence_after();
-          const uint32_t ka = umma::smem_u32(sm + SM_K + st * KBYTES);
-          if (!(a.dbg & 8))
-#pragma unroll
-            for (int s = 0; s < 2 * MM; ++s) {
-              const int mm = s >> 1, kk = s & 1;
-              umma::mma_f16_ts(t_s0 + 32 * b, t_q + 8 * s,
-                               umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4), idesc_s, s > 0 ? 1u : 0u);
-            }
-          umma::mma_commit(&s_full[b]);
-          umma::mma_commit(&empty_kv[st]);
-          if (c >= 1) value_mma(g - 1, c - 1, h);
+          // S of the next chunk first, so the rows never wait behind a value MMA
+          if (c + 1 < nch) issue_s(g0 + c + 1, h, c + 2 == nch);
+          value_mma(g0 + c, c, h);
         }
-        if (nch > 0) {
-          value_mma(g0 + nch - 1, nch - 1, h);
-          umma::mma_commit(acc_done);
-        } else {
-          umma::mbar_arrive(acc_done);
-        }
+        if (nch > 0) umma::mma_commit(acc_done);
+        else umma::mbar_arrive(acc_done);
         g0 += nch;
       }
     }
   } else if (is_row) {
     // ================= query rows =================
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const bf16* qrow = q + (size_t)(qvalid ? qi : 0) * MM * 256;
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
-      // Q_h row -> TMEM (A operand): block mm = 16 columns of packed bf16 pairs; 3 batches of loads
-#pragma unroll
-      for (int m0 = 0; m0 < MM; m0 += 3) {
-        uint32_t r[3][16];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const uint4* src = reinterpret_cast<const uint4*>(qrow + (m0 + d) * 256 + DH * h);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint4 u = qvalid ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
-            r[d][4 * t] = u.x; r[d][4 * t + 1] = u.y; r[d][4 * t + 2] = u.z; r[d][4 * t + 3] = u.w;
-          }
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) umma::tmem_st16(t_q + lane_base + 16 * (m0 + d), r[d]);
-      }
-      umma::tc_fence_before();
-      umma::mbar_arrive(q_ready);
       float mu = -INFINITY, z = 0.f;
       int ptr = 0;
       for (int c = 0; c < nch; ++c) {
@@ -287,9 +278,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
         unsigned vmask = 0;
-        while (ptr < nn && __ldg(my + ptr) < k0) ++ptr;
+        while (ptr < nn && my[ptr] < k0) ++ptr;
         while (ptr < nn) {
-          const int j = __ldg(my + ptr);
+          const int j = my[ptr];
           if (j >= k0 + KC) break;
           vmask |= 1u << (j - k0);
           ++ptr;
@@ -378,8 +369,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     // ================= per-key source coupling (warps 5-8) =================
     const int vw = warp - 5, vt_id = tid - 160;
     const int c16 = lane & 15, j0 = (lane >> 4) * 8;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const bf16* qrow = q + (size_t)(qin ? qi : 0) * MM * 256;
+    auto load_q = [&](int hh) {  // Q_hh row -> TMEM buffer hh&1 (A operand, packed bf16 pairs)
+      const uint32_t tq = t_q0 + 144 * (hh & 1);
+#pragma unroll
+      for (int m0 = 0; m0 < MM; m0 += 3) {
+        uint32_t r[3][16];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const uint4* src = reinterpret_cast<const uint4*>(qrow + (m0 + d) * 256 + DH * hh);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint4 u = qin ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
+            r[d][4 * t] = u.x; r[d][4 * t + 1] = u.y; r[d][4 * t + 2] = u.z; r[d][4 * t + 3] = u.w;
+          }
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) umma::tmem_st16(tq + lane_base + 16 * (m0 + d), r[d]);
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(&q_ready[hh & 1]);
+    };
+    load_q(0);
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
+      if (h + 1 < 8) {
+        if (h >= 1) umma::mbar_wait(&q_free[(h + 1) & 1], ((h - 1) >> 1) & 1);  // head h-1's S MMAs done
+        load_q(h + 1);
+      }
       for (int c = 0; c < nch; ++c) {
         const int g = g0 + c, b = g & 1, st = g % NSTAGE;
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
