@@ -191,10 +191,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   if (warp == 0) {
     if (lane == 0) {
       // ================= TMA producer =================
+      // L2 prefetch runs PF chunks ahead of the shared-memory stages (hides HBM latency)
+      constexpr int PF = 4;
+      auto prefetch = [&](int h, int c) {
+        const int k0 = clist[c_begin + c] * KC;
+        for (int mm = 0; mm < MM; ++mm) umma::tma_prefetch_3d(&mk, DH * h, mm, k0);
+        umma::tma_prefetch_3d(&mv, HD * h, 0, k0);
+      };
+      for (int c = 0; c < nch && c < PF; ++c) prefetch(0, c);
       int g0 = 0;
       for (int h = 0; h < 8; ++h) {
         for (int c = 0; c < nch; ++c) {
           const int g = g0 + c, st = g % NSTAGE;
+          {  // prefetch chunk c + PF (possibly of the next head)
+            const int cp = c + PF;
+            if (cp < nch) prefetch(h, cp);
+            else if (h + 1 < 8 && cp - nch < nch) prefetch(h + 1, cp - nch);
+          }
           if (g >= NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           const int nkeys = min(KC, a.Nk - k0);
