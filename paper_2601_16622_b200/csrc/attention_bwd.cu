@@ -102,7 +102,7 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
         for (int c = 0; c < CPL; ++c) y[mm][c] = 0.f;
       }
       if constexpr (EAAS) {
-        eaas_apply<L, CPL, true>(rec, g, phi, y);
+        value_apply<L, CPL, true>(rec, g, phi, y);
       } else {
 #pragma unroll
         for (int mm = 0; mm < M; ++mm)
@@ -138,25 +138,70 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
 }
 
 // Query-centric pass: dq_i = tau * sum_slot ds[i,slot,h] k_j.  Each thread
-// owns 8 consecutive q-channels of one (l,m) row (one head), loads them as
-// one vector per valid neighbour.
+// owns 8 consecutive q-channels of one (l,m) row (one head).  Warp 0 first
+// compacts the valid slots of row i (ballot over the row, so any sentinel
+// pattern works) and their per-head dscore rows into shared memory; the
+// gather loop then runs over valid pairs only, UNR k_j rows in flight.
 template <typename T>
 __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, int Dq, float tau,
                                                           const T* __restrict__ k, const int* __restrict__ nbr,
                                                           const float* __restrict__ dsbuf, T* __restrict__ dq) {
+  constexpr int UNR = 4;
+  extern __shared__ int bq_smem[];
+  int* js = bq_smem;                                   // [K]
+  float* dss = reinterpret_cast<float*>(bq_smem + K);  // [K][H]
+  __shared__ int nvalid;
   const int i = blockIdx.x;
   const int dqh = Dq / H;
   const int n = M * Dq;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int cnt = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int s = base + lane;
+      const int j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
+      const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
+      if (j >= 0) {
+        const int p = cnt + __popc(m & ((1u << lane) - 1u));
+        js[p] = j;
+        const float* src = dsbuf + ((size_t)i * K + s) * H;
+        if ((H & 3) == 0) {
+          for (int h = 0; h < H; h += 4)
+            *reinterpret_cast<float4*>(dss + p * H + h) = __ldg(reinterpret_cast<const float4*>(src + h));
+        } else {
+          for (int h = 0; h < H; ++h) dss[p * H + h] = __ldg(src + h);
+        }
+      }
+      cnt += __popc(m);
+    }
+    if (lane == 0) nvalid = cnt;
+  }
+  __syncthreads();
+  const int nv = nvalid;
   for (int e0 = threadIdx.x * 8; e0 < n; e0 += blockDim.x * 8) {
     const int h = (e0 % Dq) / dqh;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < K; ++s) {
-      const int j = __ldg(nbr + (size_t)i * K + s);
-      if (j < 0) continue;
-      const float ds = __ldg(dsbuf + ((size_t)i * K + s) * H + h);
+    int e = 0;
+    for (; e + UNR <= nv; e += UNR) {
+      float kv[UNR][8];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const T* kp = k + (size_t)js[e + u] * n + e0;
+        ldvec<4>(kp, kv[u]);
+        ldvec<4>(kp + 4, kv[u] + 4);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const float ds = dss[(e + u) * H + h];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) acc[t] = fmaf(ds, kv[u][t], acc[t]);
+      }
+    }
+    for (; e < nv; ++e) {
+      const float ds = dss[e * H + h];
       float kv[8];
-      ldvec<4>(k + (size_t)j * n + e0, kv);
-      ldvec<4>(k + (size_t)j * n + e0 + 4, kv + 4);
+      ldvec<4>(k + (size_t)js[e] * n + e0, kv);
+      ldvec<4>(k + (size_t)js[e] * n + e0 + 4, kv + 4);
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] = fmaf(ds, kv[t], acc[t]);
     }
@@ -166,7 +211,6 @@ __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, i
     stvec<4>(dq + (size_t)i * n + e0 + 4, acc + 4);
   }
 }
-
 
 template <int L, int CPL, bool EAAS, typename T>
 es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
@@ -192,7 +236,11 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   {
     int tq = (M * kp.Dq / 8 + 31) / 32 * 32;
     if (tq > 1024) tq = 1024;
-    attn_bwd_q_kernel<T><<<kp.N, tq, 0, st>>>(M, kp.K, kp.H, kp.Dq, kp.tau, (const T*)k, nbr, dsbuf, (T*)dq);
+    const size_t qsm = (size_t)kp.K * (1 + kp.H) * 4;
+    if (qsm > 200 * 1024) return fail(ES_UNSUPPORTED, "attn_bwd: K * (H + 1) too large for the dq pass");
+    if (qsm > 48 * 1024)
+      cudaFuncSetAttribute(attn_bwd_q_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
+    attn_bwd_q_kernel<T><<<kp.N, tq, qsm, st>>>(M, kp.K, kp.H, kp.Dq, kp.tau, (const T*)k, nbr, dsbuf, (T*)dq);
   }
   return cuda_status(cudaGetLastError(), "attn_bwd_q_kernel");
 }

@@ -17,9 +17,10 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
   constexpr int REC = LY::REC;
   constexpr int BP = LY::BP;
   extern __shared__ float4 smem4[];
+  __shared__ int cnt_w[32];
   float* recs = reinterpret_cast<float*>(smem4);
   float* sc = recs + BP * REC;  // [BP][H]
-
+  const int tpq = blockDim.x;
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = (warp * 32 + lane) * CPL;  // first value channel of this lane
@@ -39,19 +40,53 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
   float mu = -INFINITY, z = 0.f;
 
   for (int base = 0; base < p.K; base += BP) {
-    const int nb = min(BP, p.K - base);
+    const int nslot = min(BP, p.K - base);
     __syncthreads();
-    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-      const int j = nbr[(size_t)i * p.K + base + t];
-      float* rec = recs + t * REC;
-      if (j >= 0) pair_prepare<L, EAAS>(p, pos, i, j, rec);
-      else rec[LY::OFF_J] = __int_as_float(-1);
+    // compact this batch's valid slots: rec e < nb holds the e-th valid pair
+    int nb = 0;
+    for (int t0 = 0; t0 < nslot; t0 += tpq) {
+      const int t = t0 + warp * 32 + lane;
+      const int j = t < nslot ? nbr[(size_t)i * p.K + base + t] : -1;
+      const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
+      if (lane == 0) cnt_w[warp] = __popc(m);
+      __syncthreads();
+      int before = nb;
+      for (int w = 0; w < warp; ++w) before += cnt_w[w];
+      int tot = 0;
+      for (int w = 0; w < (tpq >> 5); ++w) tot += cnt_w[w];
+      if (j >= 0) pair_prepare<L, EAAS>(p, pos, i, j, recs + (before + __popc(m & ((1u << lane) - 1u))) * REC);
+      nb += tot;
+      __syncthreads();
     }
-    __syncthreads();
-    // phase A: scores of this warp's heads for the whole batch
-    for (int e = 0; e < nb; ++e) {
+    if (nb == 0) continue;
+    // phase A: scores of this warp's heads for the whole batch (two pairs in flight)
+    int e = 0;
+    for (; e + 2 <= nb; e += 2) {
+      const int j0 = __float_as_int(recs[e * REC + LY::OFF_J]);
+      const int j1 = __float_as_int(recs[(e + 1) * REC + LY::OFF_J]);
+      float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+      for (int mm = 0; mm < M; ++mm) {
+        float k0[2 * CPL], k1[2 * CPL];
+        ldvec<2 * CPL>(k + ((size_t)j0 * M + mm) * Dq + 2 * c0, k0);
+        ldvec<2 * CPL>(k + ((size_t)j1 * M + mm) * Dq + 2 * c0, k1);
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) {
+          s0 = fmaf(qr[mm][c], k0[c], s0);
+          s1 = fmaf(qr[mm][c], k1[c], s1);
+        }
+      }
+      for (int o = lph >> 1; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      if ((lane % lph) == 0) {
+        sc[e * p.H + head] = s0 * p.tau;
+        sc[(e + 1) * p.H + head] = s1 * p.tau;
+      }
+    }
+    for (; e < nb; ++e) {
       const int j = __float_as_int(recs[e * REC + LY::OFF_J]);
-      if (j < 0) continue;
       float s = 0.f;
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
@@ -65,9 +100,7 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
     }
     __syncwarp();
     float bm = -INFINITY;
-    for (int e = 0; e < nb; ++e)
-      if (__float_as_int(recs[e * REC + LY::OFF_J]) >= 0) bm = fmaxf(bm, sc[e * p.H + head]);
-    if (bm == -INFINITY) continue;
+    for (int e2 = 0; e2 < nb; ++e2) bm = fmaxf(bm, sc[e2 * p.H + head]);
     const float mu2 = fmaxf(mu, bm);
     const float scale = __expf(mu - mu2);  // mu = -inf -> 0
     z *= scale;
@@ -77,18 +110,22 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
       for (int c = 0; c < CPL; ++c) A[mm][c] *= scale;
     mu = mu2;
     // phase B: values
-    for (int e = 0; e < nb; ++e) {
-      const float* rec = recs + e * REC;
+    for (int e2 = 0; e2 < nb; ++e2) {
+      const float* rec = recs + e2 * REC;
       const int j = __float_as_int(rec[LY::OFF_J]);
-      if (j < 0) continue;
-      const float pr = expf(sc[e * p.H + head] - mu);
+      if (e2 + 1 < nb) {
+        const int jn = __float_as_int(recs[(e2 + 1) * REC + LY::OFF_J]);
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm) pf_l1(v + ((size_t)jn * M + mm) * p.C + c0);
+      }
+      const float pr = expf(sc[e2 * p.H + head] - mu);
       z += pr;
       const float s = pr * rec[LY::OFF_PHI];
       float vv[M][CPL];
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) ldvec<CPL>(v + ((size_t)j * M + mm) * p.C + c0, vv[mm]);
       if constexpr (EAAS) {
-        eaas_apply<L, CPL, false>(rec, vv, s, A);
+        value_apply<L, CPL, false>(rec, vv, s, A);
       } else {
 #pragma unroll
         for (int mm = 0; mm < M; ++mm)
@@ -112,11 +149,11 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
 template <int L, int CPL, bool EAAS, typename T>
 es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
                   const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
-  const int threads = kp.C / CPL;
+  const int tpq = kp.C / CPL;
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)Lay<L>::BP * kp.H * 4;
   auto fn = attn_fwd_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fn<<<kp.N, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
+  fn<<<kp.N, tpq, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_kernel");
 }
 

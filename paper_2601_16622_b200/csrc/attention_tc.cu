@@ -42,7 +42,6 @@ constexpr int DH = 32;       // q/k channels per head per (l,m) row
 constexpr int MM = 9;        // (L+1)^2, L = 2
 constexpr int KV = MM * KC;  // 144: value MMA K  ((f, j))
 constexpr int NV = MM * HD;  // 144: value MMA N  ((o, c))
-constexpr int KMAX = 64;     // neighbour slots per atom held in shared memory
 
 // shared memory map (bytes): 3 K/V/pos stages, double-buffered Wt and Vg
 constexpr int NSTAGE = 3;
@@ -58,7 +57,9 @@ constexpr int SM_POS = SM_VT + VBYTES;                 // NSTAGE x PBYTES (chunk
 constexpr int SM_WT = 48128;                           // 2 x WBYTES
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
 constexpr int SM_BAR = SM_VG + 2 * GBYTES;
-constexpr int SM_TOTAL = SM_BAR + 256;
+constexpr int SM_PROW = SM_BAR + 256;                  // [128 rows][16 keys] f32 softmax numerators
+constexpr int SM_QPOS = SM_PROW + TQ * KC * 4;         // [128 rows][3] f64 query positions
+constexpr int SM_TOTAL = SM_QPOS + TQ * 24;
 static_assert(SM_POS + NSTAGE * PBYTES <= SM_WT, "smem map overlap");
 
 struct TcTab {
@@ -68,6 +69,7 @@ struct TcTab {
   int ofs[MM * MM + 1];  // (o, f) -> entry range
 };
 __constant__ TcTab c_tc;
+__device__ long long g_trace[8][128];  // ES_TC_DBG&16: per-chunk event clocks of CTA 0
 
 struct TcArgs {
   int N, K, row0, Nk;
@@ -116,8 +118,8 @@ constexpr int TC_THREADS = 320;
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
-    const int* __restrict__ cptr, const int* __restrict__ clist, int* __restrict__ nsort, bf16* __restrict__ out,
-    float* __restrict__ lse) {
+    const int* __restrict__ cptr, const int* __restrict__ clist, const uint32_t* __restrict__ rowlist,
+    bf16* __restrict__ out, float* __restrict__ lse) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * TQ;
+  const bool TRACE = (a.dbg & 16) && blockIdx.x == 0;
   const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
   const bool is_row = warp >= 1 && warp <= 4;
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
@@ -166,19 +169,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     umma::fence_barrier_init();
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
-  int nn = 0;
-  int* my = nsort + (size_t)qi * KMAX;  // this query's neighbours, ascending j (global scratch, L1-resident)
-  double pix = 0, piy = 0, piz = 0;
-  if (qvalid) {
-    for (int s = 0; s < a.K && s < KMAX; ++s) {
-      const int j = nbr[(size_t)qi * a.K + s];
-      if (j < 0) continue;
-      int p = nn++;
-      while (p > 0 && my[p - 1] > j) { my[p] = my[p - 1]; --p; }
-      my[p] = j;
-    }
-    const int qa = a.row0 + qi;
-    pix = pos[3 * qa]; piy = pos[3 * qa + 1]; piz = pos[3 * qa + 2];
+  double* qpos = reinterpret_cast<double*>(sm + SM_QPOS);
+  if (is_row) {
+    const int qa = a.row0 + (qin ? qi : 0);
+    qpos[3 * row] = qin ? pos[3 * qa] : 0.0;
+    qpos[3 * row + 1] = qin ? pos[3 * qa + 1] : 0.0;
+    qpos[3 * row + 2] = qin ? pos[3 * qa + 2] : 0.0;
   }
   umma::tc_fence_before();
   __syncthreads();
@@ -217,6 +213,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           for (int mm = 0; mm < MM; ++mm)
             umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
           umma::tma_load_3d(sm + SM_VST + st * VBYTES, &mv, &full_kv[st], HD * h, 0, k0);
+        if (TRACE && true && g < 128) g_trace[0][g] = clock64();
           umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
         }
         g0 += nch;
@@ -238,6 +235,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
                           umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
         umma::mma_commit(&wv_free[b]);
+        if (TRACE && true && g < 128) g_trace[6][g] = clock64();
       };
       auto issue_s = [&](int g, int h, bool last) {
         const int b = g & 1, st = g % NSTAGE;
@@ -254,6 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
                              idesc_s, s > 0 ? 1u : 0u);
           }
         umma::mma_commit(&s_full[b]);
+        if (TRACE && true && g < 128) g_trace[1][g] = clock64();
         umma::mma_commit(&empty_kv[st]);
         if (last) umma::mma_commit(&q_free[h & 1]);
       };
@@ -275,29 +274,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   } else if (is_row) {
     // ================= query rows =================
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const int wrow0 = (warp & 3) * 32;  // first tile row of this warp
+    float* prow = reinterpret_cast<float*>(sm + SM_PROW);
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
       float mu = -INFINITY, z = 0.f;
-      int ptr = 0;
+      // this row's (chunk, key-mask) list, ascending chunk, 0xffff terminator
+      const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * a.K;
+      int rp = 0;
+      uint32_t ent = qin ? __ldg(rl) : 0xffff0000u;
       for (int c = 0; c < nch; ++c) {
         const int g = g0 + c, b = g & 1, st = g % NSTAGE;
-        const int k0 = clist[c_begin + c] * KC;
+        unsigned vmask = 0u;
+        if ((int)(ent >> 16) == c) {
+          vmask = ent & 0xffffu;
+          ++rp;
+          ent = rp < a.K ? __ldg(rl + rp) : 0xffff0000u;
+        }
         umma::mbar_wait(&s_full[b], (g >> 1) & 1);
+        if (TRACE && tid == 32 && g < 128) g_trace[2][g] = clock64();
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);  // key positions landed (already complete)
         umma::tc_fence_after();
-        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
         uint32_t sr[16];
         umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
-        unsigned vmask = 0;
-        while (ptr < nn && my[ptr] < k0) ++ptr;
-        while (ptr < nn) {
-          const int j = my[ptr];
-          if (j >= k0 + KC) break;
-          vmask |= 1u << (j - k0);
-          ++ptr;
-        }
         float mc = -INFINITY;
 #pragma unroll
         for (int t = 0; t < KC; ++t)
@@ -320,40 +321,74 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           }
           umma::tc_fence_before();
         }
+        // softmax numerators of this row (0 for non-neighbours) -> shared memory
+        float pr[KC];
+#pragma unroll
+        for (int t = 0; t < KC; ++t) {
+          pr[t] = (vmask >> t & 1) ? __expf(a.tau * __uint_as_float(sr[t]) - mu) : 0.f;
+          z += pr[t];
+        }
+        float4* pdst = reinterpret_cast<float4*>(prow + row * KC);
+#pragma unroll
+        for (int t = 0; t < KC / 4; ++t) pdst[t] = make_float4(pr[4 * t], pr[4 * t + 1], pr[4 * t + 2], pr[4 * t + 3]);
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
         uint8_t* wt = sm + SM_WT + b * WBYTES;
-        // zero row, then scatter the (few) valid pairs: the warp iterates
-        // max-popcount times instead of over all 16 keys
 #pragma unroll
         for (int f = 0; f < MM; ++f) {
           *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC)) = make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8)) = make_uint4(0, 0, 0, 0);
         }
-        unsigned m = (a.dbg & 2) ? 0u : vmask;
-        while (m) {
-          const int kk = __ffs(m) - 1;
-          m &= m - 1;
-          double dx = kpos[3 * kk] - pix, dy = kpos[3 * kk + 1] - piy, dz = kpos[3 * kk + 2] - piz;
-          if (a.periodic) {
-            dx -= a.bx * rint(dx / a.bx);
-            dy -= a.by * rint(dy / a.by);
-            dz -= a.bz * rint(dz / a.bz);
-          }
-          const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
-          const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
-          float phi = 1.f;
-          if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
-          const float P = __expf(a.tau * __uint_as_float(sr[kk]) - mu);
-          z += P;
-          float y[MM];
-          solid_l2(rx, ry, rz, y);
-          const float pp = P * phi;
+        __syncwarp();
+        // warp-cooperative geometry: the warp's valid (row, key) pairs are
+        // compacted (prefix sum of the row popcounts) and dealt one per lane
+        const unsigned vm = (a.dbg & 2) ? 0u : vmask;
+        const int cnt = __popc(vm);
+        int incl = cnt;
 #pragma unroll
-          for (int f = 0; f < MM; ++f)
-            *reinterpret_cast<bf16*>(wt + cm_off(row, f * KC + kk)) = __float2bfloat16_rn(pp * y[f]);
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
         }
+        const int excl = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
+        for (int base = 0; base < total; base += 32) {
+          const int idx = base + lane;
+          int owner = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int e = __shfl_sync(0xffffffffu, excl, owner + step);
+            if (e <= idx) owner += step;
+          }
+          unsigned om = __shfl_sync(0xffffffffu, vm, owner);
+          const int oex = __shfl_sync(0xffffffffu, excl, owner);
+          if (idx < total) {
+            for (int r = idx - oex; r > 0; --r) om &= om - 1;
+            const int kk = __ffs(om) - 1;
+            const int orow = wrow0 + owner;
+            double dx = kpos[3 * kk] - qpos[3 * orow], dy = kpos[3 * kk + 1] - qpos[3 * orow + 1],
+                   dz = kpos[3 * kk + 2] - qpos[3 * orow + 2];
+            if (a.periodic) {
+              dx -= a.bx * rint(dx / a.bx);
+              dy -= a.by * rint(dy / a.by);
+              dz -= a.bz * rint(dz / a.bz);
+            }
+            const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+            const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+            float phi = 1.f;
+            if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
+            float y[MM];
+            solid_l2(rx, ry, rz, y);
+            const float pp = prow[orow * KC + kk] * phi;
+#pragma unroll
+            for (int f = 0; f < MM; ++f)
+              *reinterpret_cast<bf16*>(wt + cm_off(orow, f * KC + kk)) = __float2bfloat16_rn(pp * y[f]);
+          }
+        }
+        __syncwarp();
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
+        if (TRACE && tid == 32 && g < 128) g_trace[3][g] = clock64();
         umma::mbar_arrive(&empty_kv[st]);  // done with this stage's key positions
       }
       // ---- epilogue: O_h / z
@@ -414,6 +449,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       for (int c = 0; c < nch; ++c) {
         const int g = g0 + c, b = g & 1, st = g % NSTAGE;
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
+        if (TRACE && vt_id == 0 && g < 128) g_trace[4][g] = clock64();
         const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + st * VBYTES);
         bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
         // transpose [key][mm][c] -> [mm][c][key]: one (key, mm) row of 16 channels per thread
@@ -468,6 +504,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         }
         umma::fence_proxy_async();
         umma::mbar_arrive(&vg_full[b]);
+        if (TRACE && vt_id == 0 && g < 128) g_trace[5][g] = clock64();
       }
       g0 += nch;
     }
@@ -475,6 +512,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 512);
+  if (TRACE && tid == 0) {
+    for (int g = 0; g < 128 && g < 8 * nch; ++g)
+      printf("TRACE g=%d tma=%lld sI=%lld sR=%lld wt=%lld vgS=%lld vgD=%lld vI=%lld\n", g, g_trace[0][g],
+             g_trace[1][g], g_trace[2][g], g_trace[3][g], g_trace[4][g], g_trace[5][g], g_trace[6][g]);
+  }
 }
 
 // ---------------------------------------------------------------- tile chunk lists
@@ -512,6 +554,39 @@ __global__ void tc_fill_kernel(int ntiles, int words, const uint32_t* __restrict
     }
     base += __shfl_sync(0xffffffffu, incl, 31);
   }
+}
+
+// Per query row: its valid neighbours folded into (tile chunk index << 16 | 16-bit key
+// mask) entries, ascending chunk index, terminated by 0xffff0000 (the row-level
+// tile-skip mask the attention kernel walks chunk by chunk).
+__global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
+                                  const int* __restrict__ clist, uint32_t* __restrict__ rl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int t = i / TQ, lo = cptr[t], n = cptr[t + 1] - lo;
+  uint32_t* o = rl + (size_t)i * K;
+  int cnt = 0;
+  for (int s = 0; s < K; ++s) {
+    const int j = nbr[(size_t)i * K + s];
+    if (j < 0) continue;
+    const int kb = j / KC;
+    int a = 0, b = n;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (clist[lo + m] < kb) a = m + 1;
+      else b = m;
+    }
+    const uint32_t key = (uint32_t)a << 16, bit = 1u << (j % KC);
+    bool merged = false;
+    for (int u = 0; u < cnt; ++u)
+      if ((o[u] & 0xffff0000u) == key) { o[u] |= bit; merged = true; break; }
+    if (!merged) {
+      int p = cnt++;
+      while (p > 0 && o[p - 1] > key) { o[p] = o[p - 1]; --p; }
+      o[p] = key | bit;
+    }
+  }
+  if (cnt < K) o[cnt] = 0xffff0000u;
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -582,7 +657,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 bool attn_tc_supported(const AttnArgs& a) {
   return a.dtype == ES_BF16 && a.value_mode == ES_VALUE_EAAS && a.L == 2 && a.C == 128 && a.H == 8 &&
-         a.K <= KMAX && encode_fn() != nullptr;
+         a.K <= 511 && encode_fn() != nullptr;
 }
 
 // Scratch (tile mask + chunk lists, O(N/128 * N/512) words) is stream-ordered
@@ -595,12 +670,12 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   const int ntiles = (a.N + TQ - 1) / TQ;
   const int nkb = (a.Nk + KC - 1) / KC;
   const int words = (nkb + 31) / 32;
-  const size_t per_tile = (size_t)(nkb < TQ * KMAX ? nkb : TQ * KMAX);
+  const size_t per_tile = (size_t)nkb < (size_t)TQ * a.K ? (size_t)nkb : (size_t)TQ * a.K;
   size_t cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, ntiles + 1);
   const size_t bytes = align256((size_t)ntiles * words * 4) + 2 * align256((size_t)(ntiles + 1) * 4) +
                        align256((size_t)ntiles * per_tile * 4) + align256(cub_bytes) +
-                       align256((size_t)ntiles * TQ * KMAX * 4);
+                       align256((size_t)a.N * a.K * 4);
   char* base = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&base, bytes, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_fwd_tc: scratch");
@@ -614,7 +689,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   off += align256((size_t)ntiles * per_tile * 4);
   void* cub_ws = base + off;
   off += align256(cub_bytes);
-  int* nsort = (int*)(base + off);
+  uint32_t* rowlist = (uint32_t*)(base + off);
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
   s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
@@ -623,6 +698,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
+  tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist);
 
   CUtensorMap mk, mv;
   if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
@@ -642,7 +718,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
     cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, nsort,
+  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
                                                         (bf16*)out, lse);
   s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
   cudaFreeAsync(base, st);
