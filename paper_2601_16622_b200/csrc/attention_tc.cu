@@ -57,7 +57,9 @@ constexpr int SM_POS = SM_VT + VBYTES;                 // NSTAGE x PBYTES (chunk
 constexpr int SM_WT = 48128;                           // 2 x WBYTES
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
 constexpr int SM_BAR = SM_VG + 2 * GBYTES;
-constexpr int SM_PROW = SM_BAR + 256;                  // [128 rows][16 keys] f32 softmax numerators
+constexpr int SM_VT1 = SM_BAR + 256;                   // second transposed-V buffer (VBYTES)
+constexpr int SM_ZX = SM_VT1 + VBYTES;                 // [2][128] f32 softmax denominators of the key halves
+constexpr int SM_PROW = SM_ZX + 2 * TQ * 4;            // [128 rows][16 keys] f32 softmax numerators
 constexpr int SM_QPOS = SM_PROW + TQ * KC * 4;         // [128 rows][3] f64 query positions
 constexpr int SM_TOTAL = SM_QPOS + TQ * 24;
 static_assert(SM_POS + NSTAGE * PBYTES <= SM_WT, "smem map overlap");
@@ -103,17 +105,21 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
-// Warp-specialised pipeline (320 threads):
+// Warp-specialised pipeline (448 threads):
 //   warp 0, one lane : TMA producer (K, V, key positions; 3 stages)
-//   warp 9, one lane : tcgen05 MMA issuer
-//   warps 1-4        : the 128 query rows -- Q_h into TMEM, scores from TMEM,
-//                      online softmax with lazy rescale, Wt rows, epilogue
-//   warps 5-8        : per-key source coupling Vg
+//   warp 1, one lane : tcgen05 MMA issuer
+//   warps 2-9        : the 128 query rows, two warps per TMEM lane quadrant:
+//                      each reads the row's 16 scores, both run the identical
+//                      online-softmax max/rescale decision, and each builds the
+//                      Wt entries of one half of the chunk's keys (8 keys =
+//                      one 16-byte store per f) -- no zero-fill pass, no
+//                      shuffles, two warps per scheduler for latency hiding
+//   warps 10-13      : per-key source coupling Vg (+ Q_h into TMEM)
 // Q_h lives in tensor memory (the S MMA's A operand); Wt and Vg are double
 // buffered, so chunk c+1's SIMT work overlaps chunk c's value MMA.
 // TMEM: Q[2] [0,144) / [144,288) (next head's Q is loaded by the Vg warps
 // while the current head runs), O [288,432), S[2] [448,464) / [480,496).
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 448;
 
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
@@ -124,14 +130,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
   uint64_t* full_kv = bars + 0;    // [3] TMA landed (tx)
-  uint64_t* empty_kv = bars + 3;   // [3] S MMA done with K + Vg warps with V + rows with key pos (130)
+  uint64_t* empty_kv = bars + 3;   // [3] S MMA done with K + Vg warps with V + rows with key pos (258)
   uint64_t* s_full = bars + 6;     // [2] S MMA committed
-  uint64_t* s_free = bars + 8;     // [2] rows read S (128)
-  uint64_t* wt_full = bars + 10;   // [2] rows wrote Wt (128)
+  uint64_t* s_free = bars + 8;     // [2] rows read S (256)
+  uint64_t* wt_full = bars + 10;   // [2] rows wrote Wt (256)
   uint64_t* vg_full = bars + 12;   // [2] Vg warps wrote Vg (128)
   uint64_t* wv_free = bars + 14;   // [2] value MMA committed (Wt / Vg free, O updated)
   uint64_t* acc_done = bars + 17;  // last value MMA of the head committed
-  uint64_t* epi_done = bars + 18;  // rows finished reading O (128)
+  uint64_t* epi_done = bars + 18;  // rows finished reading O (256)
   uint64_t* q_ready = bars + 19;   // [2] Q_h stored into TMEM buffer h&1 (128, Vg warps)
   uint64_t* q_free = bars + 21;    // [2] last S MMA reading Q buffer committed
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 23);
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   const int q0 = blockIdx.x * TQ;
   const bool TRACE = (a.dbg & 16) && blockIdx.x == 0;
   const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
-  const bool is_row = warp >= 1 && warp <= 4;
+  const bool is_row = warp >= 2 && warp <= 9;
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
   const int qi = q0 + row;
   const bool qvalid = is_row && qi < a.N;
@@ -151,12 +157,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     umma::prefetch_tmap(&mv);
     for (int b = 0; b < NSTAGE; ++b) {
       umma::mbar_init(&full_kv[b], 1);
-      umma::mbar_init(&empty_kv[b], 2 + 128);
+      umma::mbar_init(&empty_kv[b], 2 + 256);
     }
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&s_full[b], 1);
-      umma::mbar_init(&s_free[b], 128);
-      umma::mbar_init(&wt_full[b], 128);
+      umma::mbar_init(&s_free[b], 256);
+      umma::mbar_init(&wt_full[b], 256);
       umma::mbar_init(&vg_full[b], 128);
       umma::mbar_init(&wv_free[b], 1);
     }
@@ -165,12 +171,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     umma::mbar_init(&q_free[0], 1);
     umma::mbar_init(&q_free[1], 1);
     umma::mbar_init(acc_done, 1);
-    umma::mbar_init(epi_done, 128);
+    umma::mbar_init(epi_done, 256);
     umma::fence_barrier_init();
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
   double* qpos = reinterpret_cast<double*>(sm + SM_QPOS);
-  if (is_row) {
+  if (is_row && warp < 6) {
     const int qa = a.row0 + (qin ? qi : 0);
     qpos[3 * row] = qin ? pos[3 * qa] : 0.0;
     qpos[3 * row + 1] = qin ? pos[3 * qa + 1] : 0.0;
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         g0 += nch;
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 1) {
     if (lane == 0) {
       // ================= MMA issuer =================
       auto value_mma = [&](int g, int c, int h) {
@@ -273,8 +279,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     }
   } else if (is_row) {
     // ================= query rows =================
+    const int half = (warp - 2) >> 2;  // this warp's keys: [8 half, 8 half + 8) of every chunk
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const int wrow0 = (warp & 3) * 32;  // first tile row of this warp
+    float* zx = reinterpret_cast<float*>(sm + SM_ZX);  // [2][128] softmax denominators of the two halves
     float* prow = reinterpret_cast<float*>(sm + SM_PROW);
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
@@ -292,13 +299,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           ent = rp < a.K ? __ldg(rl + rp) : 0xffff0000u;
         }
         umma::mbar_wait(&s_full[b], (g >> 1) & 1);
-        if (TRACE && tid == 32 && g < 128) g_trace[2][g] = clock64();
+        if (TRACE && tid == 64 && g < 128) g_trace[2][g] = clock64();
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);  // key positions landed (already complete)
         umma::tc_fence_after();
         uint32_t sr[16];
         umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
+        // identical in both halves (same scores, same instructions)
         float mc = -INFINITY;
 #pragma unroll
         for (int t = 0; t < KC; ++t)
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         float factor = 1.f;
         if (mu == -INFINITY && mc > -INFINITY) mu = mc;
         else if (need) { factor = __expf(mu - mc); mu = mc; z *= factor; }
-        if (__any_sync(0xffffffffu, need)) {
+        if (half == 0 && __any_sync(0xffffffffu, need)) {
           // O must be quiescent: every value MMA up to chunk c-1 complete (c >= 1 here)
           umma::mbar_wait(&wv_free[(g - 1) & 1], ((g - 1) >> 1) & 1);
           umma::tc_fence_after();
@@ -321,28 +329,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           }
           umma::tc_fence_before();
         }
-        // softmax numerators of this row (0 for non-neighbours) -> shared memory
-        float pr[KC];
+        const unsigned hm = (vmask >> (8 * half)) & 0xffu;  // my 8 keys
+        float pw[8];
 #pragma unroll
-        for (int t = 0; t < KC; ++t) {
-          pr[t] = (vmask >> t & 1) ? __expf(a.tau * __uint_as_float(sr[t]) - mu) : 0.f;
-          z += pr[t];
+        for (int t = 0; t < 8; ++t) {
+          const float sv = half ? __uint_as_float(sr[8 + t]) : __uint_as_float(sr[t]);
+          pw[t] = (hm >> t & 1) ? __expf(a.tau * sv - mu) : 0.f;
+          z += pw[t];
         }
-        float4* pdst = reinterpret_cast<float4*>(prow + row * KC);
-#pragma unroll
-        for (int t = 0; t < KC / 4; ++t) pdst[t] = make_float4(pr[4 * t], pr[4 * t + 1], pr[4 * t + 2], pr[4 * t + 3]);
+        float4* pdst = reinterpret_cast<float4*>(prow + row * KC + 8 * half);
+        pdst[0] = make_float4(pw[0], pw[1], pw[2], pw[3]);
+        pdst[1] = make_float4(pw[4], pw[5], pw[6], pw[7]);
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
         uint8_t* wt = sm + SM_WT + b * WBYTES;
 #pragma unroll
-        for (int f = 0; f < MM; ++f) {
-          *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC)) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8)) = make_uint4(0, 0, 0, 0);
-        }
+        for (int f = 0; f < MM; ++f)
+          *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8 * half)) = make_uint4(0, 0, 0, 0);
         __syncwarp();
-        // warp-cooperative geometry: the warp's valid (row, key) pairs are
+        // warp-cooperative geometry: this warp's valid (row, key) pairs are
         // compacted (prefix sum of the row popcounts) and dealt one per lane
-        const unsigned vm = (a.dbg & 2) ? 0u : vmask;
-        const int cnt = __popc(vm);
+        const unsigned gm = (a.dbg & 2) ? 0u : hm;
+        const int cnt = __popc(gm);
         int incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -352,6 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         const int excl = incl - cnt;
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
+#pragma unroll 1
         for (int base = 0; base < total; base += 32) {
           const int idx = base + lane;
           int owner = 0;
@@ -360,12 +368,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             const int e = __shfl_sync(0xffffffffu, excl, owner + step);
             if (e <= idx) owner += step;
           }
-          unsigned om = __shfl_sync(0xffffffffu, vm, owner);
+          unsigned om = __shfl_sync(0xffffffffu, gm, owner);
           const int oex = __shfl_sync(0xffffffffu, excl, owner);
           if (idx < total) {
             for (int r = idx - oex; r > 0; --r) om &= om - 1;
-            const int kk = __ffs(om) - 1;
-            const int orow = wrow0 + owner;
+            const int kk = 8 * half + __ffs(om) - 1;
+            const int orow = ((warp & 3) << 5) + owner;
             double dx = kpos[3 * kk] - qpos[3 * orow], dy = kpos[3 * kk + 1] - qpos[3 * orow + 1],
                    dz = kpos[3 * kk + 2] - qpos[3 * orow + 2];
             if (a.periodic) {
@@ -388,16 +396,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         __syncwarp();
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
-        if (TRACE && tid == 32 && g < 128) g_trace[3][g] = clock64();
+        if (TRACE && tid == 64 && g < 128) g_trace[3][g] = clock64();
         umma::mbar_arrive(&empty_kv[st]);  // done with this stage's key positions
       }
-      // ---- epilogue: O_h / z
+      // ---- epilogue: O_h / z, the two halves each store half of the columns
+      zx[half * TQ + row] = z;
+      umma::named_bar(2, 256);
+      const float zt = zx[row] + zx[TQ + row];
+      umma::named_bar(2, 256);  // zx reusable by the next head
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
-      const float inv = z > 0.f ? 1.f / z : 0.f;
-      if (qvalid) lse[(size_t)qi * 8 + h] = z > 0.f ? mu + __logf(z) : -INFINITY;
-#pragma unroll
-      for (int cc = 0; cc < NV / 16; ++cc) {
+      const float inv = zt > 0.f ? 1.f / zt : 0.f;
+      if (qvalid && half == 0) lse[(size_t)qi * 8 + h] = zt > 0.f ? mu + __logf(zt) : -INFINITY;
+      const int cc0 = half ? 5 : 0, cc1 = half ? NV / 16 : 5;
+      for (int cc = cc0; cc < cc1; ++cc) {
         uint32_t r[16];
         if (nch > 0) umma::tmem_ld16(t_out + lane_base + cc * 16, r);
         float v[16];
@@ -414,9 +426,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       g0 += nch;
     }
   } else {
-    // ================= per-key source coupling (warps 5-8) =================
-    const int vw = warp - 5, vt_id = tid - 160;
-    const int c16 = lane & 15, j0 = (lane >> 4) * 8;
+    // ================= per-key source coupling (warps 10-13) =================
+    const int vt_id = tid - 320;
+    const int vc = vt_id & 15, vjp = vt_id >> 4;  // channel, key pair (2 vjp, 2 vjp + 1)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const bf16* qrow = q + (size_t)(qin ? qi : 0) * MM * 256;
     auto load_q = [&](int hh) {  // Q_hh row -> TMEM buffer hh&1 (A operand, packed bf16 pairs)
@@ -451,7 +463,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
         if (TRACE && vt_id == 0 && g < 128) g_trace[4][g] = clock64();
         const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + st * VBYTES);
-        bf16* vt = reinterpret_cast<bf16*>(sm + SM_VT);
+        bf16* vt = reinterpret_cast<bf16*>(sm + ((g & 1) ? SM_VT1 : SM_VT));  // double buffered
         // transpose [key][mm][c] -> [mm][c][key]: one (key, mm) row of 16 channels per thread
         for (int r2 = vt_id; r2 < KC * MM; r2 += 128) {
           const int key = r2 / MM, mm = r2 - key * MM;
@@ -467,41 +479,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         }
         umma::named_bar(1, 128);
         if (vt_id == 0) umma::mbar_arrive(&empty_kv[st]);  // V stage consumed
-        float v8[MM][8];
+        float v2[MM][2];
 #pragma unroll
         for (int ip = 0; ip < MM; ++ip) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(vt + (ip * HD + c16) * KC + j0);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float2 fv = __bfloat1622float2(b2[t]);
-            v8[ip][2 * t] = fv.x;
-            v8[ip][2 * t + 1] = fv.y;
-          }
+          const uint32_t raw = *reinterpret_cast<const uint32_t*>(vt + (ip * HD + vc) * KC + 2 * vjp);
+          const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
+          v2[ip][0] = f2.x; v2[ip][1] = f2.y;
         }
-        umma::named_bar(1, 128);  // Vt reusable by the next chunk
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Vg buffer b free
         uint8_t* vg = sm + SM_VG + b * GBYTES;
-        auto emit = [&](int o, const float (&acc)[MM][8]) {
-#pragma unroll
-          for (int f = 0; f < MM; ++f)
-            *reinterpret_cast<uint4*>(vg + cm_off(o * HD + c16, f * KC + j0)) = pack8(acc[f]);
-        };
-        float acc[MM][8];
-        if (a.dbg & 1) {
-#pragma unroll
-          for (int x = 0; x < MM; ++x)
-#pragma unroll
-            for (int t = 0; t < 8; ++t) acc[x][t] = v8[x][t];
-          emit(vw, acc);
-        } else {
-          switch (vw) {  // o split: {0,4,8} {1,5} {2,6} {3,7}
-            case 0: es_vg_o0(v8, acc); emit(0, acc); es_vg_o4(v8, acc); emit(4, acc); es_vg_o8(v8, acc); emit(8, acc); break;
-            case 1: es_vg_o1(v8, acc); emit(1, acc); es_vg_o5(v8, acc); emit(5, acc); break;
-            case 2: es_vg_o2(v8, acc); emit(2, acc); es_vg_o6(v8, acc); emit(6, acc); break;
-            default: es_vg_o3(v8, acc); emit(3, acc); es_vg_o7(v8, acc); emit(7, acc); break;
-          }
-        }
+        // Vg[(f, j), (o, c)] for this thread's (c, 2 keys), all o: one straight-line code path
+        // shared by the four warps (keeps the kernel's hot code small for the instruction cache)
+        es_vg_all(v2, [&](int o, int f, float x0, float x1) {
+          const __nv_bfloat162 pk = __floats2bfloat162_rn(x0, x1);
+          *reinterpret_cast<uint32_t*>(vg + cm_off(o * HD + vc, f * KC + 2 * vjp)) =
+              *reinterpret_cast<const uint32_t*>(&pk);
+        });
         umma::fence_proxy_async();
         umma::mbar_arrive(&vg_full[b]);
         if (TRACE && vt_id == 0 && g < 128) g_trace[5][g] = clock64();
