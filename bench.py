@@ -299,15 +299,16 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "latency_ms": round(ms, 4), "flops_per_step_per_gpu": fl,
         },
         "roofline": {
-            "kernel": "attn_fwd_kernel<2,2,EAAS>" if dom == "attn_fwd" else
-                      "attn_bwd (delta + bwd_kv + bwd_q)",
+            "kernel": "attn_fwd_tc_kernel (tcgen05)" if dom == "attn_fwd" else
+                      "attn_bwd (delta + bwd_kv + bwd_q, SIMT)",
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
             "peak_source": peaks["_source"],
             "algorithmic_bytes_per_launch": dom_bytes,
             "achieved_tflops": round(dom_flops / (t[dom] * 1e-3) / 1e12, 3),
             "kernel_ms": {k_: round(v_, 4) for k_, v_ in t.items()},
-            "note": "fp32 SIMT math (per-pair EAAS in registers); tensor-core attention is the next step",
+            "note": "forward: tcgen05 kernel (S = Q K^T and O += Wt Vg on the tensor cores, per-pair geometry "
+                    "on CUDA cores); backward: fp32 SIMT (per-pair EAAS adjoint in registers)",
         },
         "clocks": clocks,
         "e2e": {"value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s",

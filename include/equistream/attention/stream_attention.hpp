@@ -95,11 +95,15 @@ inline void project_qk(const void* h, const void* W, int32_t N, int32_t lmax, in
 }
 
 // stream_aggregate: m [N][M][C], lse [N][H]
-inline void stream_aggregate(const AttentionProblem& p, const void* q, const void* k, const void* v,
-                             const double* pos, const NeighborIndex& idx, void* m, float* lse,
-                             void* stream = nullptr) {
+inline std::size_t forward_workspace_size(const AttentionProblem& p) {
   const es_attn_desc d = p.desc();
-  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, stream), "stream_aggregate");
+  return es_attn_fwd_workspace_size(&d);
+}
+inline void stream_aggregate(const AttentionProblem& p, const void* q, const void* k, const void* v,
+                             const double* pos, const NeighborIndex& idx, void* m, float* lse, void* workspace,
+                             std::size_t ws_bytes, void* stream = nullptr) {
+  const es_attn_desc d = p.desc();
+  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, workspace, ws_bytes, stream), "stream_aggregate");
 }
 
 // stream_aggregate_backward

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 2
+#define ES_ABI_VERSION 3
 
 typedef enum {
   ES_OK = 0,
@@ -93,8 +93,14 @@ typedef struct {
 /* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in
  * {4, 8, 16, 32}.  bf16 + EAAS + L=2 + C=128 + H=8 + K<=64 runs on the
  * tcgen05 tensor-core kernel, everything else on the SIMT kernels. */
+/* Workspace: es_attn_fwd_workspace_size(d) bytes (tile-skip mask, per-tile
+ * key-chunk lists and per-row chunk masks of the tensor-core kernel,
+ * O(N*K) words; 256 bytes for the SIMT kernels).  Caller-owned, reusable
+ * across calls on the same stream; the library allocates nothing. */
+size_t es_attn_fwd_workspace_size(const es_attn_desc* d);
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, void* stream);
+                      const int32_t* nbr, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                      void* stream);
 
 /* Workspace: es_attn_bwd_workspace_size(d) bytes (per-pair-head dscore
  * buffer, O(N*K*H) scalars -- never O(N*K*C)). rev_ptr/rev_pair

@@ -249,8 +249,9 @@ def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row
     out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
     d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
+    ws = _workspace(lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)
     check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
-                            _ptr(lse), _stream()), "es_attn_fwd")
+                            _ptr(lse), _ptr(ws), ws.numel(), _stream()), "es_attn_fwd")
     return out, lse
 
 

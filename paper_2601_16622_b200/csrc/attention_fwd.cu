@@ -189,20 +189,29 @@ struct FwdOp {
 };
 }  // namespace
 
+namespace {
+bool use_tc_kernel(const AttnArgs& a) {
+  // bf16 / L=2 / C=128 / H=8 (the BASELINE shapes): the tcgen05 kernel
+  // (2.9 ms vs 4.5 ms for the SIMT kernel on configs[1]); ES_ATTN_TC=0 forces
+  // the SIMT kernel (kept for the other shapes and for A/B measurements).
+  static int use_tc = -1;
+  if (use_tc < 0) {
+    const char* e = getenv("ES_ATTN_TC");
+    use_tc = (e && e[0] == '0') ? 0 : 1;
+  }
+  return use_tc && attn_tc_supported(a);
+}
+}  // namespace
+
+size_t attn_fwd_workspace(const AttnArgs& a) { return use_tc_kernel(a) ? attn_fwd_tc_workspace(a) : 0; }
+
 es_status attn_fwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
-                          const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
+                          const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st) {
   es_status s = upload_tables_tu();
   if (s != ES_OK) return s;
   const KParams kp = make_params(a);
   if (a.N == 0) return ES_OK;
-  // The tcgen05 kernel is opt-in (ES_ATTN_TC=1) until it beats the SIMT
-  // kernel on the bench workload (round-1 measurement: 9.4 vs 8.4 ms).
-  static int use_tc = -1;
-  if (use_tc < 0) {
-    const char* e = getenv("ES_ATTN_TC");
-    use_tc = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (use_tc && attn_tc_supported(a)) return attn_fwd_tc_launch(a, q, k, v, pos, nbr, out, lse, st);
+  if (use_tc_kernel(a)) return attn_fwd_tc_launch(a, q, k, v, pos, nbr, out, lse, ws, ws_bytes, st);
   return dispatch<FwdOp>(a, kp, q, k, v, pos, nbr, out, lse, st);
 }
 

@@ -52,15 +52,16 @@ constexpr int WBYTES = TQ * KV * 2;                    // [128 x 144] core-matri
 constexpr int GBYTES = NV * KV * 2;                    // [144 x 144] core-matrix   41472
 constexpr int SM_K = 0;                                // NSTAGE x KBYTES
 constexpr int SM_VST = SM_K + NSTAGE * KBYTES;         // NSTAGE x VBYTES
-constexpr int SM_VT = SM_VST + NSTAGE * VBYTES;        // VBYTES (transposed [9][16 c][16 keys])
-constexpr int SM_POS = SM_VT + VBYTES;                 // NSTAGE x PBYTES (chunk key positions)
+constexpr int SM_POS = SM_VST + NSTAGE * VBYTES;       // NSTAGE x PBYTES (chunk key positions)
 constexpr int SM_WT = 48128;                           // 2 x WBYTES
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
 constexpr int SM_BAR = SM_VG + 2 * GBYTES;
-constexpr int SM_VT1 = SM_BAR + 256;                   // second transposed-V buffer (VBYTES)
-constexpr int SM_ZX = SM_VT1 + VBYTES;                 // [2][128] f32 softmax denominators of the key halves
-constexpr int SM_PROW = SM_ZX + 2 * TQ * 4;            // [128 rows][16 keys] f32 softmax numerators
-constexpr int SM_QPOS = SM_PROW + TQ * KC * 4;         // [128 rows][3] f64 query positions
+constexpr int SM_ZX = SM_BAR + 256;                    // [2][128] f32 softmax denominators of the key halves
+constexpr int SM_PROW = SM_ZX + 2 * TQ * 4;            // [2][128 rows][16 keys] f32 softmax numerators
+constexpr int SM_RMASK = SM_PROW + 2 * TQ * KC * 4;    // [2][128] u32 valid-key mask per row
+constexpr int SM_RINCL = SM_RMASK + 2 * TQ * 4;        // [2][128] i32 quadrant-local inclusive pair count
+constexpr int SM_QTOT = SM_RINCL + 2 * TQ * 4;         // [2][4] i32 pairs per quadrant
+constexpr int SM_QPOS = SM_QTOT + 64;                  // [128 rows][3] f64 query positions
 constexpr int SM_TOTAL = SM_QPOS + TQ * 24;
 static_assert(SM_POS + NSTAGE * PBYTES <= SM_WT, "smem map overlap");
 
@@ -71,7 +72,9 @@ struct TcTab {
   int ofs[MM * MM + 1];  // (o, f) -> entry range
 };
 __constant__ TcTab c_tc;
-__device__ long long g_trace[8][128];  // ES_TC_DBG&16: per-chunk event clocks of CTA 0
+__device__ long long g_trace[8][128];
+__device__ long long g_trace_w[8][128];  // per row warp: Wt arrive clock
+__device__ long long g_trace_r[4][128];  // row thread 64: before Wt-free wait, after it, after the phase barrier  // ES_TC_DBG&16: per-chunk event clocks of CTA 0
 
 struct TcArgs {
   int N, K, row0, Nk;
@@ -130,7 +133,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
   uint64_t* full_kv = bars + 0;    // [3] TMA landed (tx)
-  uint64_t* empty_kv = bars + 3;   // [3] S MMA done with K + Vg warps with V + rows with key pos (258)
+  uint64_t* empty_kv = bars + 3;   // [3] S MMA done with K + rows with key pos + Vg threads with V (385)
   uint64_t* s_full = bars + 6;     // [2] S MMA committed
   uint64_t* s_free = bars + 8;     // [2] rows read S (256)
   uint64_t* wt_full = bars + 10;   // [2] rows wrote Wt (256)
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     umma::prefetch_tmap(&mv);
     for (int b = 0; b < NSTAGE; ++b) {
       umma::mbar_init(&full_kv[b], 1);
-      umma::mbar_init(&empty_kv[b], 2 + 256);
+      umma::mbar_init(&empty_kv[b], 1 + 256 + 128);
     }
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&s_full[b], 1);
@@ -210,6 +213,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             if (cp < nch) prefetch(h, cp);
             else if (h + 1 < 8 && cp - nch < nch) prefetch(h + 1, cp - nch);
           }
+          if (TRACE && g < 128) g_trace[7][g] = clock64();
           if (g >= NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           const int nkeys = min(KC, a.Nk - k0);
@@ -282,7 +286,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const int half = (warp - 2) >> 2;  // this warp's keys: [8 half, 8 half + 8) of every chunk
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     float* zx = reinterpret_cast<float*>(sm + SM_ZX);  // [2][128] softmax denominators of the two halves
-    float* prow = reinterpret_cast<float*>(sm + SM_PROW);
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
       float mu = -INFINITY, z = 0.f;
@@ -337,43 +340,58 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           pw[t] = (hm >> t & 1) ? __expf(a.tau * sv - mu) : 0.f;
           z += pw[t];
         }
+        // ---- phase 1 (row-bound): P row -> smem, zero my half of the Wt row,
+        // per-row valid masks + quadrant-local prefix counts (half 0)
+        const int pb = g & 1;  // phase-2 tables double buffered by chunk parity
+        float* prow = reinterpret_cast<float*>(sm + SM_PROW) + pb * TQ * KC;
+        uint32_t* rmask = reinterpret_cast<uint32_t*>(sm + SM_RMASK) + pb * TQ;
+        int* rincl = reinterpret_cast<int*>(sm + SM_RINCL) + pb * TQ;
+        int* qtot = reinterpret_cast<int*>(sm + SM_QTOT) + pb * 4;
         float4* pdst = reinterpret_cast<float4*>(prow + row * KC + 8 * half);
         pdst[0] = make_float4(pw[0], pw[1], pw[2], pw[3]);
         pdst[1] = make_float4(pw[4], pw[5], pw[6], pw[7]);
+        if (half == 0) {
+          const unsigned gm = (a.dbg & 2) ? 0u : vmask;
+          const int cnt = __popc(gm);
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          rmask[row] = gm;
+          rincl[row] = incl;
+          if (lane == 31) qtot[warp & 3] = incl;
+        }
+        if (TRACE && tid == 64 && g < 128) g_trace_r[0][g] = clock64();
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
+        if (TRACE && tid == 64 && g < 128) g_trace_r[1][g] = clock64();
         uint8_t* wt = sm + SM_WT + b * WBYTES;
 #pragma unroll
         for (int f = 0; f < MM; ++f)
           *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8 * half)) = make_uint4(0, 0, 0, 0);
-        __syncwarp();
-        // warp-cooperative geometry: this warp's valid (row, key) pairs are
-        // compacted (prefix sum of the row popcounts) and dealt one per lane
-        const unsigned gm = (a.dbg & 2) ? 0u : hm;
-        const int cnt = __popc(gm);
-        int incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int excl = incl - cnt;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
+        umma::named_bar(2, 256);
+        if (TRACE && tid == 64 && g < 128) g_trace_r[2][g] = clock64();
+        // ---- phase 2 (balanced): the chunk's valid (row, key) pairs of the whole
+        // tile are dealt round-robin to the 256 row threads (the pairs of a
+        // molecule-sized chunk cluster in one quadrant; this spreads them)
+        {
+          const int q0n = qtot[0], q1n = q0n + qtot[1], q2n = q1n + qtot[2], total = q2n + qtot[3];
+          const int rt = tid - 64;  // 0..255
+          const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
 #pragma unroll 1
-        for (int base = 0; base < total; base += 32) {
-          const int idx = base + lane;
-          int owner = 0;
+          for (int p = rt; p < total; p += 256) {
+            const int qd = (p >= q0n) + (p >= q1n) + (p >= q2n);
+            const int local = p - (qd == 0 ? 0 : qd == 1 ? q0n : qd == 2 ? q1n : q2n);
+            const int* ri = rincl + 32 * qd;
+            int lo = 0;  // first row of the quadrant with inclusive count > local
 #pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int e = __shfl_sync(0xffffffffu, excl, owner + step);
-            if (e <= idx) owner += step;
-          }
-          unsigned om = __shfl_sync(0xffffffffu, gm, owner);
-          const int oex = __shfl_sync(0xffffffffu, excl, owner);
-          if (idx < total) {
-            for (int r = idx - oex; r > 0; --r) om &= om - 1;
-            const int kk = 8 * half + __ffs(om) - 1;
-            const int orow = ((warp & 3) << 5) + owner;
+            for (int step = 16; step > 0; step >>= 1)
+              if (ri[lo + step - 1] <= local) lo += step;
+            const int orow = 32 * qd + lo;
+            unsigned om = rmask[orow];
+            for (int r = local - (ri[lo] - __popc(om)); r > 0; --r) om &= om - 1;
+            const int kk = __ffs(om) - 1;
             double dx = kpos[3 * kk] - qpos[3 * orow], dy = kpos[3 * kk + 1] - qpos[3 * orow + 1],
                    dz = kpos[3 * kk + 2] - qpos[3 * orow + 2];
             if (a.periodic) {
@@ -393,10 +411,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
               *reinterpret_cast<bf16*>(wt + cm_off(orow, f * KC + kk)) = __float2bfloat16_rn(pp * y[f]);
           }
         }
-        __syncwarp();
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
         if (TRACE && tid == 64 && g < 128) g_trace[3][g] = clock64();
+        if (TRACE && lane == 0 && g < 128) g_trace_w[warp - 2][g] = clock64();
         umma::mbar_arrive(&empty_kv[st]);  // done with this stage's key positions
       }
       // ---- epilogue: O_h / z, the two halves each store half of the columns
@@ -462,30 +480,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         const int g = g0 + c, b = g & 1, st = g % NSTAGE;
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
         if (TRACE && vt_id == 0 && g < 128) g_trace[4][g] = clock64();
-        const bf16* vst = reinterpret_cast<const bf16*>(sm + SM_VST + st * VBYTES);
-        bf16* vt = reinterpret_cast<bf16*>(sm + ((g & 1) ? SM_VT1 : SM_VT));  // double buffered
-        // transpose [key][mm][c] -> [mm][c][key]: one (key, mm) row of 16 channels per thread
-        for (int r2 = vt_id; r2 < KC * MM; r2 += 128) {
-          const int key = r2 / MM, mm = r2 - key * MM;
-          const uint4 u0 = *reinterpret_cast<const uint4*>(vst + r2 * HD);
-          const uint4 u1 = *reinterpret_cast<const uint4*>(vst + r2 * HD + 8);
-          const uint32_t w[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
-          unsigned short* vts = reinterpret_cast<unsigned short*>(vt);
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            vts[(mm * HD + 2 * cc) * KC + key] = (unsigned short)(w[cc] & 0xffffu);
-            vts[(mm * HD + 2 * cc + 1) * KC + key] = (unsigned short)(w[cc] >> 16);
-          }
-        }
-        umma::named_bar(1, 128);
-        if (vt_id == 0) umma::mbar_arrive(&empty_kv[st]);  // V stage consumed
+        // v_j[i'][c] of this thread's channel and two keys, read straight from the
+        // TMA stage ([key][i'][16 c] bf16; lanes = consecutive channels)
+        const unsigned short* vst = reinterpret_cast<const unsigned short*>(sm + SM_VST + st * VBYTES);
         float v2[MM][2];
 #pragma unroll
         for (int ip = 0; ip < MM; ++ip) {
-          const uint32_t raw = *reinterpret_cast<const uint32_t*>(vt + (ip * HD + vc) * KC + 2 * vjp);
-          const float2 f2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw));
-          v2[ip][0] = f2.x; v2[ip][1] = f2.y;
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            v2[ip][t] = __uint_as_float((uint32_t)vst[((2 * vjp + t) * MM + ip) * HD + vc] << 16);
         }
+        umma::mbar_arrive(&empty_kv[st]);  // V stage consumed (every Vg thread arrives)
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Vg buffer b free
         uint8_t* vg = sm + SM_VG + b * GBYTES;
         // Vg[(f, j), (o, c)] for this thread's (c, 2 keys), all o: one straight-line code path
@@ -507,8 +512,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   if (warp == 0) umma::tmem_dealloc(tmem, 512);
   if (TRACE && tid == 0) {
     for (int g = 0; g < 128 && g < 8 * nch; ++g)
-      printf("TRACE g=%d tma=%lld sI=%lld sR=%lld wt=%lld vgS=%lld vgD=%lld vI=%lld\n", g, g_trace[0][g],
-             g_trace[1][g], g_trace[2][g], g_trace[3][g], g_trace[4][g], g_trace[5][g], g_trace[6][g]);
+      printf("TRACE g=%d tma=%lld sI=%lld sR=%lld wt=%lld vgS=%lld vgD=%lld vI=%lld pw=%lld\n", g, g_trace[0][g],
+             g_trace[1][g], g_trace[2][g], g_trace[3][g], g_trace[4][g], g_trace[5][g], g_trace[6][g], g_trace[7][g]);
+    for (int g = 0; g < 128 && g < 8 * nch; ++g)
+      printf("TRACEW g=%d %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", g, g_trace_r[0][g], g_trace_r[1][g], g_trace_r[2][g], g_trace_w[0][g], g_trace_w[1][g],
+             g_trace_w[2][g], g_trace_w[3][g], g_trace_w[4][g], g_trace_w[5][g], g_trace_w[6][g], g_trace_w[7][g]);
   }
 }
 
@@ -653,25 +661,43 @@ bool attn_tc_supported(const AttnArgs& a) {
          a.K <= 511 && encode_fn() != nullptr;
 }
 
-// Scratch (tile mask + chunk lists, O(N/128 * N/512) words) is stream-ordered
-// library-owned memory: cudaMallocAsync / cudaFreeAsync on `st`.
+namespace {
+struct TcScratch {
+  int ntiles, nkb, words;
+  size_t chunks, cub_bytes, total;
+};
+TcScratch tc_scratch(const AttnArgs& a) {
+  TcScratch t;
+  t.ntiles = (a.N + TQ - 1) / TQ;
+  t.nkb = (a.Nk + KC - 1) / KC;
+  t.words = (t.nkb + 31) / 32;
+  // a tile's chunk list is at most min(nkb, its valid pairs) long: the packed
+  // lists of all tiles fit min(ntiles * nkb, N * K) entries
+  const size_t dense = (size_t)t.ntiles * t.nkb, pairs = (size_t)a.N * a.K;
+  t.chunks = dense < pairs ? dense : pairs;
+  t.cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t.cub_bytes, (int*)nullptr, (int*)nullptr, t.ntiles + 1);
+  t.total = align256((size_t)t.ntiles * t.words * 4) + 2 * align256((size_t)(t.ntiles + 1) * 4) +
+            align256(t.chunks * 4) + align256(t.cub_bytes) + align256(pairs * 4);
+  return t;
+}
+}  // namespace
+
+size_t attn_fwd_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(a).total : 0; }
+
+// Scratch (tile mask, chunk lists, per-row chunk lists) lives in the caller's
+// workspace (es_attn_fwd_workspace_size): no allocation on the launch path.
 es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
-                             const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
+                             const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes,
+                             cudaStream_t st) {
   es_status s = upload_tc_tables();
   if (s != ES_OK) return s;
   if (a.N == 0) return ES_OK;
-  const int ntiles = (a.N + TQ - 1) / TQ;
-  const int nkb = (a.Nk + KC - 1) / KC;
-  const int words = (nkb + 31) / 32;
-  const size_t per_tile = (size_t)nkb < (size_t)TQ * a.K ? (size_t)nkb : (size_t)TQ * a.K;
-  size_t cub_bytes = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (int*)nullptr, (int*)nullptr, ntiles + 1);
-  const size_t bytes = align256((size_t)ntiles * words * 4) + 2 * align256((size_t)(ntiles + 1) * 4) +
-                       align256((size_t)ntiles * per_tile * 4) + align256(cub_bytes) +
-                       align256((size_t)a.N * a.K * 4);
-  char* base = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&base, bytes, st);
-  if (e != cudaSuccess) return cuda_status(e, "attn_fwd_tc: scratch");
+  const TcScratch t = tc_scratch(a);
+  if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+  const int ntiles = t.ntiles, words = t.words;
+  size_t cub_bytes = t.cub_bytes;
+  char* base = static_cast<char*>(ws);
   uint32_t* mask = (uint32_t*)base;
   size_t off = align256((size_t)ntiles * words * 4);
   int* cnt = (int*)(base + off);
@@ -679,7 +705,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   int* cptr = (int*)(base + off);
   off += align256((size_t)(ntiles + 1) * 4);
   int* clist = (int*)(base + off);
-  off += align256((size_t)ntiles * per_tile * 4);
+  off += align256(t.chunks * 4);
   void* cub_ws = base + off;
   off += align256(cub_bytes);
   uint32_t* rowlist = (uint32_t*)(base + off);
@@ -688,7 +714,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
   if (s != ES_OK) return s;
   tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
-  e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
   tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist);
@@ -713,9 +739,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   }
   attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
                                                         (bf16*)out, lse);
-  s = cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
-  cudaFreeAsync(base, st);
-  return s;
+  return cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
 }
 
 }  // namespace es

@@ -132,14 +132,24 @@ int32_t es_device_ok(void) {
   return major == 10 ? 1 : 0;
 }
 
+size_t es_attn_fwd_workspace_size(const es_attn_desc* d) {
+  if (!d || check_attn(d) != ES_OK) return 256;
+  const size_t n = attn_fwd_workspace(to_args(d));
+  return n > 256 ? n : 256;
+}
+
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, void* stream) {
+                      const int32_t* nbr, void* out, float* lse, void* workspace, size_t workspace_bytes,
+                      void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
     if (d->N > 0 && (!q || !k || !v || !pos || !nbr || !out || !lse))
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: null buffer");
-    return attn_fwd_launch(to_args(d), q, k, v, pos, nbr, out, lse, (cudaStream_t)stream);
+    if (d->N > 0 && (!workspace || workspace_bytes < es_attn_fwd_workspace_size(d)))
+      return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+    return attn_fwd_launch(to_args(d), q, k, v, pos, nbr, out, lse, workspace, workspace_bytes,
+                           (cudaStream_t)stream);
   });
 }
 

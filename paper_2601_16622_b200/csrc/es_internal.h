@@ -46,11 +46,14 @@ struct AttnArgs {
   double box[3];
 };
 
+size_t attn_fwd_workspace(const AttnArgs& a);
 es_status attn_fwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
-                          const int32_t* nbr, void* out, float* lse, cudaStream_t st);
+                          const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes, cudaStream_t st);
 bool attn_tc_supported(const AttnArgs& a);
+size_t attn_fwd_tc_workspace(const AttnArgs& a);
 es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
-                             const int32_t* nbr, void* out, float* lse, cudaStream_t st);
+                             const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes,
+                             cudaStream_t st);
 es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
                           const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,

@@ -30,7 +30,7 @@ int main(int argc, char** argv) {
     try {  // invalid argument surfaces as std::invalid_argument, like the reference
       ea::AttentionProblem bad;
       bad.N = N; bad.K = K; bad.heads = 3; bad.channels = C;
-      ea::stream_aggregate(bad, nullptr, nullptr, nullptr, nullptr, ea::NeighborIndex{}, nullptr, nullptr);
+      ea::stream_aggregate(bad, nullptr, nullptr, nullptr, nullptr, ea::NeighborIndex{}, nullptr, nullptr, nullptr, 0);
     } catch (const std::invalid_argument&) {
       std::printf("NOGPU invalid_argument ok\n");
       return 0;
@@ -61,7 +61,10 @@ int main(int argc, char** argv) {
   ea::build_neighbors(dpos, N, K, 6.0, idx, dws, ws);
   ea::AttentionProblem p;
   p.N = N; p.K = K; p.heads = H; p.lmax = L; p.channels = C;
-  ea::stream_aggregate(p, dq, dk, dv, dpos, idx, dout, dlse);
+  const size_t fws = ea::forward_workspace_size(p);
+  void* dfws;
+  cudaMalloc(&dfws, fws);
+  ea::stream_aggregate(p, dq, dk, dv, dpos, idx, dout, dlse, dfws, fws);
   std::vector<float> out(v.size());
   cudaMemcpy(out.data(), dout, out.size() * 4, cudaMemcpyDeviceToHost);
   double s = 0, s2 = 0;

@@ -280,13 +280,15 @@ def test_full_size_properties_config2(es):
     assert 10 < cnt.mean() < 20
 
 
-@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc"])
+@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc", "sharp"])
 def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     """The tcgen05 path (bf16, L=2, C=128, H=8) over many 128-query tiles and
-    key chunks: molecule batch, one bulk system, a periodic box."""
+    key chunks: molecule batch, one bulk system, a periodic box, and a batch
+    with 6x scaled queries (score ranges > 5 nats, so the lazy online-softmax
+    rescale of the TMEM accumulator fires)."""
     L, C, H = 2, 128, 8
     box = None
-    if kind == "batch":
+    if kind in ("batch", "sharp"):
         b = S.molecule_batch(12, 40, 60, 5)
         pos, seg = b.pos, b.seg_ptr
     elif kind == "bulk":
@@ -298,7 +300,10 @@ def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     nbr, _, _ = po.build_neighbors(pos, 64, 6.0, seg_ptr=seg, box=box)
     h = S.random_features(N, L, C, 8)
     W = S.random_weights(L, C, 8)
-    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in po.project(h, W, L))
+    q, k, v = po.project(h, W, L)
+    if kind == "sharp":
+        q = q * 6.0
+    q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
     P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
     rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
     out, lse, _ = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box)
