@@ -78,70 +78,110 @@ __device__ __forceinline__ void store_row32(bf16* dst, const uint32_t (&r)[32]) 
 }
 
 // ------------------------------------------------------------------ forward
-// grid (ceil(N/128), M, 5): tile = 128 atoms at one (l,m) row x 128 output columns; K = C = 128.
-__global__ void __launch_bounds__(128) proj_fwd_tc_kernel(const __grid_constant__ CUtensorMap mh,
+// grid (ceil(N/128), M): tile = 128 atoms at one (l,m) row; the A tile
+// (h rows, K = C = 128) is loaded ONCE and the five 128-column chunks of
+// [Q1|Q2|K1|K2|H] stream through a double-buffered B stage and a
+// double-buffered TMEM accumulator, so the epilogue of chunk c (TMEM ->
+// bf16 rows, warps 0-3) overlaps the MMA of chunk c+1.  Warp 4 (one lane)
+// issues TMA + MMA.
+__global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant__ CUtensorMap mh,
                                                           const __grid_constant__ CUtensorMap mw, TcP p,
                                                           bf16* __restrict__ q, bf16* __restrict__ k,
                                                           bf16* __restrict__ v) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
-  uint8_t* Bs = smem + 32768;         // [2 kb][2 nb][64 k-rows][64] bf16, 8 KB each
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 65536);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 65536 + 64);
+  uint8_t* Bs = smem + 32768;         // [2 stages][2 kb][2 nb][64 k-rows][64] bf16, 32 KB per stage
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 32768 + 65536);
+  uint64_t* a_full = bars + 0;
+  uint64_t* b_full = bars + 1;        // [2]
+  uint64_t* b_empty = bars + 3;       // [2] MMA done reading the stage
+  uint64_t* acc_full = bars + 5;      // [2]
+  uint64_t* acc_free = bars + 7;      // [2] epilogue read the accumulator (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 128, mm = blockIdx.y, chunk = blockIdx.z;
+  const int n0 = blockIdx.x * 128, mm = blockIdx.y;
   const int l = degree_of_row(mm);
-  const int o0 = chunk * 128;
+  constexpr int NCH = 5;
   if (threadIdx.x == 0) {
     umma::prefetch_tmap(&mh);
     umma::prefetch_tmap(&mw);
-    umma::mbar_init(&bars[0], 1);
-    umma::mbar_init(&bars[1], 1);
+    umma::mbar_init(a_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&b_full[b], 1);
+      umma::mbar_init(&b_empty[b], 1);
+      umma::mbar_init(&acc_full[b], 1);
+      umma::mbar_init(&acc_free[b], 128);
+    }
     umma::fence_barrier_init();
   }
-  if (warp == 0) umma::tmem_alloc(tslot, 128);
+  if (warp == 0) umma::tmem_alloc(tslot, 256);
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
   const uint32_t taddr = *tslot;
-  if (threadIdx.x == 0) {
-    umma::mbar_arrive_expect_tx(&bars[0], 65536);
-    umma::tma_load_3d(As, &mh, &bars[0], 0, mm, n0);
-    umma::tma_load_3d(As + 16384, &mh, &bars[0], 64, mm, n0);
+  if (warp == 4) {
+    if (lane == 0) {
+    auto load_b = [&](int c) {
+      uint8_t* B = Bs + (c & 1) * 32768;
+      umma::mbar_arrive_expect_tx(&b_full[c & 1], 32768);
 #pragma unroll
-    for (int kb = 0; kb < 2; ++kb)
+      for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb)
-        umma::tma_load_2d(Bs + (kb * 2 + nb) * 8192, &mw, &bars[0], o0 + 64 * nb, l * p.C + 64 * kb);
-    umma::mbar_wait(&bars[0], 0);
-    umma::tc_fence_after();
+        for (int nb = 0; nb < 2; ++nb)
+          umma::tma_load_2d(B + (kb * 2 + nb) * 8192, &mw, &b_full[c & 1], c * 128 + 64 * nb, l * p.C + 64 * kb);
+    };
+    umma::mbar_arrive_expect_tx(a_full, 32768);
+    umma::tma_load_3d(As, &mh, a_full, 0, mm, n0);
+    umma::tma_load_3d(As + 16384, &mh, a_full, 64, mm, n0);
+    load_b(0);
+    load_b(1);
+    umma::mbar_wait(a_full, 0);
     constexpr uint32_t idesc = umma::idesc_bf16(128, 128, 0, 1);
+    for (int c = 0; c < NCH; ++c) {
+      const int b = c & 1;
+      umma::mbar_wait(&b_full[b], (c >> 1) & 1);
+      if (c >= 2) umma::mbar_wait(&acc_free[b], ((c >> 1) - 1) & 1);
+      umma::tc_fence_after();
+      const uint8_t* B = Bs + b * 32768;
 #pragma unroll
-    for (int s = 0; s < 8; ++s) {
-      const int kb = s >> 2, ks = s & 3;
-      const uint64_t ad = umma::sdesc(umma::smem_u32(As + kb * 16384) + ks * 32, 16, 1024);
-      const uint64_t bd = umma::sdesc(umma::smem_u32(Bs + kb * 16384) + ks * 2048, 8192, 1024);
-      umma::mma_f16(taddr, ad, bd, idesc, s > 0 ? 1u : 0u);
+      for (int s = 0; s < 8; ++s) {
+        const int kb = s >> 2, ks = s & 3;
+        const uint64_t ad = umma::sdesc(umma::smem_u32(As + kb * 16384) + ks * 32, 16, 1024);
+        const uint64_t bd = umma::sdesc(umma::smem_u32(B + kb * 16384) + ks * 2048, 8192, 1024);
+        umma::mma_f16(taddr + 128 * b, ad, bd, idesc, s > 0 ? 1u : 0u);
+      }
+      umma::mma_commit(&acc_full[b]);
+      umma::mma_commit(&b_empty[b]);
+      if (c + 2 < NCH) {
+        umma::mbar_wait(&b_empty[b], (c >> 1) & 1);
+        load_b(c + 2);
+      }
     }
-    umma::mma_commit(&bars[1]);
-  }
-  umma::mbar_wait(&bars[1], 0);
-  umma::tc_fence_after();
+    }
+  } else {
   const int n = n0 + warp * 32 + lane;
-  bf16* dst;
-  if (o0 < 2 * p.C) dst = q + ((size_t)n * p.M + mm) * (2 * p.C) + o0;
-  else if (o0 < 4 * p.C) dst = k + ((size_t)n * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
-  else dst = v + ((size_t)n * p.M + mm) * p.C + (o0 - 4 * p.C);
+  for (int c = 0; c < NCH; ++c) {
+    const int b = c & 1, o0 = c * 128;
+    umma::mbar_wait(&acc_full[b], (c >> 1) & 1);
+    umma::tc_fence_after();
+    bf16* dst;
+    if (o0 < 2 * p.C) dst = q + ((size_t)n * p.M + mm) * (2 * p.C) + o0;
+    else if (o0 < 4 * p.C) dst = k + ((size_t)n * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
+    else dst = v + ((size_t)n * p.M + mm) * p.C + (o0 - 4 * p.C);
 #pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    uint32_t r[32];
-    umma::tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
-    if (n < p.N) store_row32(dst + cc * 32, r);
+    for (int cc = 0; cc < 4; ++cc) {
+      uint32_t r[32];
+      umma::tmem_ld32(taddr + 128 * b + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
+      if (n < p.N) store_row32(dst + cc * 32, r);
+    }
+    umma::tc_fence_before();
+    umma::mbar_arrive(&acc_free[b]);
+  }
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(taddr, 128);
+  if (warp == 0) umma::tmem_dealloc(taddr, 256);
 }
 
 // ------------------------------------------------------------------ dh
@@ -323,15 +363,15 @@ es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, vo
   CUtensorMap mh, mw;
   if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64))
     return fail(ES_CUDA_ERROR, "proj_fwd_tc: tensor map encode failed");
-  const size_t smem = 65536 + 1024 + 1024;
+  const size_t smem = 32768 + 65536 + 1024 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(proj_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   TcP p{a.N, M, a.C, a.L};
-  dim3 grid((a.N + 127) / 128, M, 5);
-  proj_fwd_tc_kernel<<<grid, 128, smem, st>>>(mh, mw, p, (bf16*)q, (bf16*)k, (bf16*)v);
+  dim3 grid((a.N + 127) / 128, M);
+  proj_fwd_tc_kernel<<<grid, 160, smem, st>>>(mh, mw, p, (bf16*)q, (bf16*)k, (bf16*)v);
   return cuda_status(cudaGetLastError(), "proj_fwd_tc_kernel");
 }
 
