@@ -28,7 +28,9 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 
 // Key-centric pass: CTA per key atom j over the transposed relation; yields
 // dk_j, dv_j exclusively (no atomics) and the per-pair-head dscore.
-template <int L, int CPL, bool EAAS, typename T>
+// CC, HH > 0: channels / heads fixed at compile time (the BASELINE shape C=128,
+// H=8): row strides become immediates, no per-row 64-bit address arithmetic.
+template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0>
 __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
@@ -36,6 +38,7 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
                                                           const float* __restrict__ lse, const T* __restrict__ dout,
                                                           const float* __restrict__ delta, T* __restrict__ dk,
                                                           T* __restrict__ dv, float* __restrict__ dsbuf) {
+  const int PC = CC ? CC : p.C, PH = HH ? HH : p.H, PDq = CC ? 2 * CC : p.Dq;
   using LY = Lay<L>;
   constexpr int M = LY::M;
   constexpr int REC = LY::REC;
@@ -46,16 +49,16 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
   const int j = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = (warp * 32 + lane) * CPL;
-  const int Ch = p.C / p.H;
+  const int Ch = PC / PH;
   const int lph = Ch / CPL;
   const int head = c0 / Ch;
-  const int Dq = p.Dq;
+  const int Dq = PDq;
 
   // k_j / v_j are re-read per pair from L1 (one row per CTA) instead of
   // being held in registers: halves the live state, doubles occupancy
   float dkr[M][2 * CPL], dvr[M][CPL];
   const T* kj = k + (size_t)j * M * Dq + 2 * c0;
-  const T* vj = v + (size_t)j * M * p.C + c0;
+  const T* vj = v + (size_t)j * M * PC + c0;
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
 #pragma unroll
@@ -92,12 +95,12 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
         for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[c], s);
       }
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const float P = expf(s * p.tau - lse[(size_t)i * p.H + head]);
+      const float P = expf(s * p.tau - lse[(size_t)i * PH + head]);
       const float phi = rec[LY::OFF_PHI];
       float g[M][CPL], y[M][CPL];
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
-        ldvec<CPL>(dout + ((size_t)i * M + mm) * p.C + c0, g[mm]);
+        ldvec<CPL>(dout + ((size_t)i * M + mm) * PC + c0, g[mm]);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) y[mm][c] = 0.f;
       }
@@ -113,7 +116,7 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
         float vr[CPL];
-        ldvec<CPL>(vj + (size_t)mm * p.C, vr);
+        ldvec<CPL>(vj + (size_t)mm * PC, vr);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           dvr[mm][c] = fmaf(P, y[mm][c], dvr[mm][c]);
@@ -121,19 +124,19 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
         }
       }
       for (int o = lph >> 1; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
-      const float ds = P * (dp - delta[(size_t)i * p.H + head]);
+      const float ds = P * (dp - delta[(size_t)i * PH + head]);
       const float tds = p.tau * ds;
 #pragma unroll
       for (int mm = 0; mm < M; ++mm)
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
-      if ((lane % lph) == 0) dsbuf[(size_t)pr * p.H + head] = ds;
+      if ((lane % lph) == 0) dsbuf[(size_t)pr * PH + head] = ds;
     }
   }
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
     stvec<2 * CPL>(dk + ((size_t)j * M + mm) * Dq + 2 * c0, dkr[mm]);
-    stvec<CPL>(dv + ((size_t)j * M + mm) * p.C + c0, dvr[mm]);
+    stvec<CPL>(dv + ((size_t)j * M + mm) * PC + c0, dvr[mm]);
   }
 }
 
@@ -227,7 +230,8 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   if (s != ES_OK) return s;
   const int threads = kp.C / CPL;
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4;
-  auto fn = attn_bwd_kv_kernel<L, CPL, EAAS, T>;
+  auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
+                                                               : attn_bwd_kv_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.Nk, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
                                   (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf);

@@ -7,11 +7,14 @@ namespace es {
 namespace {
 
 // ------------------------------------------------------------------ forward
-template <int L, int CPL, bool EAAS, typename T>
+// CC, HH > 0: channels / heads fixed at compile time (the BASELINE shape C=128,
+// H=8): row strides become immediates, no per-row 64-bit address arithmetic.
+template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0>
 __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                        const T* __restrict__ v, const double* __restrict__ pos,
                                                        const int* __restrict__ nbr, T* __restrict__ out,
                                                        float* __restrict__ lse) {
+  const int PC = CC ? CC : p.C, PH = HH ? HH : p.H, PDq = CC ? 2 * CC : p.Dq;
   using LY = Lay<L>;
   constexpr int M = LY::M;
   constexpr int REC = LY::REC;
@@ -24,10 +27,10 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
   const int i = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = (warp * 32 + lane) * CPL;  // first value channel of this lane
-  const int Ch = p.C / p.H;                 // value channels per head
+  const int Ch = PC / PH;                 // value channels per head
   const int lph = Ch / CPL;                 // lanes per head
   const int head = c0 / Ch;
-  const int Dq = p.Dq;
+  const int Dq = PDq;
 
   float qr[M][2 * CPL];
 #pragma unroll
@@ -81,8 +84,8 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
       if ((lane % lph) == 0) {
-        sc[e * p.H + head] = s0 * p.tau;
-        sc[(e + 1) * p.H + head] = s1 * p.tau;
+        sc[e * PH + head] = s0 * p.tau;
+        sc[(e + 1) * PH + head] = s1 * p.tau;
       }
     }
     for (; e < nb; ++e) {
@@ -96,11 +99,11 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qr[mm][c], kv[c], s);
       }
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((lane % lph) == 0) sc[e * p.H + head] = s * p.tau;
+      if ((lane % lph) == 0) sc[e * PH + head] = s * p.tau;
     }
     __syncwarp();
     float bm = -INFINITY;
-    for (int e2 = 0; e2 < nb; ++e2) bm = fmaxf(bm, sc[e2 * p.H + head]);
+    for (int e2 = 0; e2 < nb; ++e2) bm = fmaxf(bm, sc[e2 * PH + head]);
     const float mu2 = fmaxf(mu, bm);
     const float scale = __expf(mu - mu2);  // mu = -inf -> 0
     z *= scale;
@@ -116,14 +119,14 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
       if (e2 + 1 < nb) {
         const int jn = __float_as_int(recs[(e2 + 1) * REC + LY::OFF_J]);
 #pragma unroll
-        for (int mm = 0; mm < M; ++mm) pf_l1(v + ((size_t)jn * M + mm) * p.C + c0);
+        for (int mm = 0; mm < M; ++mm) pf_l1(v + ((size_t)jn * M + mm) * PC + c0);
       }
-      const float pr = expf(sc[e2 * p.H + head] - mu);
+      const float pr = expf(sc[e2 * PH + head] - mu);
       z += pr;
       const float s = pr * rec[LY::OFF_PHI];
       float vv[M][CPL];
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm) ldvec<CPL>(v + ((size_t)j * M + mm) * p.C + c0, vv[mm]);
+      for (int mm = 0; mm < M; ++mm) ldvec<CPL>(v + ((size_t)j * M + mm) * PC + c0, vv[mm]);
       if constexpr (EAAS) {
         value_apply<L, CPL, false>(rec, vv, s, A);
       } else {
@@ -140,9 +143,9 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
     float o[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) o[c] = A[mm][c] * inv;
-    stvec<CPL>(out + ((size_t)i * M + mm) * p.C + c0, o);
+    stvec<CPL>(out + ((size_t)i * M + mm) * PC + c0, o);
   }
-  if ((lane % lph) == 0) lse[(size_t)i * p.H + head] = z > 0.f ? mu + logf(z) : -INFINITY;
+  if ((lane % lph) == 0) lse[(size_t)i * PH + head] = z > 0.f ? mu + logf(z) : -INFINITY;
 }
 
 
@@ -151,7 +154,8 @@ es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v
                   const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
   const int tpq = kp.C / CPL;
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)Lay<L>::BP * kp.H * 4;
-  auto fn = attn_fwd_kernel<L, CPL, EAAS, T>;
+  auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_fwd_kernel<L, CPL, EAAS, T, 128, 8>
+                                                               : attn_fwd_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.N, tpq, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_kernel");
