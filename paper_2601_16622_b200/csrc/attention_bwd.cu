@@ -54,11 +54,27 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
   const int head = c0 / Ch;
   const int Dq = PDq;
 
-  // k_j / v_j are re-read per pair from L1 (one row per CTA) instead of
-  // being held in registers: halves the live state, doubles occupancy
+  // k_j / v_j: this thread's channels staged once as fp32 in shared memory
+  // ([mm][thread][2 CPL] and [mm][thread][CPL], conflict-free vector LDS)
+  // instead of registers (halves the live state) or per-pair bf16 re-reads.
   float dkr[M][2 * CPL], dvr[M][CPL];
-  const T* kj = k + (size_t)j * M * Dq + 2 * c0;
-  const T* vj = v + (size_t)j * M * PC + c0;
+  const int nthr = blockDim.x;
+  float* ks = recs + BP * REC;
+  float* vs = ks + M * nthr * 2 * CPL;
+  {
+    const T* kj = k + (size_t)j * M * Dq + 2 * c0;
+    const T* vj = v + (size_t)j * M * PC + c0;
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm) {
+      float kr[2 * CPL], vr[CPL];
+      ldvec<2 * CPL>(kj + (size_t)mm * Dq, kr);
+      ldvec<CPL>(vj + (size_t)mm * PC, vr);
+#pragma unroll
+      for (int c = 0; c < 2 * CPL; ++c) ks[(mm * nthr + threadIdx.x) * 2 * CPL + c] = kr[c];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) vs[(mm * nthr + threadIdx.x) * CPL + c] = vr[c];
+    }
+  }
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
 #pragma unroll
@@ -90,7 +106,8 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
         ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qv[mm]);
 #pragma unroll
         float kr[2 * CPL];
-        ldvec<2 * CPL>(kj + (size_t)mm * Dq, kr);
+#pragma unroll
+        for (int c = 0; c < 2 * CPL; ++c) kr[c] = ks[(mm * nthr + threadIdx.x) * 2 * CPL + c];
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[c], s);
       }
@@ -116,7 +133,8 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
         float vr[CPL];
-        ldvec<CPL>(vj + (size_t)mm * PC, vr);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) vr[c] = vs[(mm * nthr + threadIdx.x) * CPL + c];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           dvr[mm][c] = fmaf(P, y[mm][c], dvr[mm][c]);
@@ -229,7 +247,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   es_status s = cuda_status(cudaGetLastError(), "attn_delta_kernel");
   if (s != ES_OK) return s;
   const int threads = kp.C / CPL;
-  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4;
+  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)M * threads * 3 * CPL * 4;
   auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
                                                                : attn_bwd_kv_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
