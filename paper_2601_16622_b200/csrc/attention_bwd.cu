@@ -206,11 +206,7 @@ __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, i
     for (; e + UNR <= nv; e += UNR) {
       float kv[UNR][8];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const T* kp = k + (size_t)js[e + u] * n + e0;
-        ldvec<4>(kp, kv[u]);
-        ldvec<4>(kp + 4, kv[u] + 4);
-      }
+      for (int u = 0; u < UNR; ++u) ldvec<8>(k + (size_t)js[e + u] * n + e0, kv[u]);
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         const float ds = dss[(e + u) * H + h];
@@ -221,8 +217,7 @@ __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, i
     for (; e < nv; ++e) {
       const float ds = dss[e * H + h];
       float kv[8];
-      ldvec<4>(k + (size_t)js[e] * n + e0, kv);
-      ldvec<4>(k + (size_t)js[e] * n + e0 + 4, kv + 4);
+      ldvec<8>(k + (size_t)js[e] * n + e0, kv);
 #pragma unroll
       for (int t = 0; t < 8; ++t) acc[t] = fmaf(ds, kv[t], acc[t]);
     }

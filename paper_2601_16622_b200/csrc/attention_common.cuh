@@ -117,10 +117,20 @@ __device__ __forceinline__ float ldf<float>(const float* p) { return __ldg(p); }
 template <>
 __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(__ldg(p)); }
 
-// Load n (1, 2, 4) consecutive elements as floats.
+__device__ __forceinline__ float bf_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+// Load n (1, 2, 4, 8) consecutive elements as floats (bf16: exact widening by bit shifts).
 template <int n, typename T>
 __device__ __forceinline__ void ldvec(const T* p, float* o) {
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (n == 8 && sizeof(T) == 2) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    o[0] = bf_lo(u.x); o[1] = bf_hi(u.x); o[2] = bf_lo(u.y); o[3] = bf_hi(u.y);
+    o[4] = bf_lo(u.z); o[5] = bf_hi(u.z); o[6] = bf_lo(u.w); o[7] = bf_hi(u.w);
+  } else if constexpr (n == 8) {
+    ldvec<4>(p, o);
+    ldvec<4>(p + 4, o + 4);
+  } else if constexpr (sizeof(T) == 4) {
     if constexpr (n == 4) {
       const float4 v = __ldg(reinterpret_cast<const float4*>(p));
       o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
@@ -134,14 +144,10 @@ __device__ __forceinline__ void ldvec(const T* p, float* o) {
   } else {
     if constexpr (n == 4) {
       const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
-      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
-      const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
-      o[0] = fa.x; o[1] = fa.y; o[2] = fb.x; o[3] = fb.y;
+      o[0] = bf_lo(u.x); o[1] = bf_hi(u.x); o[2] = bf_lo(u.y); o[3] = bf_hi(u.y);
     } else if constexpr (n == 2) {
       const unsigned u = __ldg(reinterpret_cast<const unsigned*>(p));
-      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
-      o[0] = f.x; o[1] = f.y;
+      o[0] = bf_lo(u); o[1] = bf_hi(u);
     } else {
 #pragma unroll
       for (int a = 0; a < n; ++a) o[a] = ldf(p + a);
