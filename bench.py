@@ -71,6 +71,13 @@ def load_peaks() -> dict:
             "_source": "fallback (B200_PROFILING.md)"}
 
 
+def load_traffic():
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
+    the attention kernels from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    return json.load(open(p)) if os.path.exists(p) else None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
 
@@ -270,7 +277,13 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     if rank != 0:
         return None
     peaks = load_peaks()
+    traffic_src = load_traffic()
     dom = max(("attn_fwd", "attn_bwd"), key=lambda n: t[n])
+    dom_kernels = ["attn_fwd_tc_kernel"] if dom == "attn_fwd" else ["attn_delta_kernel", "attn_bwd_kv_kernel",
+                                                                    "attn_bwd_q_kernel"]
+    traffic = None
+    if traffic_src and all(k_ in traffic_src["bytes_per_launch"] for k_ in dom_kernels):
+        traffic = sum(traffic_src["bytes_per_launch"][k_]["total"] for k_ in dom_kernels)
     dom_bytes = by["attn_fwd"] if dom == "attn_fwd" else by["attn_bwd_kv"]
     achieved = dom_bytes / (t[dom] * 1e-3) / 1e9
     dom_flops = fl["attn_fwd"] if dom == "attn_fwd" else fl["attn_bwd"]
@@ -302,7 +315,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "kernel": "attn_fwd_tc_kernel (tcgen05)" if dom == "attn_fwd" else
                       "attn_bwd (delta + bwd_kv + bwd_q, SIMT)",
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+            "traffic_source": traffic_src["source"] if traffic is not None else None,
             "peak_source": peaks["_source"],
             "algorithmic_bytes_per_launch": dom_bytes,
             "achieved_tflops": round(dom_flops / (t[dom] * 1e-3) / 1e12, 3),

@@ -198,12 +198,17 @@ bool use_tc_kernel(const AttnArgs& a) {
   // bf16 / L=2 / C=128 / H=8 (the BASELINE shapes): the tcgen05 kernel
   // (2.9 ms vs 4.5 ms for the SIMT kernel on configs[1]); ES_ATTN_TC=0 forces
   // the SIMT kernel (kept for the other shapes and for A/B measurements).
+  // ES_ATTN_TC=1 forces it for any size (parity tests on small systems).
   static int use_tc = -1;
   if (use_tc < 0) {
     const char* e = getenv("ES_ATTN_TC");
-    use_tc = (e && e[0] == '0') ? 0 : 1;
+    use_tc = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 2 : 1;
   }
-  return use_tc && attn_tc_supported(a);
+  // one 128-query tile per CTA: below ~half a wave of tiles (N < 74 * 128)
+  // the per-atom SIMT kernel fills the GPU better (r01b sweep: SIMT faster
+  // at N = 1k..5k, tie at 10k, tcgen05 faster from 20k)
+  const bool enough_tiles = (a.N + 127) / 128 >= 74;
+  return use_tc && (enough_tiles || use_tc == 2) && attn_tc_supported(a);
 }
 }  // namespace
 

@@ -7,6 +7,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# The parity systems are small (< 74 query tiles), where the library would
+# pick the SIMT attention forward; force the tcgen05 kernel wherever its shape
+# is supported so the tests cover it (tests/test_gpu_tc_path.py re-runs the
+# bf16 cases with ES_ATTN_TC=0 for the SIMT kernel).
+os.environ.setdefault("ES_ATTN_TC", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
