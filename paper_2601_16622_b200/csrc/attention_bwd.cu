@@ -175,27 +175,35 @@ __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, i
   const int i = blockIdx.x;
   const int dqh = Dq / H;
   const int n = M * Dq;
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int cnt = 0;
-    for (int base = 0; base < K; base += 32) {
-      const int s = base + lane;
-      const int j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
-      const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
-      if (j >= 0) {
-        const int p = cnt + __popc(m & ((1u << lane) - 1u));
-        js[p] = j;
-        const float* src = dsbuf + ((size_t)i * K + s) * H;
-        if ((H & 3) == 0) {
-          for (int h = 0; h < H; h += 4)
-            *reinterpret_cast<float4*>(dss + p * H + h) = __ldg(reinterpret_cast<const float4*>(src + h));
-        } else {
-          for (int h = 0; h < H; ++h) dss[p * H + h] = __ldg(src + h);
-        }
-      }
-      cnt += __popc(m);
+  // parallel compaction: warp w ballots slots [32 w, 32 w + 32), warp
+  // counts -> exclusive prefix, then every valid lane copies its (j, dscore row)
+  __shared__ int wcnt[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = (K + 31) / 32;  // <= blockDim.x / 32 (checked at launch)
+  int j = -1, s = warp * 32 + lane;
+  unsigned m = 0;
+  if (warp < nw) {
+    j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
+    m = __ballot_sync(0xffffffffu, j >= 0);
+    if (lane == 0) wcnt[warp] = __popc(m);
+  }
+  __syncthreads();
+  if (warp < nw && j >= 0) {
+    int p = __popc(m & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; ++w) p += wcnt[w];
+    js[p] = j;
+    const float* src = dsbuf + ((size_t)i * K + s) * H;
+    if ((H & 3) == 0) {
+      for (int h = 0; h < H; h += 4)
+        *reinterpret_cast<float4*>(dss + p * H + h) = __ldg(reinterpret_cast<const float4*>(src + h));
+    } else {
+      for (int h = 0; h < H; ++h) dss[p * H + h] = __ldg(src + h);
     }
-    if (lane == 0) nvalid = cnt;
+  }
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += wcnt[w];
+    nvalid = t;
   }
   __syncthreads();
   const int nv = nvalid;
@@ -253,6 +261,8 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   {
     int tq = (M * kp.Dq / 8 + 31) / 32 * 32;
     if (tq > 1024) tq = 1024;
+    if (tq < (kp.K + 31) / 32 * 32) tq = (kp.K + 31) / 32 * 32;  // one slot per thread in the compaction
+    if (tq > 1024) return fail(ES_UNSUPPORTED, "attn_bwd: K > 1024");
     const size_t qsm = (size_t)kp.K * (1 + kp.H) * 4;
     if (qsm > 200 * 1024) return fail(ES_UNSUPPORTED, "attn_bwd: K * (H + 1) too large for the dq pass");
     if (qsm > 48 * 1024)
