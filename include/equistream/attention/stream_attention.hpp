@@ -114,10 +114,10 @@ inline std::size_t backward_workspace_size(const AttentionProblem& p) {
 inline void stream_aggregate_backward(const AttentionProblem& p, const void* grad_m, const void* q, const void* k,
                                       const void* v, const double* pos, const NeighborIndex& idx, const void* m,
                                       const float* lse, void* grad_q, void* grad_k, void* grad_v, void* workspace,
-                                      std::size_t ws_bytes, void* stream = nullptr) {
+                                      std::size_t ws_bytes, void* stream = nullptr, double* grad_pos = nullptr) {
   const es_attn_desc d = p.desc();
   check(es_attn_bwd(&d, q, k, v, pos, idx.table, idx.rev_ptr, idx.rev_pair, m, lse, grad_m, grad_q, grad_k, grad_v,
-                    workspace, ws_bytes, stream),
+                    grad_pos, workspace, ws_bytes, stream),
         "stream_aggregate_backward");
 }
 

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 3
+#define ES_ABI_VERSION 4
 
 typedef enum {
   ES_OK = 0,
@@ -104,12 +104,16 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
 
 /* Workspace: es_attn_bwd_workspace_size(d) bytes (per-pair-head dscore
  * buffer, O(N*K*H) scalars -- never O(N*K*C)). rev_ptr/rev_pair
- * come from es_neighbors_transpose on the same nbr. */
+ * come from es_neighbors_transpose on the same nbr.
+ * dpos (optional, NULL = skip): [Nk][3] f64 gradient of sum <dout, out> with
+ * respect to the atom positions (forces for the conservative mode, PAPER.md:
+ * 786) through phi(r_ij) and the solid harmonics of the value
+ * map; L = 2 only (ES_UNSUPPORTED otherwise).  Overwritten, not accumulated. */
 size_t es_attn_bwd_workspace_size(const es_attn_desc* d);
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
-                      const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace,
-                      size_t workspace_bytes, void* stream);
+                      const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
+                      void* workspace, size_t workspace_bytes, void* stream);
 
 /* Neighbour index: per atom the K nearest j != i with d^2 < r_cut^2, sorted
  * by (d^2, j), padded with -1, restricted to the atom's segment

@@ -66,7 +66,7 @@ def lib() -> ct.CDLL:
         L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 8 + [sz, vp]
         L.es_attn_fwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_fwd_workspace_size.restype = sz
-        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 14 + [sz, vp]
+        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 15 + [sz, vp]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]
@@ -84,7 +84,7 @@ def lib() -> ct.CDLL:
         L.es_cg_real.argtypes = [i32] * 6
         L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
         L.es_wigner_d_host.argtypes = [i32, dp, dp]
-        if L.es_abi_version() != 3:
+        if L.es_abi_version() != 4:
             raise EsError("libequistream_b200.so ABI mismatch: rebuild (python -m paper_2601_16622_b200.build)")
         _lib = L
     return _lib

@@ -255,9 +255,12 @@ def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row
     return out, lse
 
 
-def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention):
+def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_grad: bool = False):
     """stream_aggregate_backward (SPEC.md:293): (grad_q, grad_k, grad_v) of
-    sum <grad_m, m>, by recomputation (no O(N*K*C) buffer)."""
+    sum <grad_m, m>, by recomputation (no O(N*K*C) buffer).  pos_grad=True
+    (L = 2) also returns grad_pos [Nk][3] f64 -- the position gradient through
+    phi(r_ij) and the solid harmonics of the value map (forces):
+    (grad_q, grad_k, grad_v, grad_pos)."""
     s = saved
     N, C, Nk = _check_qkv(s.q, s.k, s.v, s.pos, s.idx, s.cfg, s.row0)
     grad_m = _need(grad_m.contiguous(), "grad_m", s.q.dtype, tuple(s.out.shape))
@@ -267,7 +270,8 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention):
     dq = torch.empty_like(s.q)
     dk = torch.empty_like(s.k)
     dv = torch.empty_like(s.v)
+    dpos = torch.empty((Nk, 3), dtype=torch.float64, device=s.q.device) if pos_grad else None
     check(lib().es_attn_bwd(ct.byref(d), _ptr(s.q), _ptr(s.k), _ptr(s.v), _ptr(s.pos), _ptr(s.idx.table),
                             _ptr(rev_ptr), _ptr(rev_pair), _ptr(s.out), _ptr(s.lse), _ptr(grad_m), _ptr(dq),
-                            _ptr(dk), _ptr(dv), _ptr(ws), ws.numel(), _stream()), "es_attn_bwd")
-    return dq, dk, dv
+                            _ptr(dk), _ptr(dv), _ptr(dpos), _ptr(ws), ws.numel(), _stream()), "es_attn_bwd")
+    return (dq, dk, dv, dpos) if pos_grad else (dq, dk, dv)

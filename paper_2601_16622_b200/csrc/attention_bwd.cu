@@ -1,4 +1,5 @@
 // Backward of the fused equivariant attention; see attention_common.cuh.
+#include "_gen_cg.h"
 #include "attention_common.cuh"
 
 namespace es {
@@ -30,14 +31,19 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 // dk_j, dv_j exclusively (no atomics) and the per-pair-head dscore.
 // CC, HH > 0: channels / heads fixed at compile time (the BASELINE shape C=128,
 // H=8): row strides become immediates, no per-row 64-bit address arithmetic.
-template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0>
+// FORCE: also the position gradients (L = 2): per pair
+//   dL/dr_ij = sum_h P_ij^h [phi'(r) r^ sum_f Y^f(r) D_f^h + phi sum_f grad Y^f(r) D_f^h],
+//   D_f^h = dO_i^h . (G_f v_j)^h   (the value map x = phi sum_f Y^f G_f v, == EAAS),
+// scattered to dpos_j (+) and dpos_i (-) with fp64 atomics.
+template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0, bool FORCE = false>
 __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
                                                           const int* __restrict__ rev_pair,
                                                           const float* __restrict__ lse, const T* __restrict__ dout,
                                                           const float* __restrict__ delta, T* __restrict__ dk,
-                                                          T* __restrict__ dv, float* __restrict__ dsbuf) {
+                                                          T* __restrict__ dv, float* __restrict__ dsbuf,
+                                                          double* __restrict__ dpos) {
   const int PC = CC ? CC : p.C, PH = HH ? HH : p.H, PDq = CC ? 2 * CC : p.Dq;
   using LY = Lay<L>;
   constexpr int M = LY::M;
@@ -58,6 +64,7 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
   // ([mm][thread][2 CPL] and [mm][thread][CPL], conflict-free vector LDS)
   // instead of registers (halves the live state) or per-pair bf16 re-reads.
   float dkr[M][2 * CPL], dvr[M][CPL];
+  double fj[3] = {0.0, 0.0, 0.0};  // FORCE: this warp's share of dL/dpos_j
   const int nthr = blockDim.x;
   float* ks = recs + BP * REC;
   float* vs = ks + M * nthr * 2 * CPL;
@@ -143,12 +150,76 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
       }
       for (int o = lph >> 1; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
       const float ds = P * (dp - delta[(size_t)i * PH + head]);
+      if constexpr (FORCE) {
+        static_assert(L == 2, "position gradients are implemented for L = 2");
+        const float rx = rec[LY::OFF_R], ry = rec[LY::OFF_R + 1], rz = rec[LY::OFF_R + 2];
+        const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+        const float inv = rn > 1e-12f ? 1.f / rn : 0.f;
+        const float dphi = rec[LY::OFF_DPHI];
+        float gx, gy, gz;
+        if constexpr (EAAS) {
+          float vv[M][2];
+#pragma unroll
+          for (int mm = 0; mm < M; ++mm) {
+            vv[mm][0] = vs[(mm * nthr + threadIdx.x) * CPL];
+            vv[mm][1] = CPL > 1 ? vs[(mm * nthr + threadIdx.x) * CPL + (CPL > 1 ? 1 : 0)] : 0.f;
+          }
+          float Df[M];
+#pragma unroll
+          for (int f = 0; f < M; ++f) Df[f] = 0.f;
+          es_vg_all(vv, [&](int o, int f, float x0, float x1) {
+            Df[f] = fmaf(g[o][0], x0, Df[f]);
+            if constexpr (CPL > 1) Df[f] = fmaf(g[o][CPL > 1 ? 1 : 0], x1, Df[f]);
+          });
+#pragma unroll
+          for (int f = 0; f < M; ++f)
+            for (int o = lph >> 1; o > 0; o >>= 1) Df[f] += __shfl_xor_sync(0xffffffffu, Df[f], o);
+          float Y[9], dY[9][3];
+          solid2_grad(rx, ry, rz, Y, dY);
+          float s0 = 0.f, s1x = 0.f, s1y = 0.f, s1z = 0.f;
+#pragma unroll
+          for (int f = 0; f < M; ++f) {
+            s0 = fmaf(Y[f], Df[f], s0);
+            s1x = fmaf(dY[f][0], Df[f], s1x);
+            s1y = fmaf(dY[f][1], Df[f], s1y);
+            s1z = fmaf(dY[f][2], Df[f], s1z);
+          }
+          const float a = dphi * inv * s0;
+          gx = P * (a * rx + phi * s1x);
+          gy = P * (a * ry + phi * s1y);
+          gz = P * (a * rz + phi * s1z);
+        } else {  // x = phi v_j: only phi depends on r
+          const float dpr = phi != 0.f ? dp / phi : 0.f;
+          const float a = P * dphi * inv * dpr;
+          gx = a * rx; gy = a * ry; gz = a * rz;
+        }
+        // every lane holds its head's value: sum the heads of this warp
+        for (int o = lph; o < 32; o <<= 1) {
+          gx += __shfl_xor_sync(0xffffffffu, gx, o);
+          gy += __shfl_xor_sync(0xffffffffu, gy, o);
+          gz += __shfl_xor_sync(0xffffffffu, gz, o);
+        }
+        if (lane == 0) {
+          const size_t ia = (size_t)(p.row0 + i);
+          atomicAdd(dpos + 3 * ia, -(double)gx);
+          atomicAdd(dpos + 3 * ia + 1, -(double)gy);
+          atomicAdd(dpos + 3 * ia + 2, -(double)gz);
+          fj[0] += gx; fj[1] += gy; fj[2] += gz;
+        }
+      }
       const float tds = p.tau * ds;
 #pragma unroll
       for (int mm = 0; mm < M; ++mm)
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
       if ((lane % lph) == 0) dsbuf[(size_t)pr * PH + head] = ds;
+    }
+  }
+  if constexpr (FORCE) {
+    if (lane == 0) {
+      atomicAdd(dpos + 3 * (size_t)j, fj[0]);
+      atomicAdd(dpos + 3 * (size_t)j + 1, fj[1]);
+      atomicAdd(dpos + 3 * (size_t)j + 2, fj[2]);
     }
   }
 #pragma unroll
@@ -240,8 +311,9 @@ template <int L, int CPL, bool EAAS, typename T>
 es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
                   const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                   const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, float* dsbuf,
-                  cudaStream_t st) {
+                  double* dpos, cudaStream_t st) {
   constexpr int M = Lay<L>::M;
+  if (dpos && L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
   {
     const int apb = 256 / (kp.C / 2);
     attn_delta_kernel<T><<<(kp.N + apb - 1) / apb, apb * (kp.C / 2), 0, st>>>(kp.N, M, kp.C, kp.H, (const T*)out,
@@ -253,9 +325,16 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)M * threads * 3 * CPL * 4;
   auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
                                                                : attn_bwd_kv_kernel<L, CPL, EAAS, T>;
+  if constexpr (L == 2) {
+    if (dpos) {
+      fn = attn_bwd_kv_kernel<L, CPL, EAAS, T, 0, 0, true>;
+      s = cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)kp.Nk, st), "attn_bwd: dpos");
+      if (s != ES_OK) return s;
+    }
+  }
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.Nk, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
-                                  (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf);
+                                  (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf, dpos);
   s = cuda_status(cudaGetLastError(), "attn_bwd_kv_kernel");
   if (s != ES_OK) return s;
   {
@@ -308,12 +387,16 @@ struct BwdOp {
 es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
                           const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
-                          float* dsbuf, cudaStream_t st) {
+                          float* dsbuf, double* dpos, cudaStream_t st) {
   es_status s = upload_tables_tu();
   if (s != ES_OK) return s;
   const KParams kp = make_params(a);
-  if (a.N == 0) return ES_OK;
-  return dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, st);
+  if (a.N == 0) {
+    if (dpos) return cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)a.Nk, st), "attn_bwd: dpos");
+    return ES_OK;
+  }
+  return dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf,
+                         dpos, st);
 }
 
 }  // namespace es

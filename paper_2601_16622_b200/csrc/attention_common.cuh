@@ -71,12 +71,14 @@ struct Lay {
   static constexpr int OFF_PHI = ND + 2 * NE;
   static constexpr int OFF_J = OFF_PHI + 1;
   static constexpr int OFF_X = OFF_PHI + 2;  // spare (query slot in backward)
+  static constexpr int OFF_DPHI = OFF_PHI + 3;  // dphi/dr (position gradients)
+  static constexpr int OFF_R = OFF_PHI + 4;     // r_ij as fp32 (3)
   // L <= 2: the per-pair EAAS steps (align D, sparse re-index P, un-align D^T)
   // are composed once per pair into the M x M operator T = D^T P D, so each
   // channel costs M^2 = 81 MACs instead of 107 (at L = 4 the three sparse
   // EAAS steps are cheaper than M^2 = 625 and are applied directly).
   static constexpr bool COMPOSE = false;  // measured: no gain on B200 (pair prep is the longer chain)
-  static constexpr int OFF_T = ((OFF_PHI + 4) + 3) / 4 * 4;
+  static constexpr int OFF_T = ((OFF_PHI + 7) + 3) / 4 * 4;
   static constexpr int REC = COMPOSE ? OFF_T + (M * M + 3) / 4 * 4 : OFF_T;
   static constexpr int BP = (L <= 2) ? 64 : 32;  // pairs per batch
 };
@@ -288,6 +290,24 @@ __device__ __forceinline__ void compose_rec(float* rec) {
 template <int L>
 __device__ __forceinline__ void compose_t(float* rec) { compose_rec<L, 0, 0>(rec); }
 
+// Real solid harmonics of degree <= 2 in the library convention (row
+// l*l+m+l; Y^1 = c1 (y, z, -x)) and their gradients -- the R^{l_f}(r) of the
+// per-pair value map x = phi sum_f Y^f(r) G_f v (same map as EAAS, Prop. 1),
+// differentiated for the position gradients.
+__device__ __forceinline__ void solid2_grad(float x, float y, float z, float (&Y)[9], float (&G)[9][3]) {
+  const float c0 = 0.28209479177387814f, c1 = 0.4886025119029199f, c2 = 1.0925484305920792f,
+              c20 = 0.6307831305050401f;
+  Y[0] = c0; G[0][0] = 0.f; G[0][1] = 0.f; G[0][2] = 0.f;
+  Y[1] = c1 * y; G[1][0] = 0.f; G[1][1] = c1; G[1][2] = 0.f;
+  Y[2] = c1 * z; G[2][0] = 0.f; G[2][1] = 0.f; G[2][2] = c1;
+  Y[3] = -c1 * x; G[3][0] = -c1; G[3][1] = 0.f; G[3][2] = 0.f;
+  Y[4] = c2 * x * y; G[4][0] = c2 * y; G[4][1] = c2 * x; G[4][2] = 0.f;
+  Y[5] = c2 * y * z; G[5][0] = 0.f; G[5][1] = c2 * z; G[5][2] = c2 * y;
+  Y[6] = c20 * (z * z - 0.5f * (x * x + y * y)); G[6][0] = -c20 * x; G[6][1] = -c20 * y; G[6][2] = 2.f * c20 * z;
+  Y[7] = -c2 * x * z; G[7][0] = -c2 * z; G[7][1] = 0.f; G[7][2] = -c2 * x;
+  Y[8] = 0.5f * c2 * (x * x - y * y); G[8][0] = c2 * x; G[8][1] = -c2 * y; G[8][2] = 0.f;
+}
+
 struct KParams {
   int N, K, H, C, Dq;
   int row0, Nk;  // query i <-> atom row0 + i (pos); keys j index k/v/pos in [0, Nk)
@@ -316,6 +336,12 @@ __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, i
   if (p.phi_mode == 0) phi = rn < p.r_cut ? 0.5f * (cospif(rn * p.inv_rcut) + 1.f) : 0.f;
   rec[Lay<L>::OFF_PHI] = phi;
   rec[Lay<L>::OFF_J] = __int_as_float(j);
+  // phi'(r) = -(pi / 2 r_cut) sin(pi r / r_cut) inside the cutoff
+  rec[Lay<L>::OFF_DPHI] =
+      (p.phi_mode == 0 && rn < p.r_cut) ? -0.5f * 3.14159265358979f * p.inv_rcut * sinpif(rn * p.inv_rcut) : 0.f;
+  rec[Lay<L>::OFF_R] = rx;
+  rec[Lay<L>::OFF_R + 1] = ry;
+  rec[Lay<L>::OFF_R + 2] = rz;
   if constexpr (EAAS) {
     float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
     if (rn > 1e-8f) {

@@ -160,12 +160,16 @@ size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
 
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
-                      const float* lse, const void* dout, void* dq, void* dk, void* dv, void* workspace,
-                      size_t workspace_bytes, void* stream) {
+                      const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
+                      void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
-    if (d->N == 0) return ES_OK;
+    if (dpos && d->L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
+    if (d->N == 0)
+      return dpos ? attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv,
+                                    nullptr, nullptr, dpos, (cudaStream_t)stream)
+                  : ES_OK;
     if (!q || !k || !v || !pos || !nbr || !rev_ptr || !rev_pair || !out || !lse || !dout || !dq || !dk || !dv)
       return fail(ES_INVALID_ARGUMENT, "attn_bwd: null buffer");
     if (!workspace || workspace_bytes < es_attn_bwd_workspace_size(d))
@@ -173,7 +177,7 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
     float* delta = (float*)workspace;
     float* dsbuf = (float*)((char*)workspace + align256(sizeof(float) * (size_t)d->N * d->H));
     return attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta,
-                           dsbuf, (cudaStream_t)stream);
+                           dsbuf, dpos, (cudaStream_t)stream);
   });
 }
 

@@ -23,9 +23,12 @@ class _AttnFn(torch.autograd.Function):
     def backward(ctx, grad_out):
         h, W, q, k, v, out, lse, pos = ctx.saved_tensors
         saved = SavedAttention(q, k, v, pos, ctx.idx, out, lse, ctx.cfg)
-        dq, dk, dv = stream_aggregate_backward(grad_out.contiguous().to(q.dtype), saved)
+        want_pos = ctx.needs_input_grad[2]  # positions require grad: forces (L = 2)
+        grads = stream_aggregate_backward(grad_out.contiguous().to(q.dtype), saved, pos_grad=want_pos)
+        dq, dk, dv = grads[:3]
         dh, dW = project_qk_backward(h, W, ctx.cfg.L, dq, dk, dv, want_dW=ctx.needs_input_grad[1])
-        return dh, (dW.to(W.dtype) if dW is not None else None), None, None, None
+        dpos = grads[3].to(pos.dtype) if want_pos else None
+        return dh, (dW.to(W.dtype) if dW is not None else None), dpos, None, None
 
 
 def attention_layer(h: torch.Tensor, W: torch.Tensor, pos: torch.Tensor, idx: NeighborIndex,

@@ -350,3 +350,79 @@ def test_row_sharded_attention_matches_unsharded(es, dtype):
     assert rel(torch.cat(dqs).float().cpu(), dq.float().cpu()) < tol
     assert rel(dk_sum.cpu(), dk.float().cpu()) < tol
     assert rel(dv_sum.cpu(), dv.float().cpu()) < tol
+
+
+# ------------------------------------------------------------------ position gradients
+def _fd_pos_grad(P, q, k, v, pos, nbr, dout, h=1e-5):
+    """Central differences of L(pos) = sum <dout, out(pos)> through the fp64
+    oracle forward, neighbour list held fixed (what the analytic gradient
+    differentiates)."""
+    g = np.zeros_like(pos)
+    for a in range(pos.shape[0]):
+        for d in range(3):
+            pp, pm = pos.copy(), pos.copy()
+            pp[a, d] += h
+            pm[a, d] -= h
+            fp = float(np.sum(dout * po.attn_fwd(P, q, k, v, pp, nbr)[0]))
+            fm = float(np.sum(dout * po.attn_fwd(P, q, k, v, pm, nbr)[0]))
+            g[a, d] = (fp - fm) / (2 * h)
+    return g
+
+
+@pytest.mark.parametrize("kind,vm,dtype", [("open", "eaas", torch.float32), ("pbc", "eaas", torch.float32),
+                                           ("batch", "plain", torch.float32), ("open", "eaas", torch.bfloat16)])
+def test_position_gradients_match_finite_differences(es, oracle, kind, vm, dtype):
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    L, C, H, K = 2, 64, 8, 64
+    box = None
+    if kind == "pbc":
+        b = S.periodic_box(48, 3, 3.8, 21)
+        pos, seg, box = b.pos, None, b.box
+    elif kind == "batch":
+        b = S.molecule_batch(3, 12, 16, 22)
+        pos, seg = b.pos, b.seg_ptr
+    else:
+        pos, seg = S.gen_fcc_system(36, 3.8, 23), None
+    N = len(pos)
+    nbr, _, _ = po.build_neighbors(pos, K, 6.0, seg_ptr=seg, box=box)
+    hf = S.random_features(N, L, C, 24)
+    W = S.random_weights(L, C, 24)
+    q, k, v = po.project(hf, W, L)
+    dout = np.random.default_rng(25).standard_normal((N, 9, C))
+    if dtype == torch.bfloat16:
+        q, k, v, dout = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v, dout))
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE if vm == "eaas" else po.VALUE_PLAIN, box=box)
+    ref = _fd_pos_grad(P, q, k, v, pos, nbr, dout)
+    cfg = AttentionConfig(heads=H, L=L, r_cut=6.0, value_mode=vm, box=None if box is None else tuple(box))
+    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    tq, tk, tv, tp = dev(q, dtype), dev(k, dtype), dev(v, dtype), dev(pos)
+    out, lse = es.stream_aggregate(tq, tk, tv, tp, idx, cfg)
+    *_, dpos = es.stream_aggregate_backward(dev(dout, dtype), SavedAttention(tq, tk, tv, tp, idx, out, lse, cfg),
+                                            pos_grad=True)
+    got = dpos.cpu().numpy()
+    assert rel(got, ref) < (F32_TOL if dtype == torch.float32 else BF16_TOL)
+    # translation invariance: the gradients sum to zero
+    assert np.abs(got.sum(0)).max() < 1e-4 * np.abs(got).max()
+
+
+def test_position_gradients_autograd_and_unsupported(es):
+    """pos.requires_grad through the autograd layer; L != 2 is ES_UNSUPPORTED."""
+    from paper_2601_16622_b200 import _lib
+    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention
+    L, C, H = 2, 64, 8
+    b = S.molecule_batch(4, 20, 30, 26)
+    pos = dev(b.pos).requires_grad_(True)
+    idx = es.build_neighbors(pos.detach(), 64, 6.0, dev(b.seg_ptr))
+    h = dev(S.random_features(len(b.pos), L, C, 27), torch.float32)
+    W = dev(S.random_weights(L, C, 27), torch.float32)
+    out = es.attention_layer(h, W, pos, idx, AttentionConfig(heads=H, L=L))
+    out.square().sum().backward()
+    assert pos.grad is not None and torch.isfinite(pos.grad).all() and pos.grad.abs().max() > 0
+    q = torch.randn(10, 4, 2 * C, device="cuda")
+    k, v = q.clone(), torch.randn(10, 4, C, device="cuda")
+    p1 = dev(S.gen_fcc_system(10, 3.8, 1))
+    i1 = es.build_neighbors(p1, 16, 6.0)
+    cfg = AttentionConfig(heads=H, L=1)
+    o1, l1 = es.stream_aggregate(q, k, v, p1, i1, cfg)
+    with pytest.raises(_lib.EsUnsupported):
+        es.stream_aggregate_backward(torch.ones_like(o1), SavedAttention(q, k, v, p1, i1, o1, l1, cfg), pos_grad=True)
