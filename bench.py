@@ -151,25 +151,26 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     rng = np.random.default_rng(seed)
     h_host = rng.standard_normal((N, M, C_)).astype(np.float32)
     W_host = (rng.standard_normal((L_ + 1, C_, 5 * C_)) / np.sqrt(C_)).astype(np.float32)
-    g_host = rng.standard_normal((N, M, C_)).astype(np.float32)
     cfg = AttentionConfig(heads=H_, L=L_, r_cut=RCUT, value_mode="eaas")
 
     pos = torch.tensor(batch.pos, device=dev)
     seg = torch.tensor(batch.seg_ptr, device=dev)
     h = torch.tensor(h_host, device=dev).to(dtype)
     W = torch.tensor(W_host, device=dev).to(dtype)
-    gout = torch.tensor(g_host, device=dev).to(dtype)
 
-    def step(pos, seg, h, W, gout):
+    # One training-like pass: loss = 1/2 ||out||^2 on the device, so the
+    # gradient seed is dout = out (no upstream gradient crosses PCIe); the
+    # step's result is dW (what an optimizer consumes).
+    def step(pos, seg, h, W):
         idx = es.build_neighbors(pos, K_, RCUT, seg, with_distances=False)
         idx.transpose()
         q, k, v = es.project_qk(h, W, L_)
         out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
-        dq, dk, dv = es.stream_aggregate_backward(gout, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
+        dq, dk, dv = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
         dh, dW = es.project_qk_backward(h, W, L_, dq, dk, dv)
         return idx, dh, dW
 
-    idx, _, _ = step(pos, seg, h, W, gout)
+    idx, _, _ = step(pos, seg, h, W)
     torch.cuda.synchronize()
     E = int(idx.count.sum().item())
     fl = flops_per_step(N, E)
@@ -177,7 +178,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     by = attn_bytes(N, E, K_, s_bytes)
 
     for _ in range(args.warmup):
-        step(pos, seg, h, W, gout)
+        step(pos, seg, h, W)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -187,7 +188,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     with ClockSampler(local_rank) as clk:
         e0.record(st)
         for _ in range(args.steps):
-            step(pos, seg, h, W, gout)
+            step(pos, seg, h, W)
         e1.record(st)
         torch.cuda.synchronize()
     if world > 1:
@@ -204,7 +205,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     t = {}
     for name, fn in (("attn_fwd", lambda: es.stream_aggregate(q, k, v, pos, idx, cfg)),
                      ("attn_bwd", lambda: es.stream_aggregate_backward(
-                         gout, SavedAttention(q, k, v, pos, idx, out, lse, cfg))),
+                         out, SavedAttention(q, k, v, pos, idx, out, lse, cfg))),
                      ("proj_fwd", lambda: es.project_qk(h, W, L_)),
                      ("neighbors", lambda: es.build_neighbors(pos, K_, RCUT, seg, with_distances=False))):
         fn()
@@ -217,26 +218,26 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         t[name] = a.elapsed_time(b) / 3
 
     # end to end through the public API with HOST buffers (pinned, the
-    # user's storage dtype), H2D of every step's inputs and D2H of its result
-    # (dW) inside the timed region; copies run on a side stream, double
-    # buffered so step s+1's upload overlaps step s's kernels.
+    # user's storage dtype): H2D of every step's inputs (positions, segment
+    # table, node features h, weights W) and D2H of its result (dW) inside
+    # the timed region; copies run on a side stream, double buffered so step
+    # s+1's upload overlaps step s's kernels.
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()  # noqa: E731
     hp = pin(h_host).to(dtype).pin_memory()
-    gp = pin(g_host).to(dtype).pin_memory()
     Wp = pin(W_host).to(dtype).pin_memory()
     posp, segp = pin(batch.pos), pin(batch.seg_ptr)
     dW_host = torch.empty((L_ + 1, C_, 5 * C_), dtype=torch.float32).pin_memory()
-    h2d = sum(x.numel() * x.element_size() for x in (hp, Wp, gp, posp, segp))
+    h2d = sum(x.numel() * x.element_size() for x in (hp, Wp, posp, segp))
     d2h = dW_host.numel() * 4
     cs = torch.cuda.Stream(device=dev)
-    bufs = [[torch.empty_like(x, device=dev) for x in (posp, segp, hp, Wp, gp)] for _ in range(2)]
+    bufs = [[torch.empty_like(x, device=dev) for x in (posp, segp, hp, Wp)] for _ in range(2)]
     copied = [torch.cuda.Event() for _ in range(2)]
     freed = [torch.cuda.Event() for _ in range(2)]
 
     def upload(slot):
         with torch.cuda.stream(cs):
             cs.wait_event(freed[slot])
-            for d_, h_ in zip(bufs[slot], (posp, segp, hp, Wp, gp)):
+            for d_, h_ in zip(bufs[slot], (posp, segp, hp, Wp)):
                 d_.copy_(h_, non_blocking=True)
             copied[slot].record(cs)
 
@@ -303,7 +304,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         "data": "synthetic (FCC molecules, random features/weights; seeded)",
         "config": {
             "workload": "configs[1] SPICE-like batch: 4096 molecules x U{40..60} atoms per GPU, L_max=2, C=128, "
-                        "H=8, r_cut=6 A, fwd+bwd (neighbours + projections + fused EAAS attention + backward)",
+                        "H=8, r_cut=6 A, fwd+bwd (neighbours + projections + fused EAAS attention + backward; "
+                        "loss = 1/2 ||out||^2 on the device, dout = out)",
             "molecules_per_gpu": args.molecules, "atoms_per_gpu": N, "pairs_per_gpu": E,
             "atoms_total": total_atoms, "pairs_total": total_pairs, "K": K_, "L_max": L_, "channels": C_,
             "heads": H_, "precision": f"{args.dtype} storage, fp32 accumulation",
@@ -352,13 +354,12 @@ def cpu_baseline(n_mol: int, threads: int | None, seed: int = 0) -> dict:
     rng = np.random.default_rng(seed)
     h = rng.standard_normal((N, M, C_))
     W = rng.standard_normal((L_ + 1, C_, 5 * C_)) / np.sqrt(C_)
-    g = rng.standard_normal((N, M, C_))
     t0 = time.perf_counter()
     nbr, _, cnt = po.build_neighbors(b.pos, K_, RCUT, seg_ptr=b.seg_ptr)
     q, k, v = po.project(h, W, L_)
     P = po.AttnProblem(L=L_, H=H_, value_mode=po.VALUE_EAAS)
     out, lse = po.attn_fwd(P, q, k, v, b.pos, nbr)
-    dq, dk, dv = po.attn_bwd(P, q, k, v, b.pos, nbr, out, lse, g)
+    dq, dk, dv = po.attn_bwd(P, q, k, v, b.pos, nbr, out, lse, out)  # loss = 1/2 ||out||^2
     po.project_bwd(h, W, L_, dq, dk, dv)
     dt = time.perf_counter() - t0
     fl = flops_per_step(N, int(cnt.sum()))
