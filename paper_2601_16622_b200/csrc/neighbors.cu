@@ -274,34 +274,57 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
 }
 
 // ---------------------------------------------------------------- transpose
-__global__ void tr_keys_kernel(int N, int K, int Nk, const int32_t* __restrict__ nbr, unsigned* __restrict__ key,
-                               int* __restrict__ val, int* __restrict__ cnt) {
+// Counting-sort transpose (no radix sort of the N*K slots): count the
+// pairs per key, exclusive-scan into rev_ptr, scatter each pair to its key's
+// segment with an atomic cursor, then restore the stable order (ascending
+// pair index i*K + s) with a per-key insertion sort -- segments hold the
+// ~15-55 queries of one key, so the sort is a few hundred register ops.
+__global__ void tr_count_kernel(int N, int K, const int32_t* __restrict__ nbr, int* __restrict__ cnt) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (size_t)N * K) return;
   const int j = nbr[t];
-  key[t] = j >= 0 ? (unsigned)j : (unsigned)Nk;
-  val[t] = (int)t;
   if (j >= 0) atomicAdd(&cnt[j], 1);
+}
+
+__global__ void tr_fill_kernel(int N, int K, const int32_t* __restrict__ nbr, const int* __restrict__ rev_ptr,
+                               int* __restrict__ cursor, int32_t* __restrict__ rev_pair) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * K) return;
+  const int j = nbr[t];
+  if (j < 0) return;
+  rev_pair[rev_ptr[j] + atomicAdd(&cursor[j], 1)] = (int32_t)t;
+}
+
+__global__ void tr_sort_kernel(int Nk, const int* __restrict__ rev_ptr, int32_t* __restrict__ rev_pair) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Nk) return;
+  const int b = rev_ptr[j], e = rev_ptr[j + 1];
+  for (int x = b + 1; x < e; ++x) {
+    const int32_t v = rev_pair[x];
+    int y = x;
+    while (y > b && rev_pair[y - 1] > v) {
+      rev_pair[y] = rev_pair[y - 1];
+      --y;
+    }
+    rev_pair[y] = v;
+  }
 }
 
 namespace {
 struct TrWs {
-  size_t key, skey, val, cnt, cub, total, cub_sort, cub_scan;
+  size_t cnt, cursor, cub, total, cub_scan;
 };
 TrWs tr_ws(int N, int K, int Nk) {
+  (void)N;
+  (void)K;
   TrWs w{};
-  const int n = N * K;
-  size_t cs = 0, cc = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, cs, (unsigned*)nullptr, (unsigned*)nullptr, (int*)nullptr,
-                                  (int*)nullptr, n);
+  size_t cc = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cc, (int*)nullptr, (int*)nullptr, Nk + 1);
   size_t o = 0;
-  w.key = o; o += align256(sizeof(unsigned) * n);
-  w.skey = o; o += align256(sizeof(unsigned) * n);
-  w.val = o; o += align256(sizeof(int) * n);
   w.cnt = o; o += align256(sizeof(int) * (Nk + 1));
-  w.cub = o; o += align256(cs > cc ? cs : cc);
-  w.cub_sort = cs; w.cub_scan = cc;
+  w.cursor = o; o += align256(sizeof(int) * (Nk + 1));
+  w.cub = o; o += align256(cc);
+  w.cub_scan = cc;
   w.total = o;
   return w;
 }
@@ -318,21 +341,18 @@ es_status nbr_transpose_launch(int N, int K, int Nk, const int32_t* nbr, int32_t
     return ES_OK;
   }
   char* base = (char*)ws;
-  unsigned* key = (unsigned*)(base + w.key);
-  unsigned* skey = (unsigned*)(base + w.skey);
-  int* val = (int*)(base + w.val);
   int* cnt = (int*)(base + w.cnt);
-  const int n = N * K;
+  int* cursor = (int*)(base + w.cursor);
+  const size_t n = (size_t)N * K;
+  const unsigned blocks = (unsigned)((n + 255) / 256);
   cudaMemsetAsync(cnt, 0, sizeof(int) * (Nk + 1), st);
-  tr_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(N, K, Nk, nbr, key, val, cnt);
-  int bits = 1;
-  while ((1u << bits) <= (unsigned)Nk) ++bits;
-  size_t cb = w.cub_sort;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(base + w.cub, cb, key, skey, val, (int*)rev_pair, n, 0, bits, st);
-  if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: sort");
-  cb = w.cub_scan;
-  e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, Nk + 1, st);
+  cudaMemsetAsync(cursor, 0, sizeof(int) * (Nk + 1), st);
+  tr_count_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, cnt);
+  size_t cb = w.cub_scan;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, Nk + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: scan");
+  tr_fill_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, rev_ptr, cursor, rev_pair);
+  tr_sort_kernel<<<(Nk + 127) / 128, 128, 0, st>>>(Nk, rev_ptr, rev_pair);
   return cuda_status(cudaGetLastError(), "neighbors_transpose");
 }
 
