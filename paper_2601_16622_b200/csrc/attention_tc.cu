@@ -72,9 +72,22 @@ struct TcTab {
   int ofs[MM * MM + 1];  // (o, f) -> entry range
 };
 __constant__ TcTab c_tc;
+// Per-chunk event clocks of CTA 0 (compile with -DES_TC_TRACE, run with
+// ES_TC_DBG=16): producer / MMA / row / Vg timelines, the tool used to find
+// this kernel's critical path.
+#ifdef ES_TC_TRACE
 __device__ long long g_trace[8][128];
 __device__ long long g_trace_w[8][128];  // per row warp: Wt arrive clock
-__device__ long long g_trace_r[4][128];  // row thread 64: before Wt-free wait, after it, after the phase barrier  // ES_TC_DBG&16: per-chunk event clocks of CTA 0
+__device__ long long g_trace_r[4][128];  // row thread 64: before / after the Wt-free wait, after the phase barrier
+#define TC_TRACE(cond, slot) \
+  do {                       \
+    if (TRACE && (cond) && g < 128) slot = clock64(); \
+  } while (0)
+#else
+#define TC_TRACE(cond, slot) \
+  do {                       \
+  } while (0)
+#endif
 
 struct TcArgs {
   int N, K, row0, Nk;
@@ -147,7 +160,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * TQ;
+#ifdef ES_TC_TRACE
   const bool TRACE = (a.dbg & 16) && blockIdx.x == 0;
+#endif
   const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
   const bool is_row = warp >= 2 && warp <= 9;
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
@@ -213,7 +228,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             if (cp < nch) prefetch(h, cp);
             else if (h + 1 < 8 && cp - nch < nch) prefetch(h + 1, cp - nch);
           }
-          if (TRACE && g < 128) g_trace[7][g] = clock64();
+          TC_TRACE(true, g_trace[7][g]);
           if (g >= NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           const int nkeys = min(KC, a.Nk - k0);
@@ -223,7 +238,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           for (int mm = 0; mm < MM; ++mm)
             umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
           umma::tma_load_3d(sm + SM_VST + st * VBYTES, &mv, &full_kv[st], HD * h, 0, k0);
-        if (TRACE && true && g < 128) g_trace[0][g] = clock64();
+        TC_TRACE(true, g_trace[0][g]);
           umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
         }
         g0 += nch;
@@ -245,7 +260,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
                           umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
         umma::mma_commit(&wv_free[b]);
-        if (TRACE && true && g < 128) g_trace[6][g] = clock64();
+        TC_TRACE(true, g_trace[6][g]);
       };
       auto issue_s = [&](int g, int h, bool last) {
         const int b = g & 1, st = g % NSTAGE;
@@ -262,7 +277,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
                              idesc_s, s > 0 ? 1u : 0u);
           }
         umma::mma_commit(&s_full[b]);
-        if (TRACE && true && g < 128) g_trace[1][g] = clock64();
+        TC_TRACE(true, g_trace[1][g]);
         umma::mma_commit(&empty_kv[st]);
         if (last) umma::mma_commit(&q_free[h & 1]);
       };
@@ -302,7 +317,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           ent = rp < a.K ? __ldg(rl + rp) : 0xffff0000u;
         }
         umma::mbar_wait(&s_full[b], (g >> 1) & 1);
-        if (TRACE && tid == 64 && g < 128) g_trace[2][g] = clock64();
+        TC_TRACE(tid == 64, g_trace[2][g]);
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);  // key positions landed (already complete)
         umma::tc_fence_after();
         uint32_t sr[16];
@@ -363,15 +378,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           rincl[row] = incl;
           if (lane == 31) qtot[warp & 3] = incl;
         }
-        if (TRACE && tid == 64 && g < 128) g_trace_r[0][g] = clock64();
+        TC_TRACE(tid == 64, g_trace_r[0][g] );
         if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // Wt buffer b free
-        if (TRACE && tid == 64 && g < 128) g_trace_r[1][g] = clock64();
+        TC_TRACE(tid == 64, g_trace_r[1][g] );
         uint8_t* wt = sm + SM_WT + b * WBYTES;
 #pragma unroll
         for (int f = 0; f < MM; ++f)
           *reinterpret_cast<uint4*>(wt + cm_off(row, f * KC + 8 * half)) = make_uint4(0, 0, 0, 0);
         umma::named_bar(2, 256);
-        if (TRACE && tid == 64 && g < 128) g_trace_r[2][g] = clock64();
+        TC_TRACE(tid == 64, g_trace_r[2][g] );
         // ---- phase 2 (balanced): the chunk's valid (row, key) pairs of the whole
         // tile are dealt round-robin to the 256 row threads (the pairs of a
         // molecule-sized chunk cluster in one quadrant; this spreads them)
@@ -413,8 +428,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         }
         umma::fence_proxy_async();
         umma::mbar_arrive(&wt_full[b]);
-        if (TRACE && tid == 64 && g < 128) g_trace[3][g] = clock64();
-        if (TRACE && lane == 0 && g < 128) g_trace_w[warp - 2][g] = clock64();
+        TC_TRACE(tid == 64, g_trace[3][g]);
+        TC_TRACE(lane == 0, g_trace_w[warp - 2][g] );
         umma::mbar_arrive(&empty_kv[st]);  // done with this stage's key positions
       }
       // ---- epilogue: O_h / z, the two halves each store half of the columns
@@ -479,7 +494,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       for (int c = 0; c < nch; ++c) {
         const int g = g0 + c, b = g & 1, st = g % NSTAGE;
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
-        if (TRACE && vt_id == 0 && g < 128) g_trace[4][g] = clock64();
+        TC_TRACE(vt_id == 0, g_trace[4][g]);
         // v_j[i'][c] of this thread's channel and two keys, read straight from the
         // TMA stage ([key][i'][16 c] bf16; lanes = consecutive channels)
         const unsigned short* vst = reinterpret_cast<const unsigned short*>(sm + SM_VST + st * VBYTES);
@@ -502,7 +517,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         });
         umma::fence_proxy_async();
         umma::mbar_arrive(&vg_full[b]);
-        if (TRACE && vt_id == 0 && g < 128) g_trace[5][g] = clock64();
+        TC_TRACE(vt_id == 0, g_trace[5][g]);
       }
       g0 += nch;
     }
@@ -510,6 +525,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tmem, 512);
+#ifdef ES_TC_TRACE
   if (TRACE && tid == 0) {
     for (int g = 0; g < 128 && g < 8 * nch; ++g)
       printf("TRACE g=%d tma=%lld sI=%lld sR=%lld wt=%lld vgS=%lld vgD=%lld vI=%lld pw=%lld\n", g, g_trace[0][g],
@@ -518,6 +534,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       printf("TRACEW g=%d %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld %lld\n", g, g_trace_r[0][g], g_trace_r[1][g], g_trace_r[2][g], g_trace_w[0][g], g_trace_w[1][g],
              g_trace_w[2][g], g_trace_w[3][g], g_trace_w[4][g], g_trace_w[5][g], g_trace_w[6][g], g_trace_w[7][g]);
   }
+#endif
 }
 
 // ---------------------------------------------------------------- tile chunk lists
