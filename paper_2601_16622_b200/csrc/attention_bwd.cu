@@ -311,7 +311,7 @@ template <int L, int CPL, bool EAAS, typename T>
 es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
                   const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                   const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, float* dsbuf,
-                  double* dpos, cudaStream_t st) {
+                  double* dpos, bool skip_dq, cudaStream_t st) {
   constexpr int M = Lay<L>::M;
   if (dpos && L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
   {
@@ -336,7 +336,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   fn<<<kp.Nk, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
                                   (const T*)dout, delta, (T*)dk, (T*)dv, dsbuf, dpos);
   s = cuda_status(cudaGetLastError(), "attn_bwd_kv_kernel");
-  if (s != ES_OK) return s;
+  if (s != ES_OK || skip_dq) return s;  // skip_dq: the tcgen05 dq kernel runs next
   {
     int tq = (M * kp.Dq / 8 + 31) / 32 * 32;
     if (tq > 1024) tq = 1024;
@@ -387,7 +387,7 @@ struct BwdOp {
 es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
                           const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
-                          float* dsbuf, double* dpos, cudaStream_t st) {
+                          float* dsbuf, double* dpos, void* ws_tc, size_t ws_tc_bytes, cudaStream_t st) {
   es_status s = upload_tables_tu();
   if (s != ES_OK) return s;
   const KParams kp = make_params(a);
@@ -395,8 +395,11 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
     if (dpos) return cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)a.Nk, st), "attn_bwd: dpos");
     return ES_OK;
   }
-  return dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf,
-                         dpos, st);
+  const bool tc_dq = attn_dq_tc_applicable(a);
+  s = dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
+                      tc_dq, st);
+  if (s != ES_OK || !tc_dq) return s;
+  return attn_dq_tc_launch(a, k, nbr, dsbuf, dq, ws_tc, ws_tc_bytes, st);
 }
 
 }  // namespace es

@@ -291,8 +291,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           if (c + 1 < nch) issue_s(g0 + c + 1, h, c + 2 == nch);
           value_mma(g0 + c, c, h);
         }
-        if (nch > 0) umma::mma_commit(acc_done);
-        else umma::mbar_arrive(acc_done);
+        if (nch > 0) {
+          umma::mma_commit(acc_done);
+        } else {  // empty tile: keep acc_done one phase ahead of the epilogue at most (parity waits)
+          if (h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);
+          umma::mbar_arrive(acc_done);
+        }
         g0 += nch;
       }
     }
@@ -576,17 +580,25 @@ __global__ void tc_fill_kernel(int ntiles, int words, const uint32_t* __restrict
 
 // Per query row: its valid neighbours folded into (tile chunk index << 16 | 16-bit key
 // mask) entries, ascending chunk index, terminated by 0xffff0000 (the row-level
-// tile-skip mask the attention kernel walks chunk by chunk).
+// tile-skip mask the attention kernels walk chunk by chunk); optionally the
+// row's neighbour slots in the same (ascending j) order, for the dq kernel's
+// dscore gathers.
 __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
-                                  const int* __restrict__ clist, uint32_t* __restrict__ rl) {
+                                  const int* __restrict__ clist, uint32_t* __restrict__ rl, int* __restrict__ slots) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int t = i / TQ, lo = cptr[t], n = cptr[t + 1] - lo;
   uint32_t* o = rl + (size_t)i * K;
-  int cnt = 0;
+  int cnt = 0, nv = 0;
   for (int s = 0; s < K; ++s) {
     const int j = nbr[(size_t)i * K + s];
     if (j < 0) continue;
+    if (slots) {  // the row's slots in ascending-j order (= the (chunk, key-bit) order of the list)
+      int* so = slots + (size_t)i * K;
+      int p = nv++;
+      while (p > 0 && nbr[(size_t)i * K + so[p - 1]] > j) { so[p] = so[p - 1]; --p; }
+      so[p] = s;
+    }
     const int kb = j / KC;
     int a = 0, b = n;
     while (a < b) {
@@ -702,16 +714,16 @@ TcScratch tc_scratch(const AttnArgs& a) {
 
 size_t attn_fwd_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(a).total : 0; }
 
-// Scratch (tile mask, chunk lists, per-row chunk lists) lives in the caller's
-// workspace (es_attn_fwd_workspace_size): no allocation on the launch path.
-es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
-                             const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes,
-                             cudaStream_t st) {
-  es_status s = upload_tc_tables();
-  if (s != ES_OK) return s;
-  if (a.N == 0) return ES_OK;
-  const TcScratch t = tc_scratch(a);
-  if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+namespace {
+struct TcLists {
+  const int* cptr;
+  const int* clist;
+  const uint32_t* rowlist;
+  int ntiles;
+};
+// tile-skip mask -> per-tile key-chunk lists -> per-row (chunk, key mask) lists
+es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const TcScratch& t, int* slots,
+                         TcLists* out, cudaStream_t st) {
   const int ntiles = t.ntiles, words = t.words;
   size_t cub_bytes = t.cub_bytes;
   char* base = static_cast<char*>(ws);
@@ -728,13 +740,35 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   uint32_t* rowlist = (uint32_t*)(base + off);
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
-  s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
+  es_status s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
   if (s != ES_OK) return s;
   tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
-  tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist);
+  tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist, slots);
+  *out = TcLists{cptr, clist, rowlist, ntiles};
+  return cuda_status(cudaGetLastError(), "attn_tc lists");
+}
+}  // namespace
+
+// Scratch (tile mask, chunk lists, per-row chunk lists) lives in the caller's
+// workspace (es_attn_fwd_workspace_size): no allocation on the launch path.
+es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                             const int32_t* nbr, void* out, float* lse, void* ws, size_t ws_bytes,
+                             cudaStream_t st) {
+  es_status s = upload_tc_tables();
+  if (s != ES_OK) return s;
+  if (a.N == 0) return ES_OK;
+  const TcScratch t = tc_scratch(a);
+  if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+  TcLists lists;
+  s = tc_build_lists(a, nbr, ws, t, nullptr, &lists, st);
+  if (s != ES_OK) return s;
+  const int ntiles = lists.ntiles;
+  const int* cptr = lists.cptr;
+  const int* clist = lists.clist;
+  const uint32_t* rowlist = lists.rowlist;
 
   CUtensorMap mk, mv;
   if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
@@ -757,6 +791,236 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
                                                         (bf16*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
+}
+
+
+// ---------------------------------------------------------------- dq on the tensor cores
+// dq_i^h = tau sum_j dS_ij^h k_j^h over the same 128-query tiles and 16-key
+// chunks as the forward: per chunk one tcgen05 MMA group
+//   D[128 queries, 288] += A[128, 16 keys] . B[16 keys, 288]
+// with A = the chunk's dscore tile (bf16, built by the row warps from the
+// backward's per-pair dscore buffer; zeros for non-neighbours) and B = the
+// TMA-staged K chunk read MN-major (the 64-byte-swizzled [16 keys][32 ch]
+// boxes of the forward's S MMA are exactly the MN-major SW64 atoms).
+namespace {
+constexpr int DQ_THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 rows + epilogue
+constexpr int DQ_ABYTES = TQ * KC * 2;  // 4096: [128 rows][16 keys] bf16, no-swizzle core matrices
+constexpr int DQ_SM_K = 0;
+constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA latency dominates
+constexpr int DQ_SM_A = DQ_NSTAGE * KBYTES;
+constexpr int DQ_SM_DS = DQ_SM_A + 2 * DQ_ABYTES;  // [128 rows][64] f32: the row's dscores of one head
+constexpr int DQ_KMAX = 64;
+constexpr int DQ_SM_BAR = DQ_SM_DS + TQ * DQ_KMAX * 4;
+constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
+
+__global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
+    const __grid_constant__ CUtensorMap mk, int N, int K, float tau, const int* __restrict__ cptr,
+    const int* __restrict__ clist, const uint32_t* __restrict__ rowlist, const int* __restrict__ slots,
+    const float* __restrict__ dsbuf, bf16* __restrict__ dq) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DQ_SM_BAR);
+  uint64_t* full_kv = bars + 0;    // [8] TMA landed
+  uint64_t* empty_kv = bars + 8;   // [8] MMA done with the K stage
+  uint64_t* a_full = bars + 16;    // [2] rows wrote the dscore tile (128)
+  uint64_t* a_free = bars + 18;    // [2] MMA done with the dscore tile
+  uint64_t* acc_done = bars + 20;
+  uint64_t* epi_done = bars + 21;  // rows read the accumulator (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 22);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
+  if (tid == 0) {
+    umma::prefetch_tmap(&mk);
+    for (int b = 0; b < DQ_NSTAGE; ++b) {
+      umma::mbar_init(&full_kv[b], 1);
+      umma::mbar_init(&empty_kv[b], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&a_full[b], 128);
+      umma::mbar_init(&a_free[b], 1);
+    }
+    umma::mbar_init(acc_done, 1);
+    umma::mbar_init(epi_done, 128);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 512);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (lane == 0) {
+      constexpr int PF = 4;  // L2 prefetch distance beyond the smem stages
+      int g = 0;
+      for (int h = 0; h < 8; ++h)
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int st = g % DQ_NSTAGE;
+          {
+            const int cp = c + DQ_NSTAGE + PF;
+            const int hp = h + cp / (nch > 0 ? nch : 1), ccp = cp % (nch > 0 ? nch : 1);
+            if (hp < 8)
+              for (int mm = 0; mm < MM; ++mm)
+                umma::tma_prefetch_3d(&mk, DH * hp, mm, clist[c_begin + ccp] * KC);
+          }
+          if (g >= DQ_NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / DQ_NSTAGE) - 1) & 1);
+          const int k0 = clist[c_begin + c] * KC;
+          uint8_t* kb = sm + DQ_SM_K + st * KBYTES;
+          umma::mbar_arrive_expect_tx(&full_kv[st], KBYTES);
+          for (int mm = 0; mm < MM; ++mm)
+            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
+        }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_a = umma::idesc_bf16(128, 256, 0, 1);
+      constexpr uint32_t idesc_b = umma::idesc_bf16(128, 32, 0, 1);
+      int g = 0;
+      for (int h = 0; h < 8; ++h) {
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int st = g % DQ_NSTAGE, b = g & 1;
+          umma::mbar_wait(&full_kv[st], (g / DQ_NSTAGE) & 1);
+          umma::mbar_wait(&a_full[b], (g >> 1) & 1);
+          if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);
+          umma::tc_fence_after();
+          const uint32_t ka = umma::smem_u32(sm + DQ_SM_K + st * KBYTES);
+          const uint64_t ad = umma::sdesc(umma::smem_u32(sm + DQ_SM_A + b * DQ_ABYTES), 128, 256, 0);
+          // B: MN-major, 64B swizzle: 32-channel atoms 1024 B apart (one per (l,m) row), 8 keys = 512 B
+          umma::mma_f16(tmem, ad, umma::sdesc(ka, 1024, 512, 4), idesc_a, c > 0 ? 1u : 0u);
+          umma::mma_f16(tmem + 256, ad, umma::sdesc(ka + 8 * 1024, 1024, 512, 4), idesc_b, c > 0 ? 1u : 0u);
+          umma::mma_commit(&empty_kv[st]);
+          umma::mma_commit(&a_free[b]);
+        }
+        if (nch > 0) {
+          umma::mma_commit(acc_done);
+        } else {  // empty tile: keep acc_done one phase ahead of the epilogue at most (parity waits)
+          if (h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);
+          umma::mbar_arrive(acc_done);
+        }
+      }
+    }
+  } else {
+    // ================= rows: dscore tiles, epilogue
+    const int row = ((warp & 3) << 5) | lane;
+    const int qi = blockIdx.x * TQ + row;
+    const bool qin = qi < N;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * K;
+    const int* sl = slots + (size_t)(qin ? qi : 0) * K;
+    float* dsr = reinterpret_cast<float*>(sm + DQ_SM_DS) + row * DQ_KMAX;  // this row's dscores (one head)
+    int nv = 0;  // valid pairs of the row (popcount over its chunk list)
+    if (qin)
+      for (int u = 0; u < K; ++u) {
+        const uint32_t e = __ldg(rl + u);
+        if ((e >> 16) == 0xffffu) break;
+        nv += __popc(e & 0xffffu);
+      }
+    int g = 0;
+    for (int h = 0; h < 8; ++h) {
+      // all of the row's dscores of head h in flight at once (one latency per
+      // head instead of one per chunk); nobody else reads dsr, and the previous
+      // head's reads finished in this thread's program order
+      for (int r0 = 0; r0 < nv; r0 += 8) {
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          x[u] = r0 + u < nv ? __ldg(dsbuf + ((size_t)qi * K + __ldg(sl + r0 + u)) * 8 + h) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (r0 + u < nv) dsr[r0 + u] = x[u];
+      }
+      int rp = 0, r = 0;
+      uint32_t ent = qin ? __ldg(rl) : 0xffff0000u;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int b = g & 1;
+        unsigned vmask = 0u;
+        if ((int)(ent >> 16) == c) {
+          vmask = ent & 0xffffu;
+          ++rp;
+          ent = rp < K ? __ldg(rl + rp) : 0xffff0000u;
+        }
+        float d[KC];
+#pragma unroll
+        for (int t = 0; t < KC; ++t) {
+          d[t] = 0.f;
+          if (vmask >> t & 1) d[t] = dsr[r++];
+        }
+        if (g >= 2) umma::mbar_wait(&a_free[b], ((g >> 1) - 1) & 1);
+        uint8_t* at = sm + DQ_SM_A + b * DQ_ABYTES + (row >> 3) * 256 + (row & 7) * 16;
+        *reinterpret_cast<uint4*>(at) = pack8(d);
+        *reinterpret_cast<uint4*>(at + 128) = pack8(d + 8);
+        umma::fence_proxy_async();
+        umma::mbar_arrive(&a_full[b]);
+      }
+      // epilogue: dq[qi][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..]
+      umma::mbar_wait(acc_done, h & 1);
+      umma::tc_fence_after();
+#pragma unroll
+      for (int mm = 0; mm < MM; ++mm) {
+        uint32_t r0[16], r1[16];
+        if (nch > 0) {
+          umma::tmem_ld16(tmem + lane_base + 32 * mm, r0);
+          umma::tmem_ld16(tmem + lane_base + 32 * mm + 16, r1);
+        }
+        float v[32];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          v[t] = nch > 0 ? tau * __uint_as_float(r0[t]) : 0.f;
+          v[16 + t] = nch > 0 ? tau * __uint_as_float(r1[t]) : 0.f;
+        }
+        if (qin) {
+          uint4* dst = reinterpret_cast<uint4*>(dq + ((size_t)qi * MM + mm) * 256 + DH * h);
+          dst[0] = pack8(v);
+          dst[1] = pack8(v + 8);
+          dst[2] = pack8(v + 16);
+          dst[3] = pack8(v + 24);
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(epi_done);
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, 512);
+}
+}  // namespace
+
+bool attn_dq_tc_applicable(const AttnArgs& a) {
+  static int use = -1;
+  if (use < 0) {
+    const char* e = getenv("ES_ATTN_TC");
+    use = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 2 : 1;
+  }
+  const bool enough_tiles = (a.N + TQ - 1) / TQ >= 74;
+  return use && (enough_tiles || use == 2) && a.K <= DQ_KMAX && attn_tc_supported(a);
+}
+
+size_t attn_dq_tc_workspace(const AttnArgs& a) {
+  if (a.N <= 0) return 0;
+  return tc_scratch(a).total + align256((size_t)a.N * a.K * 4);
+}
+
+es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
+                            void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (a.N == 0) return ES_OK;
+  const TcScratch t = tc_scratch(a);
+  if (!ws || ws_bytes < attn_dq_tc_workspace(a)) return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small");
+  int* slots = (int*)((char*)ws + t.total);
+  TcLists lists;
+  es_status s = tc_build_lists(a, nbr, ws, t, slots, &lists, st);
+  if (s != ES_OK) return s;
+  CUtensorMap mk;
+  if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B))
+    return fail(ES_CUDA_ERROR, "attn_dq_tc: tensor map encode failed");
+  const int smem = DQ_SM_TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  attn_dq_tc_kernel<<<lists.ntiles, DQ_THREADS, smem, st>>>(mk, a.N, a.K, a.tau, lists.cptr, lists.clist,
+                                                           lists.rowlist, slots, dsbuf, (bf16*)dq);
+  return cuda_status(cudaGetLastError(), "attn_dq_tc_kernel");
 }
 
 }  // namespace es

@@ -153,9 +153,14 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
   });
 }
 
-size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
-  if (!d || d->N <= 0) return 256;
+static size_t bwd_base_bytes(const es_attn_desc* d) {
   return align256(sizeof(float) * (size_t)d->N * d->H) + align256(sizeof(float) * (size_t)d->N * d->K * d->H);
+}
+
+size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
+  if (!d || d->N <= 0 || check_attn(d) != ES_OK) return 256;
+  const AttnArgs a = to_args(d);
+  return bwd_base_bytes(d) + (attn_dq_tc_applicable(a) ? attn_dq_tc_workspace(a) : 0);
 }
 
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
@@ -168,7 +173,7 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
     if (dpos && d->L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
     if (d->N == 0)
       return dpos ? attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv,
-                                    nullptr, nullptr, dpos, (cudaStream_t)stream)
+                                    nullptr, nullptr, dpos, nullptr, 0, (cudaStream_t)stream)
                   : ES_OK;
     if (!q || !k || !v || !pos || !nbr || !rev_ptr || !rev_pair || !out || !lse || !dout || !dq || !dk || !dv)
       return fail(ES_INVALID_ARGUMENT, "attn_bwd: null buffer");
@@ -176,8 +181,9 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
       return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small");
     float* delta = (float*)workspace;
     float* dsbuf = (float*)((char*)workspace + align256(sizeof(float) * (size_t)d->N * d->H));
+    const size_t base = bwd_base_bytes(d);
     return attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta,
-                           dsbuf, dpos, (cudaStream_t)stream);
+                           dsbuf, dpos, (char*)workspace + base, workspace_bytes - base, (cudaStream_t)stream);
   });
 }
 

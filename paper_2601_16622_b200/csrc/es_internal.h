@@ -57,7 +57,11 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
 es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
                           const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
-                          float* dsbuf, double* dpos, cudaStream_t st);
+                          float* dsbuf, double* dpos, void* ws_tc, size_t ws_tc_bytes, cudaStream_t st);
+bool attn_dq_tc_applicable(const AttnArgs& a);
+size_t attn_dq_tc_workspace(const AttnArgs& a);
+es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
+                            void* ws, size_t ws_bytes, cudaStream_t st);
 
 
 struct NbrArgs {

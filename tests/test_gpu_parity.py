@@ -280,17 +280,22 @@ def test_full_size_properties_config2(es):
     assert 10 < cnt.mean() < 20
 
 
-@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc", "sharp"])
+@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc", "sharp", "empty_tiles"])
 def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
-    """The tcgen05 path (bf16, L=2, C=128, H=8) over many 128-query tiles and
-    key chunks: molecule batch, one bulk system, a periodic box, and a batch
-    with 6x scaled queries (score ranges > 5 nats, so the lazy online-softmax
-    rescale of the TMEM accumulator fires)."""
+    """The tcgen05 paths (forward, dq; bf16, L=2, C=128, H=8) over many
+    128-query tiles and key chunks: molecule batch, one bulk system, a
+    periodic box, a batch with 6x scaled queries (score ranges > 5 nats, so
+    the lazy online-softmax rescale of the TMEM accumulator fires), and a
+    system whose middle 300 atoms are isolated (whole tiles without a pair)."""
     L, C, H = 2, 128, 8
     box = None
     if kind in ("batch", "sharp"):
         b = S.molecule_batch(12, 40, 60, 5)
         pos, seg = b.pos, b.seg_ptr
+    elif kind == "empty_tiles":
+        core = S.gen_fcc_system(200, 3.8, 9)
+        lone = np.stack([1000.0 + 10.0 * np.arange(300), np.zeros(300), np.zeros(300)], 1)
+        pos, seg = np.concatenate([core[:100], lone, core[100:]]), None
     elif kind == "bulk":
         pos, seg = S.gen_fcc_system(700, 3.8, 6), None
     else:
@@ -306,10 +311,14 @@ def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
     P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
     rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
-    out, lse, _ = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box)
+    dout = torch.tensor(np.random.default_rng(10).standard_normal(rout.shape)).bfloat16().double().numpy()
+    out, lse, (dq, dk, dv) = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box, dout=dout)
     assert rel(out.float().cpu(), rout) < BF16_TOL
     fin = np.isfinite(rlse)
     assert rel(lse.cpu().numpy()[fin], rlse[fin]) < 1e-3
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, dout)
+    for a_, b_ in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        assert rel(a_.float().cpu(), b_) < BF16_TOL
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
