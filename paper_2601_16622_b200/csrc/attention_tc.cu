@@ -808,9 +808,9 @@ constexpr int DQ_ABYTES = TQ * KC * 2;  // 4096: [128 rows][16 keys] bf16, no-sw
 constexpr int DQ_SM_K = 0;
 constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA latency dominates
 constexpr int DQ_SM_A = DQ_NSTAGE * KBYTES;
-constexpr int DQ_SM_DS = DQ_SM_A + 2 * DQ_ABYTES;  // [128 rows][64] f32: the row's dscores of one head
+constexpr int DQ_SM_DS = DQ_SM_A + 2 * DQ_ABYTES;  // [2 heads][128 rows][64] f32: the rows' dscores
 constexpr int DQ_KMAX = 64;
-constexpr int DQ_SM_BAR = DQ_SM_DS + TQ * DQ_KMAX * 4;
+constexpr int DQ_SM_BAR = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;
 constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 
 __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
@@ -906,7 +906,9 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * K;
     const int* sl = slots + (size_t)(qin ? qi : 0) * K;
-    float* dsr = reinterpret_cast<float*>(sm + DQ_SM_DS) + row * DQ_KMAX;  // this row's dscores (one head)
+    // this row's dscores, double buffered by head: head h+1's values are
+    // copied (cp.async, no registers) while head h's chunks run
+    float* dsr0 = reinterpret_cast<float*>(sm + DQ_SM_DS) + row * DQ_KMAX;
     int nv = 0;  // valid pairs of the row (popcount over its chunk list)
     if (qin)
       for (int u = 0; u < K; ++u) {
@@ -914,20 +916,24 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
         if ((e >> 16) == 0xffffu) break;
         nv += __popc(e & 0xffffu);
       }
+    auto fetch = [&](int hh) {
+      float* dst = dsr0 + (hh & 1) * TQ * DQ_KMAX;
+      for (int r0 = 0; r0 < nv; ++r0)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(umma::smem_u32(dst + r0)),
+                     "l"(dsbuf + ((size_t)qi * K + __ldg(sl + r0)) * 8 + hh)
+                     : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch(0);
     int g = 0;
     for (int h = 0; h < 8; ++h) {
-      // all of the row's dscores of head h in flight at once (one latency per
-      // head instead of one per chunk); nobody else reads dsr, and the previous
-      // head's reads finished in this thread's program order
-      for (int r0 = 0; r0 < nv; r0 += 8) {
-        float x[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          x[u] = r0 + u < nv ? __ldg(dsbuf + ((size_t)qi * K + __ldg(sl + r0 + u)) * 8 + h) : 0.f;
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (r0 + u < nv) dsr[r0 + u] = x[u];
+      if (h + 1 < 8) {
+        fetch(h + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // head h's group landed
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
+      const float* dsr = dsr0 + (h & 1) * TQ * DQ_KMAX;
       int rp = 0, r = 0;
       uint32_t ent = qin ? __ldg(rl) : 0xffff0000u;
       for (int c = 0; c < nch; ++c, ++g) {
