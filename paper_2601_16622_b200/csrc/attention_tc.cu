@@ -53,16 +53,16 @@ constexpr int GBYTES = NV * KV * 2;                    // [144 x 144] core-matri
 constexpr int SM_K = 0;                                // NSTAGE x KBYTES
 constexpr int SM_VST = SM_K + NSTAGE * KBYTES;         // NSTAGE x VBYTES
 constexpr int SM_POS = SM_VST + NSTAGE * VBYTES;       // NSTAGE x PBYTES (chunk key positions)
-constexpr int SM_WT = 48128;                           // 2 x WBYTES
+constexpr int SM_WT = (SM_POS + NSTAGE * PBYTES + 1023) / 1024 * 1024;  // 2 x WBYTES (1024-aligned)
 constexpr int SM_VG = SM_WT + 2 * WBYTES;              // 2 x GBYTES
 constexpr int SM_BAR = SM_VG + 2 * GBYTES;
 constexpr int SM_ZX = SM_BAR + 256;                    // [2][128] f32 softmax denominators of the key halves
 constexpr int SM_PROW = SM_ZX + 2 * TQ * 4;            // [2][128 rows][16 keys] f32 softmax numerators
-constexpr int SM_RMASK = SM_PROW + 2 * TQ * KC * 4;    // [2][128] u32 valid-key mask per row
-constexpr int SM_RINCL = SM_RMASK + 2 * TQ * 4;        // [2][128] i32 quadrant-local inclusive pair count
-constexpr int SM_QTOT = SM_RINCL + 2 * TQ * 4;         // [2][4] i32 pairs per quadrant
+constexpr int SM_PAIRS = SM_PROW + 2 * TQ * KC * 4;    // [2][4 quadrants][512] u16 (row << 4 | key) pair lists
+constexpr int SM_QTOT = SM_PAIRS + 2 * TQ * KC * 2;    // [2][4] i32 pairs per quadrant
 constexpr int SM_QPOS = SM_QTOT + 64;                  // [128 rows][3] f64 query positions
 constexpr int SM_TOTAL = SM_QPOS + TQ * 24;
+static_assert(SM_TOTAL + 1024 <= 232448, "forward kernel exceeds 227 KB of shared memory");
 static_assert(SM_POS + NSTAGE * PBYTES <= SM_WT, "smem map overlap");
 
 struct TcTab {
@@ -363,8 +363,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         // per-row valid masks + quadrant-local prefix counts (half 0)
         const int pb = g & 1;  // phase-2 tables double buffered by chunk parity
         float* prow = reinterpret_cast<float*>(sm + SM_PROW) + pb * TQ * KC;
-        uint32_t* rmask = reinterpret_cast<uint32_t*>(sm + SM_RMASK) + pb * TQ;
-        int* rincl = reinterpret_cast<int*>(sm + SM_RINCL) + pb * TQ;
         int* qtot = reinterpret_cast<int*>(sm + SM_QTOT) + pb * 4;
         float4* pdst = reinterpret_cast<float4*>(prow + row * KC + 8 * half);
         pdst[0] = make_float4(pw[0], pw[1], pw[2], pw[3]);
@@ -378,8 +376,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
           }
-          rmask[row] = gm;
-          rincl[row] = incl;
+          // this row's valid pairs, compacted into its quadrant's list
+          uint16_t* pairs = reinterpret_cast<uint16_t*>(sm + SM_PAIRS) + pb * TQ * KC + (warp & 3) * 32 * KC;
+          unsigned m = gm;
+          int o = incl - cnt;
+          while (m) {
+            const int kk = __ffs(m) - 1;
+            m &= m - 1;
+            pairs[o++] = (uint16_t)((row << 4) | kk);
+          }
           if (lane == 31) qtot[warp & 3] = incl;
         }
         TC_TRACE(tid == 64, g_trace_r[0][g] );
@@ -402,15 +407,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           for (int p = rt; p < total; p += 256) {
             const int qd = (p >= q0n) + (p >= q1n) + (p >= q2n);
             const int local = p - (qd == 0 ? 0 : qd == 1 ? q0n : qd == 2 ? q1n : q2n);
-            const int* ri = rincl + 32 * qd;
-            int lo = 0;  // first row of the quadrant with inclusive count > local
-#pragma unroll
-            for (int step = 16; step > 0; step >>= 1)
-              if (ri[lo + step - 1] <= local) lo += step;
-            const int orow = 32 * qd + lo;
-            unsigned om = rmask[orow];
-            for (int r = local - (ri[lo] - __popc(om)); r > 0; --r) om &= om - 1;
-            const int kk = __ffs(om) - 1;
+            const int e = reinterpret_cast<const uint16_t*>(sm + SM_PAIRS)[pb * TQ * KC + qd * 32 * KC + local];
+            const int orow = e >> 4, kk = e & 15;
             double dx = kpos[3 * kk] - qpos[3 * orow], dy = kpos[3 * kk + 1] - qpos[3 * orow + 1],
                    dz = kpos[3 * kk + 2] - qpos[3 * orow + 2];
             if (a.periodic) {
