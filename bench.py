@@ -281,7 +281,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     traffic_src = load_traffic()
     dom = max(("attn_fwd", "attn_bwd"), key=lambda n: t[n])
     dom_kernels = ["attn_fwd_tc_kernel"] if dom == "attn_fwd" else ["attn_delta_kernel", "attn_bwd_kv_kernel",
-                                                                    "attn_bwd_q_kernel"]
+                                                                    "attn_dq_tc_kernel"]
     traffic = None
     if traffic_src and all(k_ in traffic_src["bytes_per_launch"] for k_ in dom_kernels):
         traffic = sum(traffic_src["bytes_per_launch"][k_]["total"] for k_ in dom_kernels)
@@ -315,7 +315,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         },
         "roofline": {
             "kernel": "attn_fwd_tc_kernel (tcgen05)" if dom == "attn_fwd" else
-                      "attn_bwd (delta + bwd_kv + bwd_q, SIMT)",
+                      "attn_bwd (delta + bwd_kv SIMT + dq tcgen05)",
             "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
             "traffic_source": traffic_src["source"] if traffic is not None else None,
@@ -324,7 +324,8 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "achieved_tflops": round(dom_flops / (t[dom] * 1e-3) / 1e12, 3),
             "kernel_ms": {k_: round(v_, 4) for k_, v_ in t.items()},
             "note": "forward: tcgen05 kernel (S = Q K^T and O += Wt Vg on the tensor cores, per-pair geometry "
-                    "on CUDA cores); backward: fp32 SIMT (per-pair EAAS adjoint in registers)",
+                    "on CUDA cores); backward: key-centric fp32 SIMT kernel (per-pair EAAS adjoint; dk, dv, "
+                    "dscore) + tcgen05 dq = dS K",
         },
         "clocks": clocks,
         "e2e": {"value": round(total_flops / (e2e_ms * 1e-3) / 1e12, 4), "unit": "TFLOP/s",
