@@ -73,13 +73,7 @@ struct Lay {
   static constexpr int OFF_X = OFF_PHI + 2;  // spare (query slot in backward)
   static constexpr int OFF_DPHI = OFF_PHI + 3;  // dphi/dr (position gradients)
   static constexpr int OFF_R = OFF_PHI + 4;     // r_ij as fp32 (3)
-  // L <= 2: the per-pair EAAS steps (align D, sparse re-index P, un-align D^T)
-  // are composed once per pair into the M x M operator T = D^T P D, so each
-  // channel costs M^2 = 81 MACs instead of 107 (at L = 4 the three sparse
-  // EAAS steps are cheaper than M^2 = 625 and are applied directly).
-  static constexpr bool COMPOSE = false;  // measured: no gain on B200 (pair prep is the longer chain)
-  static constexpr int OFF_T = ((OFF_PHI + 7) + 3) / 4 * 4;
-  static constexpr int REC = COMPOSE ? OFF_T + (M * M + 3) / 4 * 4 : OFF_T;
+  static constexpr int REC = ((OFF_PHI + 7) + 3) / 4 * 4;
   static constexpr int BP = (L <= 2) ? 64 : 32;  // pairs per batch
 };
 
@@ -247,49 +241,6 @@ __device__ __forceinline__ void fit_all(const float (&R)[9], float* rec) {
   }
 }
 
-// D^l[row][col] of the pair record (D^0 = 1)
-template <int L, int l>
-__device__ __forceinline__ float dmat(const float* rec, int row, int col) {
-  if constexpr (l == 0) return 1.f;
-  else return rec[Lay<L>::doff(l) + row * (2 * l + 1) + col];
-}
-
-// T = D^T P D per (l_o, l_i) block:
-//   T[o, i] = sum_{m=-min..min} D^lo[lo+m][o] (a_e D^li[li+m][i] + b_e D^li[li-m][i])
-// (the forward EAAS map of eaas_apply, composed; Prop. 1).
-template <int L, int lo, int li>
-__device__ __forceinline__ void compose_block(float* rec) {
-  using LY = Lay<L>;
-  constexpr int mm = cmin(lo, li);
-#pragma unroll
-  for (int o = 0; o < 2 * lo + 1; ++o)
-#pragma unroll
-    for (int i = 0; i < 2 * li + 1; ++i) {
-      float t = 0.f;
-#pragma unroll
-      for (int m = -mm; m <= mm; ++m) {
-        const int e = LY::eoff(lo, li) + m + mm;
-        float src = rec[LY::OFF_AB + 2 * e] * dmat<L, li>(rec, li + m, i);
-        if (m != 0) src = fmaf(rec[LY::OFF_AB + 2 * e + 1], dmat<L, li>(rec, li - m, i), src);
-        t = fmaf(dmat<L, lo>(rec, lo + m, o), src, t);
-      }
-      rec[LY::OFF_T + (lo * lo + o) * LY::M + li * li + i] = t;
-    }
-}
-template <int L, int lo, int li>
-__device__ __forceinline__ void compose_rec(float* rec) {
-  if constexpr (lo <= L) {
-    if constexpr (li <= L) {
-      compose_block<L, lo, li>(rec);
-      compose_rec<L, lo, li + 1>(rec);
-    } else {
-      compose_rec<L, lo + 1, 0>(rec);
-    }
-  }
-}
-template <int L>
-__device__ __forceinline__ void compose_t(float* rec) { compose_rec<L, 0, 0>(rec); }
-
 // Real solid harmonics of degree <= 2 in the library convention (row
 // l*l+m+l; Y^1 = c1 (y, z, -x)) and their gradients -- the R^{l_f}(r) of the
 // per-pair value map x = phi sum_f Y^f(r) G_f v (same map as EAAS, Prop. 1),
@@ -382,7 +333,6 @@ __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, i
           rec[Lay<L>::OFF_AB + 2 * e + 1] = b;
         }
       }
-    if constexpr (Lay<L>::COMPOSE) compose_t<L>(rec);
   }
 }
 
@@ -457,45 +407,14 @@ __device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const 
   }
 }
 
-// acc += s * T v   (forward)  or  acc += s * T^T v  (adjoint), T read as
-// float4 from the pair record (broadcast: every lane of the warp reads the
-// same pair).
-template <int L, int CPL, bool ADJ>
-__device__ __forceinline__ void tapply(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
-                                       float (&acc)[Lay<L>::M][CPL]) {
-  constexpr int M = Lay<L>::M;
-  float sv[M][CPL];
-#pragma unroll
-  for (int t = 0; t < M; ++t)
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) sv[t][c] = s * v[t][c];
-  const float4* T4 = reinterpret_cast<const float4*>(rec + Lay<L>::OFF_T);
-#pragma unroll
-  for (int t4 = 0; t4 < (M * M + 3) / 4; ++t4) {
-    const float4 q = T4[t4];
-    const float tv[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = 4 * t4 + u;
-      if (t < M * M) {
-        const int o = t / M, ip = t % M;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          if constexpr (!ADJ) acc[o][c] = fmaf(tv[u], sv[ip][c], acc[o][c]);
-          else acc[ip][c] = fmaf(tv[u], sv[o][c], acc[ip][c]);
-        }
-      }
-    }
-  }
-}
-
-// The per-pair value operator of the EAAS kernels: composed T for L <= 2,
-// the three sparse EAAS steps otherwise.
+// The per-pair value operator of the SIMT kernels: the three sparse EAAS
+// steps.  (Composing them into the M x M operator T = D^T P D once per pair
+// costs 81 instead of 107 MACs per channel at L = 2 but was measured slower on
+// B200: the per-pair composition lengthens the batch-preparation chain.)
 template <int L, int CPL, bool ADJ>
 __device__ __forceinline__ void value_apply(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
                                             float (&acc)[Lay<L>::M][CPL]) {
-  if constexpr (Lay<L>::COMPOSE) tapply<L, CPL, ADJ>(rec, v, s, acc);
-  else eaas_apply<L, CPL, ADJ>(rec, v, s, acc);
+  eaas_apply<L, CPL, ADJ>(rec, v, s, acc);
 }
 
 }  // namespace
