@@ -32,23 +32,25 @@ class OracleBackend:
         dh, dW = po.project_bwd(h.numpy(), W.numpy(), L, dq.numpy(), dk.numpy(), dv.numpy())
         return torch.from_numpy(dh), torch.from_numpy(dW)
 
-    def _full(self, x_loc, row0):
-        full = np.zeros((self.N,) + tuple(x_loc.shape[1:]), dtype=np.float64)
+    def _full(self, x_loc, row0, n=None):
+        full = np.zeros((n or self.N,) + tuple(x_loc.shape[1:]), dtype=np.float64)
         full[row0:row0 + x_loc.shape[0]] = x_loc
         return full
 
     def attn_fwd(self, q_loc, k, v, pos, table_loc, row0):
-        nbr = -np.ones((self.N, table_loc.shape[1]), np.int32)
+        nk = k.shape[0]  # all atoms (all-gather) or own slab + halo (halo exchange)
+        nbr = -np.ones((nk, table_loc.shape[1]), np.int32)
         nbr[row0:row0 + len(table_loc)] = table_loc.numpy()
-        out, lse = po.attn_fwd(self.P, self._full(q_loc.numpy(), row0), k.numpy(), v.numpy(), pos.numpy(), nbr)
+        out, lse = po.attn_fwd(self.P, self._full(q_loc.numpy(), row0, nk), k.numpy(), v.numpy(), pos.numpy(), nbr)
         n = len(table_loc)
         self._ctx = (nbr, out, lse)
         return torch.from_numpy(out[row0:row0 + n]), torch.from_numpy(lse[row0:row0 + n]), None
 
     def attn_bwd(self, g_loc, q_loc, k, v, pos, idx, out, lse, row0):
         nbr, out_f, lse_f = self._ctx
-        dq, dk, dv = po.attn_bwd(self.P, self._full(q_loc.numpy(), row0), k.numpy(), v.numpy(), pos.numpy(), nbr,
-                                 out_f, lse_f, self._full(g_loc.numpy(), row0))
+        nk = k.shape[0]
+        dq, dk, dv = po.attn_bwd(self.P, self._full(q_loc.numpy(), row0, nk), k.numpy(), v.numpy(), pos.numpy(), nbr,
+                                 out_f, lse_f, self._full(g_loc.numpy(), row0, nk))
         n = q_loc.shape[0]
         return torch.from_numpy(dq[row0:row0 + n]), torch.from_numpy(dk), torch.from_numpy(dv)
 
@@ -69,13 +71,14 @@ def _system():
     return b, h, W, g
 
 
-def _row_worker(rank, world, port, outdir):
+def _row_worker(rank, world, port, outdir, halo=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     b, h, W, g = _system()
     N = len(b.pos)
     nbr, _, _ = po.build_neighbors(b.pos, K, 6.0, box=b.box)
-    layer = D.RowShardedAttention(N, OracleBackend(N, b.box), rank, world)
+    cls = D.HaloShardedAttention if halo else D.RowShardedAttention
+    layer = cls(N, OracleBackend(N, b.box), rank, world)
     a0, a1 = layer.a0, layer.a1
     out = layer.forward(torch.from_numpy(h[a0:a1].copy()), torch.from_numpy(W), torch.from_numpy(b.pos),
                         torch.from_numpy(nbr[a0:a1].copy()))
@@ -83,14 +86,15 @@ def _row_worker(rank, world, port, outdir):
     out_all = D.all_gather_rows(out, layer.plan)
     dh_all = D.all_gather_rows(dh, layer.plan)
     if rank == 0:
-        np.savez(os.path.join(outdir, "row.npz"), out=out_all.numpy(), dh=dh_all.numpy(), dW=dW.numpy())
+        extra = {"n_keys": layer.halo.n_keys} if halo else {}
+        np.savez(os.path.join(outdir, "row.npz"), out=out_all.numpy(), dh=dh_all.numpy(), dW=dW.numpy(), **extra)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_row_sharding_gloo_matches_unsharded(tmp_path, oracle):
-    world = 2
-    mp.spawn(_row_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+@pytest.mark.parametrize("world,halo", [(2, False), (2, True), (3, True)])
+def test_row_sharding_gloo_matches_unsharded(tmp_path, oracle, world, halo):
+    mp.spawn(_row_worker, args=(world, _free_port(), str(tmp_path), halo), nprocs=world, join=True)
     got = np.load(tmp_path / "row.npz")
     b, h, W, g = _system()
     nbr, _, _ = po.build_neighbors(b.pos, K, 6.0, box=b.box)
@@ -150,3 +154,38 @@ def test_shard_molecules_balance():
         assert local[0] == 0 and local[-1] == a1 - a0
         sizes.append(a1 - a0)
     assert sum(sizes) == seg[-1] and max(sizes) - min(sizes) <= 120
+
+
+def _halo_size_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos = S.gen_fcc_system(4000, 3.8, 7)
+    pos = pos[np.argsort(pos[:, 0], kind="stable")]  # slabs along x: spatially contiguous row shards
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0)
+    plan = D.RowPlan(len(pos), world)
+    a0, a1 = plan.rows(rank)
+    hp = D.HaloPlan(torch.from_numpy(nbr[a0:a1].copy()), plan, rank, world)
+    x = torch.arange(a1 - a0, dtype=torch.float64).view(-1, 1) + a0  # row value = its global id
+    keys_val = hp.gather(x)
+    ok = bool(torch.equal(keys_val.view(-1).long(), hp.keys.long()))
+    summed = hp.scatter_add(torch.ones(hp.n_keys, 1, dtype=torch.float64))
+    np.savez(os.path.join(outdir, f"halo{rank}.npz"), n_keys=hp.n_keys, n_loc=a1 - a0, ok=ok,
+             summed=summed.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_halo_plan_exchanges_only_the_halo(tmp_path):
+    """4 slabs of a 4000-atom system: each rank receives a halo far smaller
+    than the system, gather returns every key's row, and scatter_add counts
+    each row once for its owner plus once per rank that holds it as halo."""
+    world = 4
+    mp.spawn(_halo_size_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    total_halo_copies = 0
+    for r in range(world):
+        d = np.load(tmp_path / f"halo{r}.npz")
+        assert bool(d["ok"])
+        assert int(d["n_keys"]) < 0.75 * 4000
+        total_halo_copies += int(d["n_keys"]) - int(d["n_loc"])
+    summed = np.concatenate([np.load(tmp_path / f"halo{r}.npz")["summed"] for r in range(world)])
+    assert summed.min() >= 1 and summed.sum() == 4000 + total_halo_copies
