@@ -206,12 +206,14 @@ class HaloPlan:
         halo = ids[(ids < a0) | (ids >= a1)]
         owner = torch.div(halo, plan.per, rounding_mode="floor")
         self.halo = halo  # ascending = grouped by owner
-        req = torch.bincount(owner.cpu(), minlength=world)[:world].to(torch.int64)
+        # collectives run on the table's device (NCCL) or the CPU (gloo test harness)
+        cdev = table_loc.device if _is_nccl() else torch.device("cpu")
+        req = torch.bincount(owner.to(cdev), minlength=world)[:world].to(torch.int64)
         counts = [torch.zeros_like(req) for _ in range(world)]
         dist.all_gather(counts, req, group=group)  # counts[src][dst]: rows src needs from dst
         self.recv_counts = [int(counts[rank][r]) for r in range(world)]  # halo rows I receive, per owner
         self.send_counts = [int(counts[r][rank]) for r in range(world)]  # my rows each requester needs
-        asked = _all_to_all_rows(halo.cpu().view(-1, 1), self.recv_counts, self.send_counts, group)
+        asked = _all_to_all_rows(halo.to(cdev).view(-1, 1), self.recv_counts, self.send_counts, group)
         self.send_rows = (asked.view(-1).to(table_loc.device) - a0).long()  # local rows to send, by requester
         gmap = torch.full((plan.N,), -1, dtype=torch.int64, device=table_loc.device)
         gmap[a0:a1] = torch.arange(self.n_loc, device=table_loc.device)
