@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
   uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
   uint8_t* Bs = smem + 32768;         // [2 stages][2 kb][2 nb][64 k-rows][64] bf16, 32 KB per stage
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 32768 + 65536);
+  uint8_t* Stg = smem + 32768 + 65536;  // [4 warps][32 rows][80 B] epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 32768 + 65536 + 4 * 32 * 80);
   uint64_t* a_full = bars + 0;
   uint64_t* b_full = bars + 1;        // [2]
   uint64_t* b_empty = bars + 3;       // [2] MMA done reading the stage
@@ -160,20 +161,42 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
     }
     }
   } else {
-  const int n = n0 + warp * 32 + lane;
   for (int c = 0; c < NCH; ++c) {
     const int b = c & 1, o0 = c * 128;
     umma::mbar_wait(&acc_full[b], (c >> 1) & 1);
     umma::tc_fence_after();
-    bf16* dst;
-    if (o0 < 2 * p.C) dst = q + ((size_t)n * p.M + mm) * (2 * p.C) + o0;
-    else if (o0 < 4 * p.C) dst = k + ((size_t)n * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
-    else dst = v + ((size_t)n * p.M + mm) * p.C + (o0 - 4 * p.C);
+    // rows -> per-warp staging (32 rows x 32 columns, 80-byte padded rows: no
+    // bank conflicts) -> coalesced stores: 4 lanes write one row's 64 bytes,
+    // so every store instruction fills whole 32-byte sectors of 8 rows
+    // (the direct row stores wrote half sectors of 32 rows)
+    uint8_t* stg = Stg + warp * (32 * 80);
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
       uint32_t r[32];
       umma::tmem_ld32(taddr + 128 * b + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
-      if (n < p.N) store_row32(dst + cc * 32, r);
+      uint4 pk[4];
+      uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]));
+        w[t] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) *reinterpret_cast<uint4*>(stg + lane * 80 + t * 16) = pk[t];
+      __syncwarp();
+#pragma unroll
+      for (int it = 0; it < 4; ++it) {
+        const int rr = it * 8 + (lane >> 2), part = lane & 3;
+        const int nn = n0 + warp * 32 + rr;
+        if (nn < p.N) {
+          bf16* drow;
+          if (o0 < 2 * p.C) drow = q + ((size_t)nn * p.M + mm) * (2 * p.C) + o0;
+          else if (o0 < 4 * p.C) drow = k + ((size_t)nn * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
+          else drow = v + ((size_t)nn * p.M + mm) * p.C + (o0 - 4 * p.C);
+          *reinterpret_cast<uint4*>(drow + cc * 32 + part * 8) = *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
+        }
+      }
+      __syncwarp();
     }
     umma::tc_fence_before();
     umma::mbar_arrive(&acc_free[b]);
@@ -363,7 +386,7 @@ es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, vo
   CUtensorMap mh, mw;
   if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64))
     return fail(ES_CUDA_ERROR, "proj_fwd_tc: tensor map encode failed");
-  const size_t smem = 32768 + 65536 + 1024 + 1024;
+  const size_t smem = 32768 + 65536 + 4 * 32 * 80 + 1024 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(proj_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
