@@ -808,7 +808,8 @@ constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA la
 constexpr int DQ_SM_A = DQ_NSTAGE * KBYTES;
 constexpr int DQ_SM_DS = DQ_SM_A + 2 * DQ_ABYTES;  // [2 heads][128 rows][64] f32: the rows' dscores
 constexpr int DQ_KMAX = 64;
-constexpr int DQ_SM_BAR = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;
+constexpr int DQ_SM_STG = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;  // [4 warps][32 rows][80 B] epilogue staging
+constexpr int DQ_SM_BAR = DQ_SM_STG + 4 * 32 * 80;
 constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 
 __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
@@ -958,7 +959,9 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
       // epilogue: dq[qi][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..]
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
-#pragma unroll
+      // staged, coalesced stores: 4 lanes write one row's 64 bytes
+      uint8_t* stg = sm + DQ_SM_STG + (warp - 2) * (32 * 80);
+#pragma unroll 1
       for (int mm = 0; mm < MM; ++mm) {
         uint32_t r0[16], r1[16];
         if (nch > 0) {
@@ -971,13 +974,21 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
           v[t] = nch > 0 ? tau * __uint_as_float(r0[t]) : 0.f;
           v[16 + t] = nch > 0 ? tau * __uint_as_float(r1[t]) : 0.f;
         }
-        if (qin) {
-          uint4* dst = reinterpret_cast<uint4*>(dq + ((size_t)qi * MM + mm) * 256 + DH * h);
-          dst[0] = pack8(v);
-          dst[1] = pack8(v + 8);
-          dst[2] = pack8(v + 16);
-          dst[3] = pack8(v + 24);
+        uint4* sw = reinterpret_cast<uint4*>(stg + lane * 80);
+        sw[0] = pack8(v);
+        sw[1] = pack8(v + 8);
+        sw[2] = pack8(v + 16);
+        sw[3] = pack8(v + 24);
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2), part = lane & 3;
+          const int qq = blockIdx.x * TQ + (warp & 3) * 32 + rr;
+          if (qq < N)
+            *reinterpret_cast<uint4*>(dq + ((size_t)qq * MM + mm) * 256 + DH * h + part * 8) =
+                *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
         }
+        __syncwarp();
       }
       umma::tc_fence_before();
       umma::mbar_arrive(epi_done);

@@ -266,13 +266,32 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
   }
   umma::mbar_wait(done, 0);
   umma::tc_fence_after();
-  const int n = n0 + warp * 32 + lane;
-  bf16* dst = dh + ((size_t)n * p.M + mm) * p.C;
+  // staged, coalesced epilogue (see proj_fwd_tc_kernel); staging reuses
+  // pipeline stage 0, free once `done` fired
+  uint8_t* stg = smem + warp * (32 * 80);
 #pragma unroll
   for (int cc = 0; cc < 4; ++cc) {
     uint32_t r[32];
     umma::tmem_ld32(taddr + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
-    if (n < p.N) store_row32(dst + cc * 32, r);
+    uint4 pk[4];
+    uint32_t* w = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]));
+      w[t] = *reinterpret_cast<const uint32_t*>(&h2);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) *reinterpret_cast<uint4*>(stg + lane * 80 + t * 16) = pk[t];
+    __syncwarp();
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int rr = it * 8 + (lane >> 2), part = lane & 3;
+      const int nn = n0 + warp * 32 + rr;
+      if (nn < p.N)
+        *reinterpret_cast<uint4*>(dh + ((size_t)nn * p.M + mm) * p.C + cc * 32 + part * 8) =
+            *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
+    }
+    __syncwarp();
   }
   umma::tc_fence_before();
   __syncthreads();
