@@ -323,7 +323,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   if (s != ES_OK) return s;
   const int threads = kp.C / CPL;
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)M * threads * 3 * CPL * 4;
-  auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
+  auto fn = (kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
                                                                : attn_bwd_kv_kernel<L, CPL, EAAS, T>;
   if constexpr (L == 2) {
     if (dpos) {

@@ -154,7 +154,7 @@ es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v
                   const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
   const int tpq = kp.C / CPL;
   const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)Lay<L>::BP * kp.H * 4;
-  auto fn = (L == 2 && CPL == 2 && kp.C == 128 && kp.H == 8) ? attn_fwd_kernel<L, CPL, EAAS, T, 128, 8>
+  auto fn = (kp.C == 128 && kp.H == 8) ? attn_fwd_kernel<L, CPL, EAAS, T, 128, 8>
                                                                : attn_fwd_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.N, tpq, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
