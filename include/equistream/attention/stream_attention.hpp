@@ -38,6 +38,7 @@ struct NeighborIndex {
   int32_t* count = nullptr;    // [N]
   int32_t* rev_ptr = nullptr;  // [N+1]   (transposed relation, for the backward)
   int32_t* rev_pair = nullptr; // [N*K]
+  const void* tiles = nullptr; // tile lists of the tensor-core kernels (build_tiles), optional
 };
 
 struct AttentionProblem {
@@ -94,6 +95,18 @@ inline void project_qk(const void* h, const void* W, int32_t N, int32_t lmax, in
   check(es_project_fwd(&d, h, W, q, k, v, stream), "project_qk");
 }
 
+// tile structures of a neighbour index, built once and reused by every call on it
+inline std::size_t tiles_workspace_size(const AttentionProblem& p) {
+  const es_attn_desc d = p.desc();
+  return es_attn_tiles_workspace_size(&d);
+}
+inline void build_tiles(const AttentionProblem& p, NeighborIndex& idx, void* buf, std::size_t bytes,
+                        void* stream = nullptr) {
+  const es_attn_desc d = p.desc();
+  check(es_attn_tiles_build(&d, idx.table, buf, bytes, stream), "build_tiles");
+  idx.tiles = bytes ? buf : nullptr;
+}
+
 // stream_aggregate: m [N][M][C], lse [N][H]
 inline std::size_t forward_workspace_size(const AttentionProblem& p) {
   const es_attn_desc d = p.desc();
@@ -103,7 +116,7 @@ inline void stream_aggregate(const AttentionProblem& p, const void* q, const voi
                              const double* pos, const NeighborIndex& idx, void* m, float* lse, void* workspace,
                              std::size_t ws_bytes, void* stream = nullptr) {
   const es_attn_desc d = p.desc();
-  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, workspace, ws_bytes, stream), "stream_aggregate");
+  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, idx.tiles, workspace, ws_bytes, stream), "stream_aggregate");
 }
 
 // stream_aggregate_backward
@@ -117,7 +130,7 @@ inline void stream_aggregate_backward(const AttentionProblem& p, const void* gra
                                       std::size_t ws_bytes, void* stream = nullptr, double* grad_pos = nullptr) {
   const es_attn_desc d = p.desc();
   check(es_attn_bwd(&d, q, k, v, pos, idx.table, idx.rev_ptr, idx.rev_pair, m, lse, grad_m, grad_q, grad_k, grad_v,
-                    grad_pos, workspace, ws_bytes, stream),
+                    grad_pos, idx.tiles, workspace, ws_bytes, stream),
         "stream_aggregate_backward");
 }
 

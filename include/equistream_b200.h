@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 4
+#define ES_ABI_VERSION 5
 
 typedef enum {
   ES_OK = 0,
@@ -93,14 +93,23 @@ typedef struct {
 /* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in
  * {4, 8, 16, 32}.  bf16 + EAAS + L=2 + C=128 + H=8 + K<=64 runs on the
  * tcgen05 tensor-core kernel, everything else on the SIMT kernels. */
-/* Workspace: es_attn_fwd_workspace_size(d) bytes (tile-skip mask, per-tile
- * key-chunk lists and per-row chunk masks of the tensor-core kernel,
- * O(N*K) words; 256 bytes for the SIMT kernels).  Caller-owned, reusable
+/* Tile structures of one neighbour index (north-star subsystem 3): the
+ * tile-skip mask, per-tile key-chunk lists, per-row (chunk, key mask) lists
+ * and per-row slot order the tensor-core kernels walk.  Build once per
+ * neighbour index with es_attn_tiles_build into a caller buffer of
+ * es_attn_tiles_workspace_size(d) bytes (0: the kernels for d need none) and
+ * pass it to every es_attn_fwd / es_attn_bwd (every layer) using that index;
+ * tiles = NULL makes each call build them in its workspace instead. */
+size_t es_attn_tiles_workspace_size(const es_attn_desc* d);
+es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, void* tiles, size_t bytes, void* stream);
+
+/* Workspace: es_attn_fwd_workspace_size(d) bytes (the tile structures when
+ * tiles == NULL; 256 bytes for the SIMT kernels).  Caller-owned, reusable
  * across calls on the same stream; the library allocates nothing. */
 size_t es_attn_fwd_workspace_size(const es_attn_desc* d);
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, void* workspace, size_t workspace_bytes,
-                      void* stream);
+                      const int32_t* nbr, void* out, float* lse, const void* tiles, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* Workspace: es_attn_bwd_workspace_size(d) bytes (per-pair-head dscore
  * buffer, O(N*K*H) scalars -- never O(N*K*C)). rev_ptr/rev_pair
@@ -113,7 +122,7 @@ size_t es_attn_bwd_workspace_size(const es_attn_desc* d);
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                       const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
-                      void* workspace, size_t workspace_bytes, void* stream);
+                      const void* tiles, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Neighbour index: per atom the K nearest j != i with d^2 < r_cut^2, sorted
  * by (d^2, j), padded with -1, restricted to the atom's segment

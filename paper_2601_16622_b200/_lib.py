@@ -48,7 +48,7 @@ class EsUnsupported(EsError):
 _lib = None
 
 EXPORTS = [
-    "es_attn_fwd", "es_attn_fwd_workspace_size", "es_attn_bwd", "es_attn_bwd_workspace_size", "es_neighbors_build",
+    "es_attn_fwd", "es_attn_fwd_workspace_size", "es_attn_tiles_workspace_size", "es_attn_tiles_build", "es_attn_bwd", "es_attn_bwd_workspace_size", "es_neighbors_build",
     "es_neighbors_workspace_size", "es_neighbors_transpose", "es_neighbors_transpose_workspace_size",
     "es_tile_mask", "es_project_fwd", "es_project_bwd", "es_conventions_manifest", "es_cg_real",
     "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
@@ -63,10 +63,13 @@ def lib() -> ct.CDLL:
                           "(python -m paper_2601_16622_b200.build); there is no CPU fallback")
         L = ct.CDLL(LIB_PATH)
         vp, i32, sz, dp = ct.c_void_p, ct.c_int32, ct.c_size_t, ct.POINTER(ct.c_double)
-        L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 8 + [sz, vp]
+        L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 9 + [sz, vp]
+        L.es_attn_tiles_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
+        L.es_attn_tiles_workspace_size.restype = sz
+        L.es_attn_tiles_build.argtypes = [ct.POINTER(AttnDesc), vp, vp, sz, vp]
         L.es_attn_fwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_fwd_workspace_size.restype = sz
-        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 15 + [sz, vp]
+        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 16 + [sz, vp]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]
@@ -84,7 +87,7 @@ def lib() -> ct.CDLL:
         L.es_cg_real.argtypes = [i32] * 6
         L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
         L.es_wigner_d_host.argtypes = [i32, dp, dp]
-        if L.es_abi_version() != 4:
+        if L.es_abi_version() != 5:
             raise EsError("libequistream_b200.so ABI mismatch: rebuild (python -m paper_2601_16622_b200.build)")
         _lib = L
     return _lib

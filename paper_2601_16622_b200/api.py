@@ -72,6 +72,23 @@ class NeighborIndex:
     def K(self) -> int:
         return self.table.shape[1]
 
+    def tiles(self, d: "_lib.AttnDesc") -> torch.Tensor | None:
+        """The tile structures (tile-skip mask, chunk lists, per-row chunk
+        masks and slot order) the tensor-core kernels walk for this index --
+        built once (es_attn_tiles_build) and reused by every forward /
+        backward / layer on it; None when the kernels for `d` need none."""
+        nbytes = lib().es_attn_tiles_workspace_size(ct.byref(d))
+        if nbytes == 0:
+            return None
+        key = (d.N, d.K, d.Nk, d.row0, nbytes)
+        cache = self.__dict__.setdefault("_tiles", {})
+        if key not in cache:
+            buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.table.device)
+            check(lib().es_attn_tiles_build(ct.byref(d), _ptr(self.table), _ptr(buf), buf.numel(), _stream()),
+                  "es_attn_tiles_build")
+            cache[key] = buf
+        return cache[key]
+
     def transpose(self, n_keys: int | None = None):
         nk = self.N if n_keys is None else int(n_keys)
         if self._rev is None or self._rev[0].numel() != nk + 1:
@@ -249,9 +266,10 @@ def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row
     out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
     d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
-    ws = _workspace(lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)
+    tiles = idx.tiles(d)
+    ws = _workspace(256 if tiles is not None else lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)
     check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
-                            _ptr(lse), _ptr(ws), ws.numel(), _stream()), "es_attn_fwd")
+                            _ptr(lse), _ptr(tiles), _ptr(ws), ws.numel(), _stream()), "es_attn_fwd")
     return out, lse
 
 
@@ -271,7 +289,9 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_g
     dk = torch.empty_like(s.k)
     dv = torch.empty_like(s.v)
     dpos = torch.empty((Nk, 3), dtype=torch.float64, device=s.q.device) if pos_grad else None
+    tiles = s.idx.tiles(d)
     check(lib().es_attn_bwd(ct.byref(d), _ptr(s.q), _ptr(s.k), _ptr(s.v), _ptr(s.pos), _ptr(s.idx.table),
                             _ptr(rev_ptr), _ptr(rev_pair), _ptr(s.out), _ptr(s.lse), _ptr(grad_m), _ptr(dq),
-                            _ptr(dk), _ptr(dv), _ptr(dpos), _ptr(ws), ws.numel(), _stream()), "es_attn_bwd")
+                            _ptr(dk), _ptr(dv), _ptr(dpos), _ptr(tiles), _ptr(ws), ws.numel(), _stream()),
+          "es_attn_bwd")
     return (dq, dk, dv, dpos) if pos_grad else (dq, dk, dv)

@@ -719,23 +719,45 @@ struct TcLists {
   const uint32_t* rowlist;
   int ntiles;
 };
+// the list arrays inside a tile / workspace buffer laid out by tc_scratch
+struct TcPtrs {
+  uint32_t* mask;
+  int *cnt, *cptr, *clist;
+  void* cub;
+  uint32_t* rowlist;
+  int* slots;  // only when the buffer holds them (tile buffers do)
+};
+TcPtrs tc_ptrs(void* base_, const TcScratch& t) {
+  char* base = static_cast<char*>(base_);
+  TcPtrs p;
+  const int ntiles = t.ntiles, words = t.words;
+  p.mask = (uint32_t*)base;
+  size_t off = align256((size_t)ntiles * words * 4);
+  p.cnt = (int*)(base + off);
+  off += align256((size_t)(ntiles + 1) * 4);
+  p.cptr = (int*)(base + off);
+  off += align256((size_t)(ntiles + 1) * 4);
+  p.clist = (int*)(base + off);
+  off += align256(t.chunks * 4);
+  p.cub = base + off;
+  off += align256(t.cub_bytes);
+  p.rowlist = (uint32_t*)(base + off);
+  p.slots = (int*)(base + t.total);
+  return p;
+}
+
 // tile-skip mask -> per-tile key-chunk lists -> per-row (chunk, key mask) lists
 es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const TcScratch& t, int* slots,
                          TcLists* out, cudaStream_t st) {
   const int ntiles = t.ntiles, words = t.words;
   size_t cub_bytes = t.cub_bytes;
-  char* base = static_cast<char*>(ws);
-  uint32_t* mask = (uint32_t*)base;
-  size_t off = align256((size_t)ntiles * words * 4);
-  int* cnt = (int*)(base + off);
-  off += align256((size_t)(ntiles + 1) * 4);
-  int* cptr = (int*)(base + off);
-  off += align256((size_t)(ntiles + 1) * 4);
-  int* clist = (int*)(base + off);
-  off += align256(t.chunks * 4);
-  void* cub_ws = base + off;
-  off += align256(cub_bytes);
-  uint32_t* rowlist = (uint32_t*)(base + off);
+  const TcPtrs pp = tc_ptrs(ws, t);
+  uint32_t* mask = pp.mask;
+  int* cnt = pp.cnt;
+  int* cptr = pp.cptr;
+  int* clist = pp.clist;
+  void* cub_ws = pp.cub;
+  uint32_t* rowlist = pp.rowlist;
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
   es_status s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
@@ -759,10 +781,15 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   if (s != ES_OK) return s;
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
-  if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
   TcLists lists;
-  s = tc_build_lists(a, nbr, ws, t, nullptr, &lists, st);
-  if (s != ES_OK) return s;
+  if (a.tiles) {  // lists prebuilt for this neighbour index (es_attn_tiles_build)
+    const TcPtrs pp = tc_ptrs(const_cast<void*>(a.tiles), t);
+    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles};
+  } else {
+    if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+    s = tc_build_lists(a, nbr, ws, t, nullptr, &lists, st);
+    if (s != ES_OK) return s;
+  }
   const int ntiles = lists.ntiles;
   const int* cptr = lists.cptr;
   const int* clist = lists.clist;
@@ -1019,11 +1046,18 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
                             void* ws, size_t ws_bytes, cudaStream_t st) {
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
-  if (!ws || ws_bytes < attn_dq_tc_workspace(a)) return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small");
-  int* slots = (int*)((char*)ws + t.total);
   TcLists lists;
-  es_status s = tc_build_lists(a, nbr, ws, t, slots, &lists, st);
-  if (s != ES_OK) return s;
+  int* slots;
+  if (a.tiles) {  // lists + slot order prebuilt for this neighbour index
+    const TcPtrs pp = tc_ptrs(const_cast<void*>(a.tiles), t);
+    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles};
+    slots = pp.slots;
+  } else {
+    if (!ws || ws_bytes < attn_dq_tc_workspace(a)) return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small");
+    slots = (int*)((char*)ws + t.total);
+    es_status s = tc_build_lists(a, nbr, ws, t, slots, &lists, st);
+    if (s != ES_OK) return s;
+  }
   CUtensorMap mk;
   if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(ES_CUDA_ERROR, "attn_dq_tc: tensor map encode failed");
@@ -1036,6 +1070,23 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
   attn_dq_tc_kernel<<<lists.ntiles, DQ_THREADS, smem, st>>>(mk, a.N, a.K, a.tau, lists.cptr, lists.clist,
                                                            lists.rowlist, slots, dsbuf, (bf16*)dq);
   return cuda_status(cudaGetLastError(), "attn_dq_tc_kernel");
+}
+
+bool attn_tc_tiles_used(const AttnArgs& a) { return attn_dq_tc_applicable(a) || attn_fwd_workspace(a) > 0; }
+
+size_t attn_tc_tiles_bytes(const AttnArgs& a) {
+  if (a.N <= 0) return 0;
+  return tc_scratch(a).total + align256((size_t)a.N * a.K * 4);
+}
+
+// The tile structures of one neighbour index, built once and reused by every
+// forward / backward (and every layer) that uses the same index.
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, void* tiles, size_t bytes, cudaStream_t st) {
+  if (a.N == 0) return ES_OK;
+  const TcScratch t = tc_scratch(a);
+  if (!tiles || bytes < attn_tc_tiles_bytes(a)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: buffer too small");
+  TcLists lists;
+  return tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st);
 }
 
 }  // namespace es

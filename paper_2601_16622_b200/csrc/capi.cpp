@@ -138,18 +138,36 @@ size_t es_attn_fwd_workspace_size(const es_attn_desc* d) {
   return n > 256 ? n : 256;
 }
 
+size_t es_attn_tiles_workspace_size(const es_attn_desc* d) {
+  if (!d || check_attn(d) != ES_OK) return 0;
+  const AttnArgs a = to_args(d);
+  return attn_tc_tiles_used(a) ? attn_tc_tiles_bytes(a) : 0;
+}
+
+es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, void* tiles, size_t bytes, void* stream) {
+  return guarded([&] {
+    es_status s = check_attn(d);
+    if (s != ES_OK) return s;
+    const AttnArgs a = to_args(d);
+    if (!attn_tc_tiles_used(a)) return ES_OK;  // the SIMT kernels need no tile lists
+    if (d->N > 0 && !nbr) return fail(ES_INVALID_ARGUMENT, "attn_tiles: null buffer");
+    return attn_tc_tiles_build(a, nbr, tiles, bytes, (cudaStream_t)stream);
+  });
+}
+
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, void* workspace, size_t workspace_bytes,
-                      void* stream) {
+                      const int32_t* nbr, void* out, float* lse, const void* tiles, void* workspace,
+                      size_t workspace_bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
     if (d->N > 0 && (!q || !k || !v || !pos || !nbr || !out || !lse))
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: null buffer");
-    if (d->N > 0 && (!workspace || workspace_bytes < es_attn_fwd_workspace_size(d)))
+    if (d->N > 0 && !tiles && (!workspace || workspace_bytes < es_attn_fwd_workspace_size(d)))
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
-    return attn_fwd_launch(to_args(d), q, k, v, pos, nbr, out, lse, workspace, workspace_bytes,
-                           (cudaStream_t)stream);
+    AttnArgs a = to_args(d);
+    a.tiles = tiles;
+    return attn_fwd_launch(a, q, k, v, pos, nbr, out, lse, workspace, workspace_bytes, (cudaStream_t)stream);
   });
 }
 
@@ -166,7 +184,7 @@ size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                       const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
-                      void* workspace, size_t workspace_bytes, void* stream) {
+                      const void* tiles, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
@@ -182,8 +200,10 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
     float* delta = (float*)workspace;
     float* dsbuf = (float*)((char*)workspace + align256(sizeof(float) * (size_t)d->N * d->H));
     const size_t base = bwd_base_bytes(d);
-    return attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta,
-                           dsbuf, dpos, (char*)workspace + base, workspace_bytes - base, (cudaStream_t)stream);
+    AttnArgs a = to_args(d);
+    a.tiles = tiles;
+    return attn_bwd_launch(a, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
+                           (char*)workspace + base, workspace_bytes - base, (cudaStream_t)stream);
   });
 }
 

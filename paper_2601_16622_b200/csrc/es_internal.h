@@ -44,6 +44,7 @@ struct AttnArgs {
   int value_mode, phi_mode, dtype, periodic;
   float tau, r_cut;
   double box[3];
+  const void* tiles = nullptr;  // prebuilt tile lists (es_attn_tiles_build) or NULL
 };
 
 size_t attn_fwd_workspace(const AttnArgs& a);
@@ -59,6 +60,9 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
                           const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta,
                           float* dsbuf, double* dpos, void* ws_tc, size_t ws_tc_bytes, cudaStream_t st);
 bool attn_dq_tc_applicable(const AttnArgs& a);
+bool attn_tc_tiles_used(const AttnArgs& a);    // the tcgen05 forward or dq would consume tile lists
+size_t attn_tc_tiles_bytes(const AttnArgs& a);
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, void* tiles, size_t bytes, cudaStream_t st);
 size_t attn_dq_tc_workspace(const AttnArgs& a);
 es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
                             void* ws, size_t ws_bytes, cudaStream_t st);

@@ -101,10 +101,10 @@ def test_invalid_arguments_and_no_cpu_fallback(eslib):
     from paper_2601_16622_b200 import _lib
     d = _lib.AttnDesc()
     d.N, d.K, d.H, d.L, d.C, d.r_cut = 4, 4, 3, 2, 64, 6.0  # C % H != 0
-    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 8), 0, None) == _lib.ES_INVALID_ARGUMENT
+    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 9), 0, None) == _lib.ES_INVALID_ARGUMENT
     assert b"multiple of H" in eslib.es_last_error()
     d.H, d.L = 8, 7
-    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 8), 0, None) == _lib.ES_UNSUPPORTED
+    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 9), 0, None) == _lib.ES_UNSUPPORTED
     if not eslib.es_device_ok():
         import torch
         import paper_2601_16622_b200 as es
