@@ -71,6 +71,20 @@ def load_peaks() -> dict:
             "_source": "fallback (B200_PROFILING.md)"}
 
 
+def count_launches(fn) -> int:
+    """Kernels of libequistream_b200.so (incl. the cub scans it launches)
+    in one call of `fn`, from a torch.profiler CUDA trace taken outside the
+    timed region."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    names = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+    return sum(1 for n in names if "es::" in n or "cub::" in n)
+
+
 def load_traffic():
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of
     the attention kernels from the committed ncu --set full capture."""
@@ -288,7 +302,7 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     dom_bytes = by["attn_fwd"] if dom == "attn_fwd" else by["attn_bwd_kv"]
     achieved = dom_bytes / (t[dom] * 1e-3) / 1e9
     dom_flops = fl["attn_fwd"] if dom == "attn_fwd" else fl["attn_bwd"]
-    launches_per_step = 1 + 1 + (L_ + 1) + 1 + 3 + 2 * (L_ + 1)  # nbr, transpose keys, proj fwd, fwd, bwd(3), proj bwd
+    launches_per_step = count_launches(lambda: step(pos, seg, h, W))
     line = {
         "metric": METRIC,
         "value": round(total_flops / (ms * 1e-3) / 1e12, 4),
