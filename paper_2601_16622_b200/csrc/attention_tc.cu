@@ -617,6 +617,96 @@ __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, con
   if (cnt < K) o[cnt] = 0xffff0000u;
 }
 
+// Warp-per-row list builder for K <= 64 (two slots per lane): the row's
+// (j << 6 | slot) keys are bitonic-sorted across the warp with shuffles, so
+// the valid pairs come out in ascending j (= ascending (chunk, key bit));
+// chunk indices by binary search per lane, one entry per run of equal chunk
+// (bits OR-ed over the run), slots written in sorted order.
+__global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
+                                       const int* __restrict__ clist, uint32_t* __restrict__ rl,
+                                       int* __restrict__ slots) {
+  const int i = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= N) return;
+  const int t = i / TQ, lo = cptr[t], n = cptr[t + 1] - lo;
+  unsigned key[2];  // element e = lane + 32 u
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int s = lane + 32 * u;
+    const int j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
+    key[u] = j >= 0 ? ((unsigned)j << 6) | (unsigned)s : 0xffffffffu;
+  }
+  // bitonic sort of 64 keys, ascending by element index e
+#pragma unroll
+  for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj == 32) {  // partner is the other element of this lane (k == 64 here: ascending)
+        const unsigned a = key[0], b = key[1];
+        key[0] = min(a, b);
+        key[1] = max(a, b);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = lane + 32 * u;
+          const unsigned other = __shfl_xor_sync(0xffffffffu, key[u], jj);
+          const bool up = ((e & k) == 0), lower = ((e & jj) == 0);
+          key[u] = (up == lower) ? min(key[u], other) : max(key[u], other);
+        }
+      }
+    }
+  }
+  // chunk index per valid element; runs of equal chunk -> one entry
+  int ci[2];
+  unsigned bit[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    ci[u] = -1;
+    bit[u] = 0u;
+    if (key[u] != 0xffffffffu) {
+      const int j = (int)(key[u] >> 6), kb = j / KC;
+      int a = 0, b = n;
+      while (a < b) {
+        const int m = (a + b) >> 1;
+        if (clist[lo + m] < kb) a = m + 1;
+        else b = m;
+      }
+      ci[u] = a;
+      bit[u] = 1u << (j % KC);
+      if (slots) slots[(size_t)i * K + lane + 32 * u] = (int)(key[u] & 63u);
+    }
+  }
+  // predecessor's chunk (element e - 1)
+  const int prev0 = __shfl_up_sync(0xffffffffu, ci[0], 1);
+  const int last0 = __shfl_sync(0xffffffffu, ci[0], 31);
+  const int prev1 = __shfl_up_sync(0xffffffffu, ci[1], 1);
+  const bool head0 = ci[0] >= 0 && (lane == 0 || prev0 != ci[0]);
+  const bool head1 = ci[1] >= 0 && (lane == 0 ? last0 != ci[1] : prev1 != ci[1]);
+  // OR of the run's bits: runs have at most 16 elements; accumulate forward
+  uint32_t m0 = bit[0], m1 = bit[1];
+#pragma unroll
+  for (int d = 1; d < KC; ++d) {
+    // element e + d: same half if lane + d < 32, else the other half
+    const int src = (lane + d) & 31;
+    const unsigned b0n = __shfl_sync(0xffffffffu, bit[0], src), b1n = __shfl_sync(0xffffffffu, bit[1], src);
+    const int c0n = __shfl_sync(0xffffffffu, ci[0], src), c1n = __shfl_sync(0xffffffffu, ci[1], src);
+    const bool wrap = lane + d >= 32;
+    // successor of element lane (u = 0) is (wrap ? u = 1 at src : u = 0 at src)
+    const int cs0 = wrap ? c1n : c0n;
+    const unsigned bs0 = wrap ? b1n : b0n;
+    if (head0 && cs0 == ci[0]) m0 |= bs0;
+    if (head1 && !wrap && c1n == ci[1]) m1 |= b1n;
+  }
+  // entry rank = number of heads before this element
+  const unsigned hb0 = __ballot_sync(0xffffffffu, head0), hb1 = __ballot_sync(0xffffffffu, head1);
+  const unsigned below = (1u << lane) - 1u;
+  uint32_t* o = rl + (size_t)i * K;
+  if (head0) o[__popc(hb0 & below)] = ((uint32_t)ci[0] << 16) | m0;
+  if (head1) o[__popc(hb0) + __popc(hb1 & below)] = ((uint32_t)ci[1] << 16) | m1;
+  const int nent = __popc(hb0) + __popc(hb1);
+  if (lane == 0 && nent < K) o[nent] = 0xffff0000u;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -766,7 +856,11 @@ es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const 
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
-  tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist, slots);
+  if (a.K <= 64)
+    tc_rowlist_warp_kernel<<<(unsigned)(((size_t)a.N * 32 + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, cptr, clist,
+                                                                                     rowlist, slots);
+  else
+    tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist, slots);
   *out = TcLists{cptr, clist, rowlist, ntiles};
   return cuda_status(cudaGetLastError(), "attn_tc lists");
 }
