@@ -101,9 +101,9 @@ inline std::size_t tiles_workspace_size(const AttentionProblem& p) {
   return es_attn_tiles_workspace_size(&d);
 }
 inline void build_tiles(const AttentionProblem& p, NeighborIndex& idx, void* buf, std::size_t bytes,
-                        void* stream = nullptr) {
+                        void* stream = nullptr, const int32_t* seg_ptr = nullptr, int32_t nseg = 0) {
   const es_attn_desc d = p.desc();
-  check(es_attn_tiles_build(&d, idx.table, buf, bytes, stream), "build_tiles");
+  check(es_attn_tiles_build(&d, idx.table, seg_ptr, nseg, buf, bytes, stream), "build_tiles");
   idx.tiles = bytes ? buf : nullptr;
 }
 

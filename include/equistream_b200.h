@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 5
+#define ES_ABI_VERSION 6
 
 typedef enum {
   ES_OK = 0,
@@ -93,15 +93,19 @@ typedef struct {
 /* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in
  * {4, 8, 16, 32}.  bf16 + EAAS + L=2 + C=128 + H=8 + K<=64 runs on the
  * tcgen05 tensor-core kernel, everything else on the SIMT kernels. */
-/* Tile structures of one neighbour index (north-star subsystem 3): the
- * tile-skip mask, per-tile key-chunk lists, per-row (chunk, key mask) lists
- * and per-row slot order the tensor-core kernels walk.  Build once per
- * neighbour index with es_attn_tiles_build into a caller buffer of
+/* Tile structures of one neighbour index (north-star subsystem 3): query
+ * tiles, the tile-skip mask, per-tile key-chunk lists, per-row (chunk, key
+ * mask) lists and per-row slot order the tensor-core kernels walk.  Build
+ * once per neighbour index with es_attn_tiles_build into a caller buffer of
  * es_attn_tiles_workspace_size(d) bytes (0: the kernels for d need none) and
  * pass it to every es_attn_fwd / es_attn_bwd (every layer) using that index;
- * tiles = NULL makes each call build them in its workspace instead. */
+ * tiles = NULL makes each call build uniform tiles in its workspace instead.
+ * seg_ptr[nseg + 1] (molecule batches, the array given to
+ * es_neighbors_build; NULL / 0 for one system): query tiles pack whole
+ * segments, so a tile's key chunks cover only its own molecules. */
 size_t es_attn_tiles_workspace_size(const es_attn_desc* d);
-es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, void* tiles, size_t bytes, void* stream);
+es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const int32_t* seg_ptr, int32_t nseg,
+                              void* tiles, size_t bytes, void* stream);
 
 /* Workspace: es_attn_fwd_workspace_size(d) bytes (the tile structures when
  * tiles == NULL; 256 bytes for the SIMT kernels).  Caller-owned, reusable

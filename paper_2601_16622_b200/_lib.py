@@ -66,7 +66,7 @@ def lib() -> ct.CDLL:
         L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 9 + [sz, vp]
         L.es_attn_tiles_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_tiles_workspace_size.restype = sz
-        L.es_attn_tiles_build.argtypes = [ct.POINTER(AttnDesc), vp, vp, sz, vp]
+        L.es_attn_tiles_build.argtypes = [ct.POINTER(AttnDesc), vp, vp, i32, vp, sz, vp]
         L.es_attn_fwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_fwd_workspace_size.restype = sz
         L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 16 + [sz, vp]
@@ -87,7 +87,7 @@ def lib() -> ct.CDLL:
         L.es_cg_real.argtypes = [i32] * 6
         L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
         L.es_wigner_d_host.argtypes = [i32, dp, dp]
-        if L.es_abi_version() != 5:
+        if L.es_abi_version() != 6:
             raise EsError("libequistream_b200.so ABI mismatch: rebuild (python -m paper_2601_16622_b200.build)")
         _lib = L
     return _lib

@@ -63,6 +63,7 @@ class NeighborIndex:
     r_cut: float
     box: tuple | None = None
     _rev: tuple | None = None
+    seg_ptr: torch.Tensor | None = None  # molecule segments the index was built with (packed query tiles)
 
     @property
     def N(self) -> int:
@@ -84,8 +85,10 @@ class NeighborIndex:
         cache = self.__dict__.setdefault("_tiles", {})
         if key not in cache:
             buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.table.device)
-            check(lib().es_attn_tiles_build(ct.byref(d), _ptr(self.table), _ptr(buf), buf.numel(), _stream()),
-                  "es_attn_tiles_build")
+            seg = self.seg_ptr if (self.seg_ptr is not None and d.row0 == 0 and d.N == self.N) else None
+            nseg = 0 if seg is None else seg.numel() - 1
+            check(lib().es_attn_tiles_build(ct.byref(d), _ptr(self.table), _ptr(seg), nseg, _ptr(buf), buf.numel(),
+                                            _stream()), "es_attn_tiles_build")
             cache[key] = buf
         return cache[key]
 
@@ -124,7 +127,8 @@ def build_neighbors(pos: torch.Tensor, K: int, r_cut: float, seg_ptr: torch.Tens
     ws = _workspace(lib().es_neighbors_workspace_size(ct.byref(d)), dev)
     check(lib().es_neighbors_build(ct.byref(d), _ptr(pos), _ptr(seg_ptr), _ptr(nbr), _ptr(dist), _ptr(cnt),
                                    _ptr(ws), ws.numel(), _stream()), "es_neighbors_build")
-    return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box))
+    return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box),
+                         seg_ptr=seg_ptr)
 
 
 def neighbors_transpose(table: torch.Tensor, n_keys: int | None = None):

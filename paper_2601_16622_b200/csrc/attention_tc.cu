@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
     const int* __restrict__ cptr, const int* __restrict__ clist, const uint32_t* __restrict__ rowlist,
-    bf16* __restrict__ out, float* __restrict__ lse) {
+    const int* __restrict__ tstart, bf16* __restrict__ out, float* __restrict__ lse) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + SM_BAR);
@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 23);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int q0 = blockIdx.x * TQ;
+  const int q0 = tstart[blockIdx.x], q1 = tstart[blockIdx.x + 1];
+  if (q0 >= q1) return;  // surplus (empty) tile: nothing to do, no barrier touched yet
 #ifdef ES_TC_TRACE
   const bool TRACE = (a.dbg & 16) && blockIdx.x == 0;
 #endif
@@ -167,8 +168,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
   const bool is_row = warp >= 2 && warp <= 9;
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane of a row thread (warp w -> lanes 32 (w%4) ..)
   const int qi = q0 + row;
-  const bool qvalid = is_row && qi < a.N;
-  const bool qin = qi < a.N;  // row exists (Vg warps load Q rows too)
+  const bool qvalid = is_row && qi < q1;
+  const bool qin = qi < q1;  // row exists (Vg warps load Q rows too)
 
   if (tid == 0) {
     umma::prefetch_tmap(&mk);
@@ -582,10 +583,11 @@ __global__ void tc_fill_kernel(int ntiles, int words, const uint32_t* __restrict
 // row's neighbour slots in the same (ascending j) order, for the dq kernel's
 // dscore gathers.
 __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
-                                  const int* __restrict__ clist, uint32_t* __restrict__ rl, int* __restrict__ slots) {
+                                  const int* __restrict__ clist, const int* __restrict__ rtile,
+                                  uint32_t* __restrict__ rl, int* __restrict__ slots) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  const int t = i / TQ, lo = cptr[t], n = cptr[t + 1] - lo;
+  const int t = rtile[i], lo = cptr[t], n = cptr[t + 1] - lo;
   uint32_t* o = rl + (size_t)i * K;
   int cnt = 0, nv = 0;
   for (int s = 0; s < K; ++s) {
@@ -623,12 +625,12 @@ __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, con
 // chunk indices by binary search per lane, one entry per run of equal chunk
 // (bits OR-ed over the run), slots written in sorted order.
 __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
-                                       const int* __restrict__ clist, uint32_t* __restrict__ rl,
-                                       int* __restrict__ slots) {
+                                       const int* __restrict__ clist, const int* __restrict__ rtile,
+                                       uint32_t* __restrict__ rl, int* __restrict__ slots) {
   const int i = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
-  const int t = i / TQ, lo = cptr[t], n = cptr[t + 1] - lo;
+  const int t = rtile[i], lo = cptr[t], n = cptr[t + 1] - lo;
   unsigned key[2];  // element e = lane + 32 u
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -707,6 +709,84 @@ __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr
   if (lane == 0 && nent < K) o[nent] = 0xffff0000u;
 }
 
+// Query tiles.  Uniform: TQ consecutive rows.  Segment-packed (molecule
+// batches): whole segments greedily packed up to TQ rows (a segment longer
+// than TQ is split at TQ-row boundaries).  The greedy scan is sequential, so
+// the segment list is cut into at most tc_pack_parts(N) parts of consecutive
+// segments, each packed by one thread starting a fresh tile (a part costs at
+// most one under-full tile); a block scan of the per-part tile counts places
+// them.  Tiles past the last start at N (empty CTAs exit).
+__host__ __device__ inline int tc_pack_parts(int N) { return min(1024, ((N + TQ - 1) / TQ) / 32 + 1); }
+
+__global__ void tc_tiles_uniform_kernel(int N, int ntiles, int* __restrict__ tstart) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t <= ntiles) tstart[t] = min(N, t * TQ);
+}
+
+// greedy packing of segments [s0, s1) starting a tile at seg[s0]; emit(row)
+// is called for every tile start
+template <class F>
+__device__ __forceinline__ int tc_pack_part(const int* __restrict__ seg, int s0, int s1, int N, F emit) {
+  int nt = 0;
+  if (s0 >= s1) return 0;
+  int cur = s0 == 0 ? 0 : min(N, max(0, seg[s0]));  // the first tile starts at row 0
+  emit(nt++, cur);
+  int lo = cur;
+  for (int x = s0; x < s1; ++x) {
+    const int hi = min(N, max(lo, seg[x + 1]));
+    if (hi - cur > TQ && lo > cur) {  // the segment does not fit: close the tile before it
+      cur = lo;
+      emit(nt++, cur);
+    }
+    while (hi - cur > TQ) {  // segment longer than a tile: split it
+      cur += TQ;
+      emit(nt++, cur);
+    }
+    lo = hi;
+  }
+  return nt;
+}
+
+__global__ void __launch_bounds__(1024) tc_tiles_packed_kernel(int N, int nseg, const int* __restrict__ seg,
+                                                                int ntiles, int* __restrict__ tstart) {
+  __shared__ int off[1025];
+  const int parts = tc_pack_parts(N), G = (nseg + parts - 1) / parts;
+  const int p = threadIdx.x;
+  const int s0 = min(nseg, p * G), s1 = min(nseg, s0 + G);
+  const int cnt = p < parts ? tc_pack_part(seg, s0, s1, N, [](int, int) {}) : 0;
+  // block exclusive scan of the per-part tile counts
+  off[p + 1] = cnt;
+  if (p == 0) off[0] = 0;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {
+    const int v = p + 1 >= d + 1 ? off[p + 1 - d] : 0;
+    __syncthreads();
+    off[p + 1] += v;
+    __syncthreads();
+  }
+  const int base = off[p], total = min(ntiles, off[1024]);
+  if (p < parts)
+    tc_pack_part(seg, s0, s1, N, [&](int t, int row) {
+      if (base + t < ntiles) tstart[base + t] = row;
+    });
+  for (int t = total + p; t <= ntiles; t += blockDim.x) tstart[t] = N;
+}
+__global__ void tc_rowtile_kernel(int ntiles, const int* __restrict__ tstart, int* __restrict__ rtile) {
+  const int t = blockIdx.x;
+  if (t >= ntiles) return;
+  const int a = tstart[t], b = tstart[t + 1];
+  for (int r = a + threadIdx.x; r < b; r += blockDim.x) rtile[r] = t;
+}
+__global__ void tc_mask_kernel(int N, int K, const int32_t* __restrict__ nbr, const int* __restrict__ rtile,
+                               int words, uint32_t* __restrict__ mask) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * K) return;
+  const int j = nbr[t];
+  if (j < 0) return;
+  const int kb = j / KC;
+  atomicOr(&mask[(size_t)rtile[t / K] * words + kb / 32], 1u << (kb % 32));
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -780,22 +860,32 @@ bool attn_tc_supported(const AttnArgs& a) {
 
 namespace {
 struct TcScratch {
-  int ntiles, nkb, words;
-  size_t chunks, cub_bytes, total;
+  int ntiles, nkb, words;  // ntiles: upper bound (segment-packed tiles are fewer)
+  size_t chunks, cub_bytes, total, pairs;
 };
+// Query tiles are uniform TQ-row blocks, or -- with segments (molecule
+// batches) -- whole segments greedily packed up to TQ rows, so a tile's key
+// chunks cover only its own molecules.  Greedy packing closes a tile only
+// when the next segment does not fit, so two consecutive tiles of one part
+// hold > TQ rows: a part of R rows packs into <= 2 ceil(R / TQ) tiles, and
+// 2 ceil(N / TQ) + 2 parts + 1 bounds the tile count of both schemes (the
+// layout does not depend on which one built the buffer; surplus tiles are
+// empty).
 TcScratch tc_scratch(const AttnArgs& a) {
   TcScratch t;
-  t.ntiles = (a.N + TQ - 1) / TQ;
+  t.ntiles = 2 * ((a.N + TQ - 1) / TQ) + 2 * tc_pack_parts(a.N) + 1;
   t.nkb = (a.Nk + KC - 1) / KC;
   t.words = (t.nkb + 31) / 32;
   // a tile's chunk list is at most min(nkb, its valid pairs) long: the packed
   // lists of all tiles fit min(ntiles * nkb, N * K) entries
   const size_t dense = (size_t)t.ntiles * t.nkb, pairs = (size_t)a.N * a.K;
+  t.pairs = pairs;
   t.chunks = dense < pairs ? dense : pairs;
   t.cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, t.cub_bytes, (int*)nullptr, (int*)nullptr, t.ntiles + 1);
   t.total = align256((size_t)t.ntiles * t.words * 4) + 2 * align256((size_t)(t.ntiles + 1) * 4) +
-            align256(t.chunks * 4) + align256(t.cub_bytes) + align256(pairs * 4);
+            align256(t.chunks * 4) + align256(t.cub_bytes) + align256(pairs * 4) +
+            align256((size_t)(t.ntiles + 1) * 4) + align256((size_t)a.N * 4);
   return t;
 }
 }  // namespace
@@ -808,6 +898,7 @@ struct TcLists {
   const int* clist;
   const uint32_t* rowlist;
   int ntiles;
+  const int* tstart;  // [ntiles + 1] first query row of each tile (N past the last)
 };
 // the list arrays inside a tile / workspace buffer laid out by tc_scratch
 struct TcPtrs {
@@ -815,6 +906,8 @@ struct TcPtrs {
   int *cnt, *cptr, *clist;
   void* cub;
   uint32_t* rowlist;
+  int* tstart;  // [ntiles + 1]
+  int* rtile;   // [N] tile of each query row
   int* slots;  // only when the buffer holds them (tile buffers do)
 };
 TcPtrs tc_ptrs(void* base_, const TcScratch& t) {
@@ -832,13 +925,17 @@ TcPtrs tc_ptrs(void* base_, const TcScratch& t) {
   p.cub = base + off;
   off += align256(t.cub_bytes);
   p.rowlist = (uint32_t*)(base + off);
+  off += align256(t.pairs * 4);
+  p.tstart = (int*)(base + off);
+  off += align256((size_t)(ntiles + 1) * 4);
+  p.rtile = (int*)(base + off);
   p.slots = (int*)(base + t.total);
   return p;
 }
 
 // tile-skip mask -> per-tile key-chunk lists -> per-row (chunk, key mask) lists
 es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const TcScratch& t, int* slots,
-                         TcLists* out, cudaStream_t st) {
+                         TcLists* out, cudaStream_t st, const int32_t* seg = nullptr, int nseg = 0) {
   const int ntiles = t.ntiles, words = t.words;
   size_t cub_bytes = t.cub_bytes;
   const TcPtrs pp = tc_ptrs(ws, t);
@@ -848,20 +945,25 @@ es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const 
   int* clist = pp.clist;
   void* cub_ws = pp.cub;
   uint32_t* rowlist = pp.rowlist;
+  if (seg && nseg > 0) tc_tiles_packed_kernel<<<1, 1024, 0, st>>>(a.N, nseg, seg, ntiles, pp.tstart);
+  else tc_tiles_uniform_kernel<<<(ntiles + 256) / 256, 256, 0, st>>>(a.N, ntiles, pp.tstart);
+  tc_rowtile_kernel<<<ntiles, 128, 0, st>>>(ntiles, pp.tstart, pp.rtile);
   cudaMemsetAsync(mask, 0, (size_t)ntiles * words * 4, st);
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
-  es_status s = tile_mask_launch(a.N, a.K, nbr, TQ, KC, (a.Nk + KC - 1) / KC, mask, st);
-  if (s != ES_OK) return s;
+  {
+    const size_t n = (size_t)a.N * a.K;
+    tc_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, pp.rtile, words, mask);
+  }
   tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
   if (a.K <= 64)
     tc_rowlist_warp_kernel<<<(unsigned)(((size_t)a.N * 32 + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, cptr, clist,
-                                                                                     rowlist, slots);
+                                                                                     pp.rtile, rowlist, slots);
   else
-    tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, rowlist, slots);
-  *out = TcLists{cptr, clist, rowlist, ntiles};
+    tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, pp.rtile, rowlist, slots);
+  *out = TcLists{cptr, clist, rowlist, ntiles, pp.tstart};
   return cuda_status(cudaGetLastError(), "attn_tc lists");
 }
 }  // namespace
@@ -878,7 +980,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   TcLists lists;
   if (a.tiles) {  // lists prebuilt for this neighbour index (es_attn_tiles_build)
     const TcPtrs pp = tc_ptrs(const_cast<void*>(a.tiles), t);
-    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles};
+    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles, pp.tstart};
   } else {
     if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
     s = tc_build_lists(a, nbr, ws, t, nullptr, &lists, st);
@@ -908,7 +1010,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
     attr = true;
   }
   attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
-                                                        (bf16*)out, lse);
+                                                        lists.tstart, (bf16*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
 }
 
@@ -936,7 +1038,7 @@ constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
     const __grid_constant__ CUtensorMap mk, int N, int K, float tau, const int* __restrict__ cptr,
     const int* __restrict__ clist, const uint32_t* __restrict__ rowlist, const int* __restrict__ slots,
-    const float* __restrict__ dsbuf, bf16* __restrict__ dq) {
+    const int* __restrict__ tstart, const float* __restrict__ dsbuf, bf16* __restrict__ dq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DQ_SM_BAR);
@@ -948,6 +1050,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
   uint64_t* epi_done = bars + 21;  // rows read the accumulator (128)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 22);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q0 = tstart[blockIdx.x], q1 = tstart[blockIdx.x + 1];
+  if (q0 >= q1) return;  // surplus (empty) tile
   const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
   if (tid == 0) {
     umma::prefetch_tmap(&mk);
@@ -1021,8 +1125,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
   } else {
     // ================= rows: dscore tiles, epilogue
     const int row = ((warp & 3) << 5) | lane;
-    const int qi = blockIdx.x * TQ + row;
-    const bool qin = qi < N;
+    const int qi = q0 + row;
+    const bool qin = qi < q1;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * K;
     const int* sl = slots + (size_t)(qin ? qi : 0) * K;
@@ -1104,8 +1208,8 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
           const int rr = it * 8 + (lane >> 2), part = lane & 3;
-          const int qq = blockIdx.x * TQ + (warp & 3) * 32 + rr;
-          if (qq < N)
+          const int qq = q0 + (warp & 3) * 32 + rr;
+          if (qq < q1)
             *reinterpret_cast<uint4*>(dq + ((size_t)qq * MM + mm) * 256 + DH * h + part * 8) =
                 *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
         }
@@ -1144,7 +1248,7 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
   int* slots;
   if (a.tiles) {  // lists + slot order prebuilt for this neighbour index
     const TcPtrs pp = tc_ptrs(const_cast<void*>(a.tiles), t);
-    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles};
+    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles, pp.tstart};
     slots = pp.slots;
   } else {
     if (!ws || ws_bytes < attn_dq_tc_workspace(a)) return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small");
@@ -1162,7 +1266,7 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
     attr = true;
   }
   attn_dq_tc_kernel<<<lists.ntiles, DQ_THREADS, smem, st>>>(mk, a.N, a.K, a.tau, lists.cptr, lists.clist,
-                                                           lists.rowlist, slots, dsbuf, (bf16*)dq);
+                                                           lists.rowlist, slots, lists.tstart, dsbuf, (bf16*)dq);
   return cuda_status(cudaGetLastError(), "attn_dq_tc_kernel");
 }
 
@@ -1175,12 +1279,13 @@ size_t attn_tc_tiles_bytes(const AttnArgs& a) {
 
 // The tile structures of one neighbour index, built once and reused by every
 // forward / backward (and every layer) that uses the same index.
-es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, void* tiles, size_t bytes, cudaStream_t st) {
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg, void* tiles,
+                              size_t bytes, cudaStream_t st) {
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
   if (!tiles || bytes < attn_tc_tiles_bytes(a)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: buffer too small");
   TcLists lists;
-  return tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st);
+  return tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st, seg, nseg);
 }
 
 }  // namespace es

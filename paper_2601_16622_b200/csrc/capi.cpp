@@ -144,14 +144,16 @@ size_t es_attn_tiles_workspace_size(const es_attn_desc* d) {
   return attn_tc_tiles_used(a) ? attn_tc_tiles_bytes(a) : 0;
 }
 
-es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, void* tiles, size_t bytes, void* stream) {
+es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const int32_t* seg_ptr, int32_t nseg,
+                              void* tiles, size_t bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
     const AttnArgs a = to_args(d);
     if (!attn_tc_tiles_used(a)) return ES_OK;  // the SIMT kernels need no tile lists
     if (d->N > 0 && !nbr) return fail(ES_INVALID_ARGUMENT, "attn_tiles: null buffer");
-    return attn_tc_tiles_build(a, nbr, tiles, bytes, (cudaStream_t)stream);
+    if (nseg < 0 || (nseg > 0 && !seg_ptr)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: nseg > 0 needs seg_ptr");
+    return attn_tc_tiles_build(a, nbr, nseg > 0 ? seg_ptr : nullptr, nseg, tiles, bytes, (cudaStream_t)stream);
   });
 }
 

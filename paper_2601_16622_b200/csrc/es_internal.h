@@ -62,7 +62,8 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
 bool attn_dq_tc_applicable(const AttnArgs& a);
 bool attn_tc_tiles_used(const AttnArgs& a);    // the tcgen05 forward or dq would consume tile lists
 size_t attn_tc_tiles_bytes(const AttnArgs& a);
-es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, void* tiles, size_t bytes, cudaStream_t st);
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg, void* tiles,
+                              size_t bytes, cudaStream_t st);
 size_t attn_dq_tc_workspace(const AttnArgs& a);
 es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
                             void* ws, size_t ws_bytes, cudaStream_t st);

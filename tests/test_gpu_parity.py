@@ -132,10 +132,11 @@ def _attn_inputs(N, L, C, H, K, seed, seg=False, box=None):
     return pos, nbr, q, k, v, box
 
 
-def _run_attn(es, pos, nbr, q, k, v, L, H, vm, dtype, box=None, dout=None):
+def _run_attn(es, pos, nbr, q, k, v, L, H, vm, dtype, box=None, dout=None, seg=None):
     from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
     cfg = AttentionConfig(heads=H, L=L, r_cut=6.0, value_mode=vm, box=None if box is None else tuple(box))
-    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    # seg: the molecule segments -> segment-packed query tiles on the TC path
+    idx = NeighborIndex(dev(nbr), None, None, 6.0, seg_ptr=None if seg is None else dev(seg))
     tq, tk, tv = dev(q, dtype), dev(k, dtype), dev(v, dtype)
     tp = dev(pos)
     out, lse = es.stream_aggregate(tq, tk, tv, tp, idx, cfg)
@@ -280,17 +281,22 @@ def test_full_size_properties_config2(es):
     assert 10 < cnt.mean() < 20
 
 
-@pytest.mark.parametrize("kind", ["batch", "bulk", "pbc", "sharp", "empty_tiles"])
+@pytest.mark.parametrize("kind", ["batch", "batch_uniform", "long_segments", "bulk", "pbc", "sharp", "empty_tiles"])
 def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     """The tcgen05 paths (forward, dq; bf16, L=2, C=128, H=8) over many
-    128-query tiles and key chunks: molecule batch, one bulk system, a
-    periodic box, a batch with 6x scaled queries (score ranges > 5 nats, so
-    the lazy online-softmax rescale of the TMEM accumulator fires), and a
-    system whose middle 300 atoms are isolated (whole tiles without a pair)."""
+    128-query tiles and key chunks: molecule batch (segment-packed query
+    tiles, and uniform tiles), a batch of molecules longer than a tile (split
+    segments), one bulk system, a periodic box, a batch with 6x scaled
+    queries (score ranges > 5 nats, so the lazy online-softmax rescale of the
+    TMEM accumulator fires), and a system whose middle 300 atoms are isolated
+    (whole tiles without a pair)."""
     L, C, H = 2, 128, 8
     box = None
-    if kind in ("batch", "sharp"):
+    if kind in ("batch", "batch_uniform", "sharp"):
         b = S.molecule_batch(12, 40, 60, 5)
+        pos, seg = b.pos, b.seg_ptr
+    elif kind == "long_segments":
+        b = S.molecule_batch(5, 100, 300, 5)
         pos, seg = b.pos, b.seg_ptr
     elif kind == "empty_tiles":
         core = S.gen_fcc_system(200, 3.8, 9)
@@ -312,13 +318,40 @@ def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
     P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
     rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
     dout = torch.tensor(np.random.default_rng(10).standard_normal(rout.shape)).bfloat16().double().numpy()
-    out, lse, (dq, dk, dv) = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box, dout=dout)
+    out, lse, (dq, dk, dv) = _run_attn(es, pos, nbr, q, k, v, L, H, "eaas", torch.bfloat16, box=box, dout=dout,
+                                       seg=None if kind == "batch_uniform" else seg)
     assert rel(out.float().cpu(), rout) < BF16_TOL
     fin = np.isfinite(rlse)
     assert rel(lse.cpu().numpy()[fin], rlse[fin]) < 1e-3
     rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, dout)
     for a_, b_ in ((dq, rdq), (dk, rdk), (dv, rdv)):
         assert rel(a_.float().cpu(), b_) < BF16_TOL
+
+
+def test_segment_packed_tiles_match_uniform(es):
+    """Segment-packed query tiles at a size where the packing runs in several
+    parts (N > 32 tiles of 128 rows), molecules of 20..300 atoms (some split
+    across tiles): forward and backward equal those on uniform tiles (the
+    per-row key-chunk order is the same, so the results are bit-identical)."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    b = S.molecule_batch(90, 20, 300, 11)
+    N = len(b.pos)
+    assert N > 32 * 128 * 2
+    tp, seg = dev(b.pos), dev(b.seg_ptr)
+    idx = es.build_neighbors(tp, 64, 6.0, seg)
+    assert idx.seg_ptr is not None
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q, k = (torch.randn(N, 9, 256, device="cuda", generator=g).bfloat16() for _ in range(2))
+    v, go = (torch.randn(N, 9, 128, device="cuda", generator=g).bfloat16() for _ in range(2))
+    cfg = AttentionConfig(heads=8, L=2)
+    res = []
+    for packed in (True, False):
+        ix = NeighborIndex(idx.table, None, idx.count, 6.0, seg_ptr=seg if packed else None)
+        out, lse = es.stream_aggregate(q, k, v, tp, ix, cfg)
+        grads = es.stream_aggregate_backward(go, SavedAttention(q, k, v, tp, ix, out, lse, cfg))
+        res.append((out, lse) + tuple(grads))
+    for a_, b_ in zip(*res):
+        assert torch.equal(a_, b_)
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
