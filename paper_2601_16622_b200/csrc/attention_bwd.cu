@@ -107,17 +107,20 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
       const int i = __float_as_int(rec[LY::OFF_J]);
       const int pr = __float_as_int(rec[LY::OFF_X]);
       float qv[M][2 * CPL];
-      float s = 0.f;
+      float sc[2 * CPL];
+#pragma unroll
+      for (int c = 0; c < 2 * CPL; ++c) sc[c] = 0.f;
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
         ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qv[mm]);
-#pragma unroll
         float kr[2 * CPL];
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) kr[c] = ks[(mm * nthr + threadIdx.x) * 2 * CPL + c];
-#pragma unroll
-        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qv[mm][c], kr[c], s);
+        fmav<2 * CPL>(qv[mm], kr, sc);
       }
+      float s = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2 * CPL; ++c) s += sc[c];
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       const float P = expf(s * p.tau - lse[(size_t)i * PH + head]);
       const float phi = rec[LY::OFF_PHI];
@@ -136,18 +139,20 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
 #pragma unroll
           for (int c = 0; c < CPL; ++c) y[mm][c] = phi * g[mm][c];
       }
-      float dp = 0.f;
+      float dpc[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) dpc[c] = 0.f;
 #pragma unroll
       for (int mm = 0; mm < M; ++mm) {
         float vr[CPL];
 #pragma unroll
         for (int c = 0; c < CPL; ++c) vr[c] = vs[(mm * nthr + threadIdx.x) * CPL + c];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          dvr[mm][c] = fmaf(P, y[mm][c], dvr[mm][c]);
-          dp = fmaf(y[mm][c], vr[c], dp);
-        }
+        fmac<CPL>(P, y[mm], dvr[mm]);
+        fmav<CPL>(y[mm], vr, dpc);
       }
+      float dp = 0.f;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) dp += dpc[c];
       for (int o = lph >> 1; o > 0; o >>= 1) dp += __shfl_xor_sync(0xffffffffu, dp, o);
       const float ds = P * (dp - delta[(size_t)i * PH + head]);
       if constexpr (FORCE) {
@@ -209,9 +214,7 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
       }
       const float tds = p.tau * ds;
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm)
-#pragma unroll
-        for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+      for (int mm = 0; mm < M; ++mm) fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
       if ((lane % lph) == 0) dsbuf[(size_t)pr * PH + head] = ds;
     }
   }

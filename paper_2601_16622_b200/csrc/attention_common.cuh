@@ -336,6 +336,45 @@ __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, i
   }
 }
 
+// acc[c] += a * x[c] over a thread's channels: channel pairs go through the
+// packed FFMA2 (sm_100: two fp32 FMAs per issue slot, the scalar broadcast is
+// an operand modifier), so the FMA-bound per-pair value work issues half the
+// instructions.  Same rounding as fmaf per lane.
+__device__ __forceinline__ void ffma2(float a, float x0, float x1, float& c0, float& c1) {
+  asm("{\n\t.reg .b64 a2, x2, c2;\n\t"
+      "mov.b64 a2, {%2, %2};\n\t"
+      "mov.b64 x2, {%3, %4};\n\t"
+      "mov.b64 c2, {%0, %1};\n\t"
+      "fma.rn.f32x2 c2, a2, x2, c2;\n\t"
+      "mov.b64 {%0, %1}, c2;\n\t}"
+      : "+f"(c0), "+f"(c1)
+      : "f"(a), "f"(x0), "f"(x1));
+}
+// acc[c] += x[c] * y[c] (element-wise pairs)
+__device__ __forceinline__ void ffma2v(float x0, float x1, float y0, float y1, float& c0, float& c1) {
+  asm("{\n\t.reg .b64 x2, y2, c2;\n\t"
+      "mov.b64 x2, {%2, %3};\n\t"
+      "mov.b64 y2, {%4, %5};\n\t"
+      "mov.b64 c2, {%0, %1};\n\t"
+      "fma.rn.f32x2 c2, x2, y2, c2;\n\t"
+      "mov.b64 {%0, %1}, c2;\n\t}"
+      : "+f"(c0), "+f"(c1)
+      : "f"(x0), "f"(x1), "f"(y0), "f"(y1));
+}
+template <int CPL>
+__device__ __forceinline__ void fmac(float a, const float (&x)[CPL], float (&acc)[CPL]) {
+#pragma unroll
+  for (int c = 0; c + 1 < CPL; c += 2) ffma2(a, x[c], x[c + 1], acc[c], acc[c + 1]);
+  if constexpr (CPL & 1) acc[CPL - 1] = fmaf(a, x[CPL - 1], acc[CPL - 1]);
+}
+// acc[c] += x[c] * y[c]
+template <int CPL>
+__device__ __forceinline__ void fmav(const float (&x)[CPL], const float (&y)[CPL], float (&acc)[CPL]) {
+#pragma unroll
+  for (int c = 0; c + 1 < CPL; c += 2) ffma2v(x[c], x[c + 1], y[c], y[c + 1], acc[c], acc[c + 1]);
+  if constexpr (CPL & 1) acc[CPL - 1] = fmaf(x[CPL - 1], y[CPL - 1], acc[CPL - 1]);
+}
+
 // x += s * (D^T P D) v  per channel (EAAS forward value operator), or the
 // adjoint y += s * (D^T P^T D) g when ADJ.  v: [M][CPL] registers.
 template <int L, int CPL, bool ADJ>
@@ -351,14 +390,12 @@ __device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const 
     const float* D = rec + Lay<L>::doff(l);
     const int d = 2 * l + 1;
 #pragma unroll
-    for (int m = 0; m < d; ++m)
+    for (int m = 0; m < d; ++m) {
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        float t = 0.f;
+      for (int c = 0; c < CPL; ++c) vt[l * l + m][c] = 0.f;
 #pragma unroll
-        for (int mp = 0; mp < d; ++mp) t = fmaf(D[m * d + mp], v[l * l + mp][c], t);
-        vt[l * l + m][c] = t;
-      }
+      for (int mp = 0; mp < d; ++mp) fmac<CPL>(D[m * d + mp], v[l * l + mp], vt[l * l + m]);
+    }
   }
   // sparse re-index in the aligned frame (forward P or adjoint P^T)
   float w[M][CPL];
@@ -376,34 +413,30 @@ __device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const 
         const int e = Lay<L>::eoff(lo, li) + m + mm;
         const float a = rec[Lay<L>::OFF_AB + 2 * e];
         const float b = rec[Lay<L>::OFF_AB + 2 * e + 1];
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          if constexpr (!ADJ) {
-            w[lo * lo + lo + m][c] = fmaf(a, vt[li * li + li + m][c], w[lo * lo + lo + m][c]);
-            if (m != 0) w[lo * lo + lo + m][c] = fmaf(b, vt[li * li + li - m][c], w[lo * lo + lo + m][c]);
-          } else {
-            w[li * li + li + m][c] = fmaf(a, vt[lo * lo + lo + m][c], w[li * li + li + m][c]);
-            if (m != 0) w[li * li + li - m][c] = fmaf(b, vt[lo * lo + lo + m][c], w[li * li + li - m][c]);
-          }
+        if constexpr (!ADJ) {
+          fmac<CPL>(a, vt[li * li + li + m], w[lo * lo + lo + m]);
+          if (m != 0) fmac<CPL>(b, vt[li * li + li - m], w[lo * lo + lo + m]);
+        } else {
+          fmac<CPL>(a, vt[lo * lo + lo + m], w[li * li + li + m]);
+          if (m != 0) fmac<CPL>(b, vt[lo * lo + lo + m], w[li * li + li - m]);
         }
       }
     }
   // un-align and accumulate: acc^l += s * D^l^T w^l
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[0][c] = fmaf(s, w[0][c], acc[0][c]);
+  fmac<CPL>(s, w[0], acc[0]);
 #pragma unroll
   for (int l = 1; l <= L; ++l) {
     const float* D = rec + Lay<L>::doff(l);
     const int d = 2 * l + 1;
 #pragma unroll
-    for (int m = 0; m < d; ++m)
+    for (int m = 0; m < d; ++m) {
+      float t[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        float t = 0.f;
+      for (int c = 0; c < CPL; ++c) t[c] = 0.f;
 #pragma unroll
-        for (int mp = 0; mp < d; ++mp) t = fmaf(D[mp * d + m], w[l * l + mp][c], t);
-        acc[l * l + m][c] = fmaf(s, t, acc[l * l + m][c]);
-      }
+      for (int mp = 0; mp < d; ++mp) fmac<CPL>(D[mp * d + m], w[l * l + mp], t);
+      fmac<CPL>(s, t, acc[l * l + m]);
+    }
   }
 }
 
