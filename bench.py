@@ -387,7 +387,8 @@ def reference_arm(args, rank: int, world: int):
     if rank != 0:
         return None
     steps = []
-    for _ in range(args.warmup_ref):
+    warm = args.warmup if args.warmup_ref is None else args.warmup_ref
+    for _ in range(warm):
         cpu_baseline(args.cpu_molecules, threads=None)
     for _ in range(max(1, min(args.steps, args.ref_steps))):
         steps.append(cpu_baseline(args.cpu_molecules, threads=None))
@@ -395,7 +396,7 @@ def reference_arm(args, rank: int, world: int):
     base = steps[0]
     return {
         "impl": "reference", "metric": METRIC, "value": round(val, 6), "unit": "TFLOP/s", "n_gpus": world,
-        "steps": len(steps), "warmup": args.warmup_ref, "higher_is_better": True, "scaling": "weak",
+        "steps": len(steps), "warmup": warm, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp64", "data": "synthetic (FCC molecules, random features/weights; seeded)",
         "config": {"workload": "configs[1] SPICE-like batch (bounded sample, see cpu_baseline.sample)",
                    "L_max": L_, "channels": C_, "heads": H_, "K": K_},
@@ -415,7 +416,7 @@ def main():
     ap.add_argument("--molecules", type=int, default=4096)
     ap.add_argument("--cpu-molecules", type=int, default=32)
     ap.add_argument("--ref-steps", type=int, default=3)
-    ap.add_argument("--warmup-ref", type=int, default=0)
+    ap.add_argument("--warmup-ref", type=int, default=None)  # default: --warmup
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
