@@ -10,7 +10,8 @@
 // (hashed cell grid or per-segment scan) cannot change a single bit.
 //
 // Search structures:
-//  * segmented input (molecule batches): thread per atom scans its segment;
+//  * segmented input (molecule batches): warp per atom over its segment,
+//    slots by rank (nbr_segment_warp_kernel);
 //  * one system: hashed uniform grid, cell edge >= r_cut, 27-cell stencil,
 //    exact cell-coordinate filter against hash collisions; under PBC the grid
 //    tiles the box (>= 3 cells per axis).
@@ -67,15 +68,28 @@ __device__ __forceinline__ void emit(const NbrK& p, int i, const TopK& t, int32_
   count[i] = t.n;
 }
 
-__global__ void __launch_bounds__(128) nbr_segment_kernel(NbrK p, const double* __restrict__ pos,
-                                                          const int32_t* __restrict__ seg_ptr,
-                                                          int32_t* __restrict__ nbr, float* __restrict__ dist,
-                                                          int32_t* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per atom for segments of <= SEG_WARP_MAX + 1 atoms (molecule
+// batches): the lanes evaluate the segment's candidates 32 at a time and
+// compact the kept ones (d2 < r_cut^2, j != i) into shared memory; each kept
+// candidate's slot is then its rank under (d2, j) -- the same order the
+// sorted top-K produces -- so no per-thread sorted list (the scan kernel's
+// TopK lives in local memory).  Larger segments: lane 0 runs the scan.
+constexpr int SEG_WARP_MAX = 256;
+constexpr int SEG_WARPS = 8;
+
+__global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p, const double* __restrict__ pos,
+                                                                          const int32_t* __restrict__ seg_ptr,
+                                                                          int32_t* __restrict__ nbr,
+                                                                          float* __restrict__ dist,
+                                                                          int32_t* __restrict__ count) {
+  __shared__ double cd[SEG_WARPS][SEG_WARP_MAX];
+  __shared__ int cj[SEG_WARPS][SEG_WARP_MAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * SEG_WARPS + warp;
   if (i >= p.N) return;
   int a0 = 0, a1 = p.N;
   if (seg_ptr) {
-    int lo = 0, hi = p.nseg;  // find s with seg_ptr[s] <= i < seg_ptr[s+1]
+    int lo = 0, hi = p.nseg;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (seg_ptr[mid] <= i) lo = mid;
@@ -84,15 +98,60 @@ __global__ void __launch_bounds__(128) nbr_segment_kernel(NbrK p, const double* 
     a0 = seg_ptr[lo];
     a1 = seg_ptr[lo + 1];
   }
-  TopK t;
-  t.n = 0;
   const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
-  for (int j = a0; j < a1; ++j) {
-    if (j == i) continue;
-    const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
-    if (d < p.rc2) t.insert(d, j, p.K);
+  if (a1 - a0 > SEG_WARP_MAX + 1) {  // more candidates than the shared buffer holds
+    if (lane == 0) {
+      TopK t;
+      t.n = 0;
+      for (int j = a0; j < a1; ++j) {
+        if (j == i) continue;
+        const double d =
+            d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
+        if (d < p.rc2) t.insert(d, j, p.K);
+      }
+      emit(p, i, t, nbr, dist, count);
+    }
+    return;
   }
-  emit(p, i, t, nbr, dist, count);
+  int n = 0;
+  for (int j0 = a0; j0 < a1; j0 += 32) {
+    const int j = j0 + lane;
+    double d = 0.0;
+    bool keep = false;
+    if (j < a1 && j != i) {
+      d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
+      keep = d < p.rc2;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int at = n + __popc(m & ((1u << lane) - 1u));
+      cd[warp][at] = d;
+      cj[warp][at] = j;
+    }
+    n += __popc(m);
+  }
+  __syncwarp();
+  const int K = p.K;
+  int32_t* orow = nbr + (size_t)i * K;
+  float* drow = dist ? dist + (size_t)i * K : nullptr;
+  for (int c = lane; c < n; c += 32) {
+    const double d = cd[warp][c];
+    const int j = cj[warp][c];
+    int rank = 0;
+    for (int o = 0; o < n; ++o) {
+      const double od = cd[warp][o];
+      rank += (od < d || (od == d && cj[warp][o] < j)) ? 1 : 0;
+    }
+    if (rank < K) {
+      orow[rank] = j;
+      if (drow) drow[rank] = (float)sqrt(d);
+    }
+  }
+  for (int s = min(n, K) + lane; s < K; s += 32) {
+    orow[s] = -1;
+    if (drow) drow[s] = 0.f;
+  }
+  if (lane == 0) count[i] = min(n, K);
 }
 
 // ---------------------------------------------------------------- hashed grid
@@ -234,8 +293,9 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
   const int tpb = 128, blocks = (a.N + tpb - 1) / tpb;
   if (!use_grid(a)) {
     const int32_t* sp = (seg_ptr && a.nseg >= 1) ? seg_ptr : nullptr;  // NULL: one segment [0, N)
-    nbr_segment_kernel<<<blocks, tpb, 0, st>>>(p, pos, sp, nbr, dist, count);
-    return cuda_status(cudaGetLastError(), "nbr_segment_kernel");
+    nbr_segment_warp_kernel<<<(a.N + SEG_WARPS - 1) / SEG_WARPS, SEG_WARPS * 32, 0, st>>>(p, pos, sp, nbr, dist,
+                                                                                           count);
+    return cuda_status(cudaGetLastError(), "nbr_segment_warp_kernel");
   }
   const GridWs w = grid_ws(a.N);
   if (ws_bytes < w.total) return fail(ES_INVALID_ARGUMENT, "neighbors: workspace too small");

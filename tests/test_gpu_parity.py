@@ -44,6 +44,8 @@ NBR_CASES = {
     "fcc600_scan": lambda: (S.gen_fcc_system(600, 3.8, 1), None, None, 64),
     "fcc3000_K8": lambda: (S.gen_fcc_system(3000, 3.8, 2), None, None, 8),
     "batch": lambda: (lambda b: (b.pos, b.seg_ptr, None, 32))(S.molecule_batch(64, 40, 60, 3)),
+    "batch_K8": lambda: (lambda b: (b.pos, b.seg_ptr, None, 8))(S.molecule_batch(40, 40, 60, 6)),
+    "batch_big_segments": lambda: (lambda b: (b.pos, b.seg_ptr, None, 64))(S.molecule_batch(6, 150, 420, 7)),
     "pbc_grid": lambda: (lambda b: (b.pos, None, b.box, 64))(S.periodic_box(6000, 12, 3.8, 4)),
     "pbc_small_box": lambda: (lambda b: (b.pos, None, b.box, 64))(S.periodic_box(100, 4, 3.8, 5)),
 }
