@@ -619,11 +619,13 @@ __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, con
   if (cnt < K) o[cnt] = 0xffff0000u;
 }
 
-// Warp-per-row list builder for K <= 64 (two slots per lane): the row's
-// (j << 6 | slot) keys are bitonic-sorted across the warp with shuffles, so
-// the valid pairs come out in ascending j (= ascending (chunk, key bit));
-// chunk indices by binary search per lane, one entry per run of equal chunk
-// (bits OR-ed over the run), slots written in sorted order.
+// Warp-per-row list builder for K <= 64 (two slots per lane): each valid
+// slot finds its chunk's index in the tile list (binary search); the row's
+// distinct chunks are then emitted in ascending order, one warp min-reduce
+// (next chunk) and one OR-reduce (its 16-bit key mask) per entry -- a row
+// touches a handful of chunks, so this replaces a 64-key sort.  A slot's
+// position in the ascending-j slot order is the valid keys in earlier
+// chunks plus the key bits below its own.
 __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
                                        const int* __restrict__ clist, const int* __restrict__ rtile,
                                        uint32_t* __restrict__ rl, int* __restrict__ slots) {
@@ -631,42 +633,17 @@ __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
   const int t = rtile[i], lo = cptr[t], n = cptr[t + 1] - lo;
-  unsigned key[2];  // element e = lane + 32 u
-#pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int s = lane + 32 * u;
-    const int j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
-    key[u] = j >= 0 ? ((unsigned)j << 6) | (unsigned)s : 0xffffffffu;
-  }
-  // bitonic sort of 64 keys, ascending by element index e
-#pragma unroll
-  for (int k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-    for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      if (jj == 32) {  // partner is the other element of this lane (k == 64 here: ascending)
-        const unsigned a = key[0], b = key[1];
-        key[0] = min(a, b);
-        key[1] = max(a, b);
-      } else {
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int e = lane + 32 * u;
-          const unsigned other = __shfl_xor_sync(0xffffffffu, key[u], jj);
-          const bool up = ((e & k) == 0), lower = ((e & jj) == 0);
-          key[u] = (up == lower) ? min(key[u], other) : max(key[u], other);
-        }
-      }
-    }
-  }
-  // chunk index per valid element; runs of equal chunk -> one entry
+  constexpr int NONE = 0x7fffffff;
   int ci[2];
   unsigned bit[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    ci[u] = -1;
+    const int s = lane + 32 * u;
+    const int j = s < K ? __ldg(nbr + (size_t)i * K + s) : -1;
+    ci[u] = NONE;
     bit[u] = 0u;
-    if (key[u] != 0xffffffffu) {
-      const int j = (int)(key[u] >> 6), kb = j / KC;
+    if (j >= 0) {
+      const int kb = j / KC;
       int a = 0, b = n;
       while (a < b) {
         const int m = (a + b) >> 1;
@@ -675,37 +652,24 @@ __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr
       }
       ci[u] = a;
       bit[u] = 1u << (j % KC);
-      if (slots) slots[(size_t)i * K + lane + 32 * u] = (int)(key[u] & 63u);
     }
   }
-  // predecessor's chunk (element e - 1)
-  const int prev0 = __shfl_up_sync(0xffffffffu, ci[0], 1);
-  const int last0 = __shfl_sync(0xffffffffu, ci[0], 31);
-  const int prev1 = __shfl_up_sync(0xffffffffu, ci[1], 1);
-  const bool head0 = ci[0] >= 0 && (lane == 0 || prev0 != ci[0]);
-  const bool head1 = ci[1] >= 0 && (lane == 0 ? last0 != ci[1] : prev1 != ci[1]);
-  // OR of the run's bits: runs have at most 16 elements; accumulate forward
-  uint32_t m0 = bit[0], m1 = bit[1];
-#pragma unroll
-  for (int d = 1; d < KC; ++d) {
-    // element e + d: same half if lane + d < 32, else the other half
-    const int src = (lane + d) & 31;
-    const unsigned b0n = __shfl_sync(0xffffffffu, bit[0], src), b1n = __shfl_sync(0xffffffffu, bit[1], src);
-    const int c0n = __shfl_sync(0xffffffffu, ci[0], src), c1n = __shfl_sync(0xffffffffu, ci[1], src);
-    const bool wrap = lane + d >= 32;
-    // successor of element lane (u = 0) is (wrap ? u = 1 at src : u = 0 at src)
-    const int cs0 = wrap ? c1n : c0n;
-    const unsigned bs0 = wrap ? b1n : b0n;
-    if (head0 && cs0 == ci[0]) m0 |= bs0;
-    if (head1 && !wrap && c1n == ci[1]) m1 |= b1n;
-  }
-  // entry rank = number of heads before this element
-  const unsigned hb0 = __ballot_sync(0xffffffffu, head0), hb1 = __ballot_sync(0xffffffffu, head1);
-  const unsigned below = (1u << lane) - 1u;
   uint32_t* o = rl + (size_t)i * K;
-  if (head0) o[__popc(hb0 & below)] = ((uint32_t)ci[0] << 16) | m0;
-  if (head1) o[__popc(hb0) + __popc(hb1 & below)] = ((uint32_t)ci[1] << 16) | m1;
-  const int nent = __popc(hb0) + __popc(hb1);
+  int nent = 0, before = 0;
+  for (;;) {
+    const int c = __reduce_min_sync(0xffffffffu, min(ci[0], ci[1]));
+    if (c == NONE) break;
+    const unsigned m = __reduce_or_sync(0xffffffffu, (ci[0] == c ? bit[0] : 0u) | (ci[1] == c ? bit[1] : 0u));
+    if (lane == 0) o[nent] = ((uint32_t)c << 16) | m;
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+      if (ci[u] == c) {
+        if (slots) slots[(size_t)i * K + before + __popc(m & (bit[u] - 1u))] = lane + 32 * u;
+        ci[u] = NONE;
+      }
+    ++nent;
+    before += __popc(m);
+  }
   if (lane == 0 && nent < K) o[nent] = 0xffff0000u;
 }
 
@@ -777,9 +741,34 @@ __global__ void tc_rowtile_kernel(int ntiles, const int* __restrict__ tstart, in
   const int a = tstart[t], b = tstart[t + 1];
   for (int r = a + threadIdx.x; r < b; r += blockDim.x) rtile[r] = t;
 }
+// tile-skip mask: bit kb of tile t set iff a row of t has a key in chunk kb.
+// vec (K % 4 == 0, 16-byte aligned table): four slots of one row per thread
+// (one 16-byte load), bits of the same mask word OR-ed before the atomic.
 __global__ void tc_mask_kernel(int N, int K, const int32_t* __restrict__ nbr, const int* __restrict__ rtile,
-                               int words, uint32_t* __restrict__ mask) {
+                               int words, uint32_t* __restrict__ mask, bool vec) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    if (t * 4 >= (size_t)N * K) return;
+    const int4 jv = __ldg(reinterpret_cast<const int4*>(nbr) + t);
+    const int js[4] = {jv.x, jv.y, jv.z, jv.w};
+    if (js[0] < 0 && js[1] < 0 && js[2] < 0 && js[3] < 0) return;
+    uint32_t* row = mask + (size_t)rtile[t * 4 / K] * words;
+    int w = -1;
+    uint32_t acc = 0u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (js[e] < 0) continue;
+      const int kb = js[e] / KC;
+      if (kb / 32 != w) {
+        if (acc) atomicOr(row + w, acc);
+        w = kb / 32;
+        acc = 0u;
+      }
+      acc |= 1u << (kb % 32);
+    }
+    if (acc) atomicOr(row + w, acc);
+    return;
+  }
   if (t >= (size_t)N * K) return;
   const int j = nbr[t];
   if (j < 0) return;
@@ -952,7 +941,9 @@ es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const 
   cudaMemsetAsync(cnt, 0, (size_t)(ntiles + 1) * 4, st);
   {
     const size_t n = (size_t)a.N * a.K;
-    tc_mask_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, pp.rtile, words, mask);
+    const bool vec = (a.K & 3) == 0 && ((uintptr_t)nbr & 15) == 0;
+    const size_t nt = vec ? n / 4 : n;
+    tc_mask_kernel<<<(unsigned)((nt + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, pp.rtile, words, mask, vec);
   }
   tc_count_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cnt);
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
