@@ -337,29 +337,66 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
 // Counting-sort transpose (no radix sort of the N*K slots): count the
 // pairs per key, exclusive-scan into rev_ptr, scatter each pair to its key's
 // segment with an atomic cursor, then restore the stable order (ascending
-// pair index i*K + s) with a per-key insertion sort -- segments hold the
-// ~15-55 queries of one key, so the sort is a few hundred register ops.
-__global__ void tr_count_kernel(int N, int K, const int32_t* __restrict__ nbr, int* __restrict__ cnt) {
+// pair index i*K + s) per key -- segments hold the ~15-55 queries of one
+// key, ranked by a warp in registers.
+// vec: K % 4 == 0 and a 16-byte aligned table -> four slots per thread
+__device__ __forceinline__ int tr_load4(const int32_t* __restrict__ nbr, size_t t, size_t n, bool vec, int (&js)[4]) {
+  if (vec) {
+    if (t * 4 >= n) return 0;
+    const int4 v = __ldg(reinterpret_cast<const int4*>(nbr) + t);
+    js[0] = v.x; js[1] = v.y; js[2] = v.z; js[3] = v.w;
+    return 4;
+  }
+  if (t >= n) return 0;
+  js[0] = nbr[t];
+  return 1;
+}
+
+__global__ void tr_count_kernel(int N, int K, const int32_t* __restrict__ nbr, int* __restrict__ cnt, bool vec) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (size_t)N * K) return;
-  const int j = nbr[t];
-  if (j >= 0) atomicAdd(&cnt[j], 1);
+  int js[4];
+  const int m = tr_load4(nbr, t, (size_t)N * K, vec, js);
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (e < m && js[e] >= 0) atomicAdd(&cnt[js[e]], 1);
 }
 
 __global__ void tr_fill_kernel(int N, int K, const int32_t* __restrict__ nbr, const int* __restrict__ rev_ptr,
-                               int* __restrict__ cursor, int32_t* __restrict__ rev_pair) {
+                               int* __restrict__ cursor, int32_t* __restrict__ rev_pair, bool vec) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (size_t)N * K) return;
-  const int j = nbr[t];
-  if (j < 0) return;
-  rev_pair[rev_ptr[j] + atomicAdd(&cursor[j], 1)] = (int32_t)t;
+  int js[4];
+  const int m = tr_load4(nbr, t, (size_t)N * K, vec, js);
+  const size_t t0 = vec ? t * 4 : t;
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (e < m && js[e] >= 0) rev_pair[rev_ptr[js[e]] + atomicAdd(&cursor[js[e]], 1)] = (int32_t)(t0 + e);
 }
 
+// Restore ascending pair order per key: warp per key, each lane ranks its
+// (<= 2) entries against the segment's by shuffles and stores them at their
+// rank (pair indices are unique); segments over 64 pairs: lane 0 insertion sort.
 __global__ void tr_sort_kernel(int Nk, const int* __restrict__ rev_ptr, int32_t* __restrict__ rev_pair) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (j >= Nk) return;
-  const int b = rev_ptr[j], e = rev_ptr[j + 1];
-  for (int x = b + 1; x < e; ++x) {
+  const int b = rev_ptr[j], n = rev_ptr[j + 1] - b;
+  if (n <= 1) return;
+  if (n <= 64) {
+    constexpr int32_t BIG = 0x7fffffff;
+    const int32_t v0 = lane < n ? rev_pair[b + lane] : BIG;
+    const int32_t v1 = lane + 32 < n ? rev_pair[b + 32 + lane] : BIG;
+    int r0 = 0, r1 = 0;
+    for (int x = 0; x < n; ++x) {
+      const int32_t w = __shfl_sync(0xffffffffu, x < 32 ? v0 : v1, x & 31);
+      r0 += w < v0 ? 1 : 0;
+      r1 += w < v1 ? 1 : 0;
+    }
+    if (lane < n) rev_pair[b + r0] = v0;
+    if (lane + 32 < n) rev_pair[b + r1] = v1;
+    return;
+  }
+  if (lane != 0) return;
+  for (int x = b + 1; x < b + n; ++x) {
     const int32_t v = rev_pair[x];
     int y = x;
     while (y > b && rev_pair[y - 1] > v) {
@@ -404,15 +441,17 @@ es_status nbr_transpose_launch(int N, int K, int Nk, const int32_t* nbr, int32_t
   int* cnt = (int*)(base + w.cnt);
   int* cursor = (int*)(base + w.cursor);
   const size_t n = (size_t)N * K;
-  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const bool vec = (K & 3) == 0 && ((uintptr_t)nbr & 15) == 0;
+  const size_t nt = vec ? n / 4 : n;
+  const unsigned blocks = (unsigned)((nt + 255) / 256);
   cudaMemsetAsync(cnt, 0, sizeof(int) * (Nk + 1), st);
   cudaMemsetAsync(cursor, 0, sizeof(int) * (Nk + 1), st);
-  tr_count_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, cnt);
+  tr_count_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, cnt, vec);
   size_t cb = w.cub_scan;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(base + w.cub, cb, cnt, (int*)rev_ptr, Nk + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "neighbors_transpose: scan");
-  tr_fill_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, rev_ptr, cursor, rev_pair);
-  tr_sort_kernel<<<(Nk + 127) / 128, 128, 0, st>>>(Nk, rev_ptr, rev_pair);
+  tr_fill_kernel<<<blocks, 256, 0, st>>>(N, K, nbr, rev_ptr, cursor, rev_pair, vec);
+  tr_sort_kernel<<<(unsigned)(((size_t)Nk * 32 + 255) / 256), 256, 0, st>>>(Nk, rev_ptr, rev_pair);
   return cuda_status(cudaGetLastError(), "neighbors_transpose");
 }
 

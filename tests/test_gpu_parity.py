@@ -91,6 +91,30 @@ def test_transpose_and_tile_mask(es, oracle):
     np.testing.assert_array_equal(mask, exp)
 
 
+@pytest.mark.parametrize("K", [4, 6])
+def test_transpose_hub_keys(es, K):
+    """Keys with in-degree > 64 (the per-key rank sort's fallback), K % 4 != 0
+    (scalar count / fill path), sentinels mixed in."""
+    rng = np.random.default_rng(K)
+    N = 300
+    nbr = rng.integers(0, N, size=(N, K)).astype(np.int32)
+    nbr[:, 0] = 0                      # every row points at key 0 (in-degree 300)
+    nbr[::3, 1] = 7                    # key 7: in-degree 100
+    nbr[rng.random((N, K)) < 0.2] = -1
+    for i in range(N):                 # unique keys per row, as a neighbour table has
+        seen = set()
+        for s_ in range(K):
+            if nbr[i, s_] in seen:
+                nbr[i, s_] = -1
+            elif nbr[i, s_] >= 0:
+                seen.add(int(nbr[i, s_]))
+    rev_ptr, rev_pair = es.neighbors_transpose(dev(nbr))
+    rev_ptr, rev_pair = rev_ptr.cpu().numpy(), rev_pair.cpu().numpy()
+    for j in range(N):
+        exp = np.sort(np.nonzero(nbr.ravel() == j)[0])
+        np.testing.assert_array_equal(rev_pair[rev_ptr[j]:rev_ptr[j + 1]], exp)
+
+
 # ------------------------------------------------------------------ projections
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("L,C", [(2, 64), (4, 32), (1, 128)])
