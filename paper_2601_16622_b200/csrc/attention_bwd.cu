@@ -6,25 +6,31 @@ namespace es {
 namespace {
 
 // ------------------------------------------------------------------ backward
-// Delta_i^h = sum_{rows, head channels} dout * out.  C/2 threads per atom,
-// two channels each (same head), shuffle-reduced over the C_h/2 lanes of a head.
-template <typename T>
+// Delta_i^h = sum_{rows, head channels} dout * out.  C/V threads per atom,
+// V channels each (same head; V = 8: 16-byte loads of bf16), shuffle-reduced
+// over the C_h/V lanes of a head.
+template <typename T, int V>
 __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, int H, const T* __restrict__ out,
                                                          const T* __restrict__ dout, float* __restrict__ delta) {
-  const int tpa = C / 2;
+  const int tpa = C / V;
   const int i = blockIdx.x * (blockDim.x / tpa) + threadIdx.x / tpa;
   const int t = threadIdx.x % tpa;
   if (i >= N) return;
-  float acc = 0.f;
+  float acc[V];
+#pragma unroll
+  for (int c = 0; c < V; ++c) acc[c] = 0.f;
   for (int mm = 0; mm < M; ++mm) {
-    float a[2], b[2];
-    ldvec<2>(out + ((size_t)i * M + mm) * C + 2 * t, a);
-    ldvec<2>(dout + ((size_t)i * M + mm) * C + 2 * t, b);
-    acc = fmaf(a[0], b[0], fmaf(a[1], b[1], acc));
+    float a[V], b[V];
+    ldvec<V>(out + ((size_t)i * M + mm) * C + V * t, a);
+    ldvec<V>(dout + ((size_t)i * M + mm) * C + V * t, b);
+    fmav<V>(a, b, acc);
   }
-  const int g = (C / H) / 2;  // threads per head (power of two <= 32)
-  for (int o = g >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (t % g == 0) delta[(size_t)i * H + (2 * t) / (C / H)] = acc;
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < V; ++c) s += acc[c];
+  const int g = (C / H) / V;  // threads per head (power of two <= 32)
+  for (int o = g >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (t % g == 0) delta[(size_t)i * H + (V * t) / (C / H)] = s;
 }
 
 // Key-centric pass: CTA per key atom j over the transposed relation; yields
@@ -317,10 +323,15 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
                   double* dpos, bool skip_dq, cudaStream_t st) {
   constexpr int M = Lay<L>::M;
   if (dpos && L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
-  {
+  const int g8 = (kp.C / kp.H) / 8;
+  if ((kp.C / kp.H) % 8 == 0 && (g8 & (g8 - 1)) == 0) {
+    const int apb = 256 / (kp.C / 8);
+    attn_delta_kernel<T, 8><<<(kp.N + apb - 1) / apb, apb * (kp.C / 8), 0, st>>>(kp.N, M, kp.C, kp.H, (const T*)out,
+                                                                                 (const T*)dout, delta);
+  } else {
     const int apb = 256 / (kp.C / 2);
-    attn_delta_kernel<T><<<(kp.N + apb - 1) / apb, apb * (kp.C / 2), 0, st>>>(kp.N, M, kp.C, kp.H, (const T*)out,
-                                                                              (const T*)dout, delta);
+    attn_delta_kernel<T, 2><<<(kp.N + apb - 1) / apb, apb * (kp.C / 2), 0, st>>>(kp.N, M, kp.C, kp.H, (const T*)out,
+                                                                                 (const T*)dout, delta);
   }
   es_status s = cuda_status(cudaGetLastError(), "attn_delta_kernel");
   if (s != ES_OK) return s;
