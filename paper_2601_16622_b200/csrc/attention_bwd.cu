@@ -112,6 +112,9 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
       const float* rec = recs + e * REC;
       const int i = __float_as_int(rec[LY::OFF_J]);
       const int pr = __float_as_int(rec[LY::OFF_X]);
+      // packed FFMA2 forms only for even CPL: with CPL = 1 (L = 4) the
+      // register pairing they impose costs spills
+      constexpr bool PK = CPL % 2 == 0;
       float qv[M][2 * CPL];
       float sc[2 * CPL];
 #pragma unroll
@@ -122,7 +125,12 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
         float kr[2 * CPL];
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) kr[c] = ks[(mm * nthr + threadIdx.x) * 2 * CPL + c];
-        fmav<2 * CPL>(qv[mm], kr, sc);
+        if constexpr (PK) {
+          fmav<2 * CPL>(qv[mm], kr, sc);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2 * CPL; ++c) sc[0] = fmaf(qv[mm][c], kr[c], sc[0]);
+        }
       }
       float s = 0.f;
 #pragma unroll
@@ -220,7 +228,14 @@ __global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_b
       }
       const float tds = p.tau * ds;
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm) fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
+      for (int mm = 0; mm < M; ++mm) {
+        if constexpr (PK) {
+          fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+        }
+      }
       if ((lane % lph) == 0) dsbuf[(size_t)pr * PH + head] = ds;
     }
   }

@@ -375,11 +375,86 @@ __device__ __forceinline__ void fmav(const float (&x)[CPL], const float (&y)[CPL
   if constexpr (CPL & 1) acc[CPL - 1] = fmaf(x[CPL - 1], y[CPL - 1], acc[CPL - 1]);
 }
 
+// Odd channel counts per thread (CPL = 1: the L = 4 kernels): the scalar
+// form, whose register allocation the packed form would disturb.
+template <int L, int CPL, bool ADJ>
+__device__ __forceinline__ void eaas_apply_scalar(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
+                                           float (&acc)[Lay<L>::M][CPL]) {
+  constexpr int M = Lay<L>::M;
+  float vt[M][CPL];
+  // align: vt^l = D^l v^l
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) vt[0][c] = v[0][c];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    const float* D = rec + Lay<L>::doff(l);
+    const int d = 2 * l + 1;
+#pragma unroll
+    for (int m = 0; m < d; ++m)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        float t = 0.f;
+#pragma unroll
+        for (int mp = 0; mp < d; ++mp) t = fmaf(D[m * d + mp], v[l * l + mp][c], t);
+        vt[l * l + m][c] = t;
+      }
+  }
+  // sparse re-index in the aligned frame (forward P or adjoint P^T)
+  float w[M][CPL];
+#pragma unroll
+  for (int t = 0; t < M; ++t)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) w[t][c] = 0.f;
+#pragma unroll
+  for (int lo = 0; lo <= L; ++lo)
+#pragma unroll
+    for (int li = 0; li <= L; ++li) {
+      const int mm = cmin(lo, li);
+#pragma unroll
+      for (int m = -mm; m <= mm; ++m) {
+        const int e = Lay<L>::eoff(lo, li) + m + mm;
+        const float a = rec[Lay<L>::OFF_AB + 2 * e];
+        const float b = rec[Lay<L>::OFF_AB + 2 * e + 1];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          if constexpr (!ADJ) {
+            w[lo * lo + lo + m][c] = fmaf(a, vt[li * li + li + m][c], w[lo * lo + lo + m][c]);
+            if (m != 0) w[lo * lo + lo + m][c] = fmaf(b, vt[li * li + li - m][c], w[lo * lo + lo + m][c]);
+          } else {
+            w[li * li + li + m][c] = fmaf(a, vt[lo * lo + lo + m][c], w[li * li + li + m][c]);
+            if (m != 0) w[li * li + li - m][c] = fmaf(b, vt[lo * lo + lo + m][c], w[li * li + li - m][c]);
+          }
+        }
+      }
+    }
+  // un-align and accumulate: acc^l += s * D^l^T w^l
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[0][c] = fmaf(s, w[0][c], acc[0][c]);
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    const float* D = rec + Lay<L>::doff(l);
+    const int d = 2 * l + 1;
+#pragma unroll
+    for (int m = 0; m < d; ++m)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        float t = 0.f;
+#pragma unroll
+        for (int mp = 0; mp < d; ++mp) t = fmaf(D[mp * d + m], w[l * l + mp][c], t);
+        acc[l * l + m][c] = fmaf(s, t, acc[l * l + m][c]);
+      }
+  }
+}
+
 // x += s * (D^T P D) v  per channel (EAAS forward value operator), or the
 // adjoint y += s * (D^T P^T D) g when ADJ.  v: [M][CPL] registers.
 template <int L, int CPL, bool ADJ>
 __device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
                                            float (&acc)[Lay<L>::M][CPL]) {
+  if constexpr (CPL % 2 == 1) {
+    eaas_apply_scalar<L, CPL, ADJ>(rec, v, s, acc);
+    return;
+  }
   constexpr int M = Lay<L>::M;
   float vt[M][CPL];
   // align: vt^l = D^l v^l
