@@ -43,7 +43,7 @@ def _compile(src: str, verbose: bool) -> str:
     deps.append(os.path.join(INCLUDE, "equistream_b200.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *os.environ.get("ES_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
     if verbose or os.environ.get("ES_PTXAS_V"):
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

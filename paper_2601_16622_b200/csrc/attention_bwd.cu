@@ -41,8 +41,14 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 //   dL/dr_ij = sum_h P_ij^h [phi'(r) r^ sum_f Y^f(r) D_f^h + phi sum_f grad Y^f(r) D_f^h],
 //   D_f^h = dO_i^h . (G_f v_j)^h   (the value map x = phi sum_f Y^f G_f v, == EAAS),
 // scattered to dpos_j (+) and dpos_i (-) with fp64 atomics.
+// CTAs per SM the C=128 specialisation (64 threads) is compiled for (register cap)
+#ifndef ES_BWD_MINB
+#define ES_BWD_MINB 0
+#endif
 template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0, bool FORCE = false>
-__global__ void __launch_bounds__((L <= 2 ? 192 : 256), (L <= 2 ? 2 : 1)) attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 : (L <= 2 ? 192 : 256)),
+                                  (ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? ES_BWD_MINB : (L <= 2 ? 2 : 1)))
+    attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
                                                           const int* __restrict__ rev_pair,
