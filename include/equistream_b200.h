@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 6
+#define ES_ABI_VERSION 7
 
 typedef enum {
   ES_OK = 0,
@@ -62,6 +62,11 @@ typedef enum {
   ES_VALUE_EAAS = 1   /* value = phi(r_ij) * sum_paths (v_j (x) R^lf(r_ij))^lo via per-pair EAAS
                          (north star; == edge_centric_message SPEC.md:342-350) */
 } es_value_mode;
+
+typedef enum {
+  ES_BIAS_NONE = 0,  /* b == 0 */
+  ES_BIAS_POLY2 = 1  /* b(r) = bias[0] + bias[1] r + bias[2] r^2 */
+} es_bias_mode;
 
 typedef enum {
   ES_PHI_COSINE = 0, /* phi = (cos(pi r / r_cut) + 1) / 2 for r < r_cut */
@@ -88,6 +93,12 @@ typedef struct {
    * dout, dq and nbr hold the N local rows, k, v, pos, dk and dv all Nk atoms
    * (nbr entries index [0, Nk)).  Nk = 0 means Nk = N, row0 = 0. */
   int32_t row0, Nk;
+  /* Radial score bias b(r_ij) of s_ij = tau q_i.k_j + b(r_ij) (RadialScalars,
+   * SPEC.md:247-250, Eq. 18): the SPEC's callable as an enum + parameters.
+   * ES_BIAS_NONE: b == 0 (the default); ES_BIAS_POLY2:
+   * b(r) = bias[0] + bias[1] r + bias[2] r^2. */
+  int32_t bias_mode;
+  double bias[3];
 } es_attn_desc;
 
 /* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in
@@ -140,6 +151,10 @@ typedef struct {
   int32_t periodic;
   double r_cut;
   double box[3];
+  /* Row range (query-row sharding, SURVEY 8 e): only atoms row0 .. row0 +
+   * nrows - 1 are searched (against all N atoms); nbr, dist and count then
+   * hold nrows rows.  nrows = 0 means all N rows (row0 must be 0). */
+  int32_t row0, nrows;
 } es_nbr_desc;
 size_t es_neighbors_workspace_size(const es_nbr_desc* d);
 es_status es_neighbors_build(const es_nbr_desc* d, const double* pos, const int32_t* seg_ptr, int32_t* nbr,

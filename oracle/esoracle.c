@@ -329,6 +329,60 @@ int eso_wigner_d(int l, const double* R, double* D) {
   return st;
 }
 
+/* The same least-squares D in closed form for the per-pair hot loops of
+ * the CPU baseline: D = Z Y^T (Y Y^T)^-1 with the fixed-point factor
+ * Pinv = Y^T (Y Y^T)^-1 ([np][d]) computed once per l. */
+static double* g_pinv[ESO_LT];
+static void pinv_init(void) {
+#pragma omp critical(eso_pinv_cache)
+  if (!g_pinv[ESO_LT - 1]) {
+    for (int l = 0; l < ESO_LT; ++l) {
+      const int d = 2 * l + 1, np = 4 * d;
+      double* P = (double*)malloc(sizeof(double) * np * d);
+      double* Y = (double*)malloc(sizeof(double) * d * np);
+      double* A = (double*)malloc(sizeof(double) * d * d);
+      double* Bt = (double*)malloc(sizeof(double) * d * np); /* (Y Y^T)^-1 Y  -> [d][np] */
+      double tmp[2 * ESO_MAXL + 1];
+      const double ga = ESO_PI * (3.0 - sqrt(5.0));
+      for (int k = 0; k < np; ++k) {
+        const double zz = 1.0 - (2.0 * k + 1.0) / np, rr = sqrt(1.0 - zz * zz);
+        const double p[3] = {rr * cos(ga * k), rr * sin(ga * k), zz};
+        eso_solid_harmonics(l, p, tmp);
+        for (int m = 0; m < d; ++m) Y[m * np + k] = tmp[m];
+      }
+      for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) {
+          double t = 0.0;
+          for (int k = 0; k < np; ++k) t += Y[a * np + k] * Y[b * np + k];
+          A[a * d + b] = t;
+        }
+      memcpy(Bt, Y, sizeof(double) * d * np);
+      solve_inplace(A, Bt, d, np);
+      for (int k = 0; k < np; ++k)
+        for (int m = 0; m < d; ++m) P[k * d + m] = Bt[m * np + k];
+      free(Y); free(A); free(Bt);
+      g_pinv[l] = P;
+    }
+  }
+}
+static void wigner_d_fast(int l, const double* R, double* D) {
+  const int d = 2 * l + 1, np = 4 * d;
+  if (l == 0) { D[0] = 1.0; return; }
+  const double* P = g_pinv[l];
+  const double ga = ESO_PI * (3.0 - sqrt(5.0));
+  double z[2 * ESO_MAXL + 1];
+  for (int a = 0; a < d * d; ++a) D[a] = 0.0;
+  for (int k = 0; k < np; ++k) {
+    const double zz = 1.0 - (2.0 * k + 1.0) / np, rr = sqrt(1.0 - zz * zz);
+    const double p[3] = {rr * cos(ga * k), rr * sin(ga * k), zz};
+    const double q[3] = {R[0] * p[0] + R[1] * p[1] + R[2] * p[2], R[3] * p[0] + R[4] * p[1] + R[5] * p[2],
+                         R[6] * p[0] + R[7] * p[1] + R[8] * p[2]};
+    eso_solid_harmonics(l, q, z);
+    for (int a = 0; a < d; ++a)
+      for (int b = 0; b < d; ++b) D[a * d + b] += z[a] * P[k * d + b];
+  }
+}
+
 /* ------------------------------------------------------------------ */
 /* SPEC eaas (gauge SPEC.md:216): R with R r = |r| e_z */
 /* rotating about (r^ x e_z)/|.| by arccos(r^.e_z); identity / pi about */
@@ -555,22 +609,23 @@ void eso_project_bwd(int N, int L, int C, int Dq, int Cv, const double* h, const
         }
       }
   if (!dW) return;
+  /* dW[l][c][o] = sum_(n, m) h[n][lm][c] g[n][lm][o]: per (l, c) row, outputs innermost (contiguous) */
 #pragma omp parallel for schedule(static)
   for (int lc = 0; lc < (L + 1) * C; ++lc) {
     const int l = lc / C, c = lc % C;
-    for (int o = 0; o < Wc; ++o) {
-      double s = 0.0;
-      for (int n = 0; n < N; ++n)
-        for (int m = 0; m < 2 * l + 1; ++m) {
-          const int mm = l * l + m;
-          double g;
-          if (o < Dq) g = dq[((size_t)n * M + mm) * Dq + o];
-          else if (o < 2 * Dq) g = dk[((size_t)n * M + mm) * Dq + (o - Dq)];
-          else g = dv[((size_t)n * M + mm) * Cv + (o - 2 * Dq)];
-          s += h[((size_t)n * M + mm) * C + c] * g;
-        }
-      dW[((size_t)l * C + c) * Wc + o] = s;
-    }
+    double* row = dW + ((size_t)l * C + c) * Wc;
+    for (int o = 0; o < Wc; ++o) row[o] = 0.0;
+    for (int n = 0; n < N; ++n)
+      for (int m = 0; m < 2 * l + 1; ++m) {
+        const int mm = l * l + m;
+        const double hv = h[((size_t)n * M + mm) * C + c];
+        const double* gq = dq + ((size_t)n * M + mm) * Dq;
+        const double* gk = dk + ((size_t)n * M + mm) * Dq;
+        const double* gv = dv + ((size_t)n * M + mm) * Cv;
+        for (int o = 0; o < Dq; ++o) row[o] += hv * gq[o];
+        for (int o = 0; o < Dq; ++o) row[Dq + o] += hv * gk[o];
+        for (int o = 0; o < Cv; ++o) row[2 * Dq + o] += hv * gv[o];
+      }
   }
 }
 
@@ -603,7 +658,8 @@ static inline double phi_of(const eso_attn_desc* d, double rn) {
  * Mode 2 is EAAS organised the way a CPU implementation
  * would: one alignment rotation and D^l per pair, align each l_i block
  * once, sparse re-index every path, un-align each l_o block once. */
-static void pair_value(const eso_attn_desc* d, const double* v, int j, const double* r, double phi, double* x) {
+static void pair_value(const eso_attn_desc* d, const double* v, int j, const double* r, double phi, double* x,
+                       double* scratch /* [2][M][Cv] */) {
   const int L = d->L, M = (L + 1) * (L + 1), Cv = d->Cv;
   const double* vj = v + (size_t)j * M * Cv;
   if (d->value_mode == 0) {
@@ -613,7 +669,7 @@ static void pair_value(const eso_attn_desc* d, const double* v, int j, const dou
   memset(x, 0, sizeof(double) * M * Cv);
   const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
   if (d->value_mode == 1 || rn <= 1e-8) {
-    double* tmp = (double*)malloc(sizeof(double) * (2 * L + 1) * Cv);
+    double* tmp = scratch;
     double y[2 * ESO_LT + 1];
     for (int li = 0; li <= L; ++li)
       for (int lf = 0; lf <= L; ++lf) {
@@ -625,17 +681,17 @@ static void pair_value(const eso_attn_desc* d, const double* v, int j, const dou
           for (int t = 0; t < (2 * lo + 1) * Cv; ++t) xo[t] += phi * tmp[t];
         }
       }
-    free(tmp);
     return;
   }
   double R[9];
   eso_alignment_rotation(r, R);
-  double* ht = (double*)malloc(sizeof(double) * M * Cv);
-  double* w = (double*)calloc((size_t)M * Cv, sizeof(double));
+  double* ht = scratch;
+  double* w = scratch + (size_t)M * Cv;
+  memset(w, 0, sizeof(double) * M * Cv);
   double D[ESO_LT][(2 * ESO_LT - 1) * (2 * ESO_LT - 1)];
   for (int l = 0; l <= L; ++l) {
     const int dl = 2 * l + 1;
-    eso_wigner_d(l, R, D[l]);
+    wigner_d_fast(l, R, D[l]);
     for (int a = 0; a < dl; ++a)
       for (int c = 0; c < Cv; ++c) {
         double s = 0.0;
@@ -667,7 +723,6 @@ static void pair_value(const eso_attn_desc* d, const double* v, int j, const dou
         x[(size_t)(l * l + a) * Cv + c] = phi * s;
       }
   }
-  free(ht); free(w);
 }
 
 /* stream_aggregate: one pass per atom with (mu, z, A)
@@ -679,9 +734,11 @@ void eso_attn_fwd(const eso_attn_desc* d, const double* q, const double* k, cons
   const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
   const double tau = 1.0 / sqrt((double)M * dqh);
   cg_cache_init();
+  pinv_init();
 #pragma omp parallel
   {
     double* x = (double*)malloc(sizeof(double) * M * Cv);
+    double* scr = (double*)malloc(sizeof(double) * 2 * M * Cv);
     double* A = (double*)malloc(sizeof(double) * M * Cv);
     double* mu = (double*)malloc(sizeof(double) * H);
     double* z = (double*)malloc(sizeof(double) * H);
@@ -703,7 +760,7 @@ void eso_attn_fwd(const eso_attn_desc* d, const double* q, const double* k, cons
               acc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
           s[h] = tau * acc; /* Eq. 18 with b == 0 */
         }
-        pair_value(d, v, j, r, phi_of(d, rn), x);
+        pair_value(d, v, j, r, phi_of(d, rn), x, scr);
         for (int h = 0; h < H; ++h) { /* Eqs. 15-17 */
           const double mu2 = s[h] > mu[h] ? s[h] : mu[h];
           const double sc = exp(mu[h] - mu2), e = exp(s[h] - mu2);
@@ -722,7 +779,7 @@ void eso_attn_fwd(const eso_attn_desc* d, const double* q, const double* k, cons
         if (lse) lse[(size_t)i * H + h] = empty ? -INFINITY : mu[h] + log(z[h]);
       }
     }
-    free(x); free(A); free(mu); free(z); free(s);
+    free(x); free(scr); free(A); free(mu); free(z); free(s);
   }
 }
 
@@ -734,6 +791,7 @@ void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k
   const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
   const double tau = 1.0 / sqrt((double)M * dqh);
   cg_cache_init();
+  pinv_init();
   double* S = (double*)malloc(sizeof(double) * (size_t)N * K * H);
 #pragma omp parallel for schedule(static)
   for (int i = 0; i < N; ++i)
@@ -754,6 +812,7 @@ void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k
 #pragma omp parallel
   {
     double* x = (double*)malloc(sizeof(double) * M * Cv);
+    double* scr = (double*)malloc(sizeof(double) * 2 * M * Cv);
 #pragma omp for schedule(dynamic, 4)
     for (int i = 0; i < N; ++i) {
       double* o = out + (size_t)i * M * Cv;
@@ -772,7 +831,7 @@ void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k
         double r[3];
         pair_vec(pos, i, j, d->box, r);
         const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-        pair_value(d, v, j, r, phi_of(d, rn), x);
+        pair_value(d, v, j, r, phi_of(d, rn), x, scr);
         for (int h = 0; h < H; ++h) {
           const double a = S[((size_t)i * K + kk) * H + h];
           for (int mm = 0; mm < M; ++mm)
@@ -780,7 +839,7 @@ void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k
         }
       }
     }
-    free(x);
+    free(x); free(scr);
   }
   free(S);
 }
@@ -811,7 +870,12 @@ static void pair_T(const eso_attn_desc* d, const double* r, double phi, double* 
 }
 
 /* stream_aggregate_backward: gradients of
- * sum <dout, out> w.r.t. q, k, v by recomputation from (q,k,v,lse). */
+ * sum <dout, out> w.r.t. q, k, v by recomputation from (q,k,v,lse).
+ * Two race-free parallel phases, the GPU's split: (1) query-centric over i:
+ * Delta_i, per-pair p and ds = p (dout_i . x_ij - Delta_i), dq_i; (2)
+ * key-centric over j through the transposed relation (pairs of key j in
+ * ascending (i, slot) order, so sums are deterministic): dv_j += p T^T dout_i,
+ * dk_j += tau ds q_i.  Only O(N K H) scalars are kept between the phases. */
 void eso_attn_bwd(const eso_attn_desc* d, const double* q, const double* k, const double* v, const double* pos,
                   const int* nbr, const double* out, const double* lse, const double* dout, double* dq, double* dk,
                   double* dv) {
@@ -819,57 +883,99 @@ void eso_attn_bwd(const eso_attn_desc* d, const double* q, const double* k, cons
   const int Dq = d->Dq, Cv = d->Cv, dqh = Dq / H, cvh = Cv / H;
   const double tau = 1.0 / sqrt((double)M * dqh);
   cg_cache_init();
-  memset(dq, 0, sizeof(double) * (size_t)N * M * Dq);
-  memset(dk, 0, sizeof(double) * (size_t)N * M * Dq);
-  memset(dv, 0, sizeof(double) * (size_t)N * M * Cv);
-  /* serial over i (scatter onto j), parallel inside would race: keep simple */
-  double* T = (double*)malloc(sizeof(double) * M * M);
-  double* Delta = (double*)malloc(sizeof(double) * H);
-  double* y = (double*)malloc(sizeof(double) * M * Cv);
-  for (int i = 0; i < N; ++i) {
-    for (int h = 0; h < H; ++h) {
-      double s = 0.0;
-      for (int mm = 0; mm < M; ++mm)
-        for (int c = h * cvh; c < (h + 1) * cvh; ++c)
-          s += dout[((size_t)i * M + mm) * Cv + c] * out[((size_t)i * M + mm) * Cv + c];
-      Delta[h] = s;
-    }
-    for (int kk = 0; kk < K; ++kk) {
-      const int j = nbr[(size_t)i * K + kk];
-      if (j < 0) continue;
-      double r[3];
-      pair_vec(pos, i, j, d->box, r);
-      const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
-      pair_T(d, r, phi_of(d, rn), T);
-      /* y = T^T dout_i  [M][Cv] */
-      for (int a = 0; a < M; ++a)
-        for (int c = 0; c < Cv; ++c) {
-          double s = 0.0;
-          for (int o = 0; o < M; ++o) s += T[o * M + a] * dout[((size_t)i * M + o) * Cv + c];
-          y[a * Cv + c] = s;
-        }
+  double* P = (double*)malloc(sizeof(double) * ((size_t)N * K * H + 1));
+  double* DS = (double*)malloc(sizeof(double) * ((size_t)N * K * H + 1));
+  int* rptr = (int*)calloc((size_t)N + 2, sizeof(int));
+  int* rpair = (int*)malloc(sizeof(int) * ((size_t)N * K + 1));
+#pragma omp parallel
+  {
+    double* T = (double*)malloc(sizeof(double) * M * M);
+    double* y = (double*)malloc(sizeof(double) * M * Cv);
+    double* Delta = (double*)malloc(sizeof(double) * H);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < N; ++i) {
+      double* dqi = dq + (size_t)i * M * Dq;
+      memset(dqi, 0, sizeof(double) * M * Dq);
       for (int h = 0; h < H; ++h) {
-        double sc = 0.0;
+        double s = 0.0;
         for (int mm = 0; mm < M; ++mm)
-          for (int c = h * dqh; c < (h + 1) * dqh; ++c)
-            sc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
-        const double p = exp(tau * sc - lse[(size_t)i * H + h]);
-        double dp = 0.0;
-        for (int mm = 0; mm < M; ++mm)
-          for (int c = h * cvh; c < (h + 1) * cvh; ++c) {
-            dp += y[mm * Cv + c] * v[((size_t)j * M + mm) * Cv + c];
-            dv[((size_t)j * M + mm) * Cv + c] += p * y[mm * Cv + c];
+          for (int c = h * cvh; c < (h + 1) * cvh; ++c)
+            s += dout[((size_t)i * M + mm) * Cv + c] * out[((size_t)i * M + mm) * Cv + c];
+        Delta[h] = s;
+      }
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = nbr[(size_t)i * K + kk];
+        if (j < 0) continue;
+        double r[3];
+        pair_vec(pos, i, j, d->box, r);
+        const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        pair_T(d, r, phi_of(d, rn), T);
+        for (int a = 0; a < M; ++a) /* y = T^T dout_i  [M][Cv] */
+          for (int c = 0; c < Cv; ++c) {
+            double s = 0.0;
+            for (int o = 0; o < M; ++o) s += T[o * M + a] * dout[((size_t)i * M + o) * Cv + c];
+            y[a * Cv + c] = s;
           }
-        const double ds = p * (dp - Delta[h]);
-        for (int mm = 0; mm < M; ++mm)
-          for (int c = h * dqh; c < (h + 1) * dqh; ++c) {
-            dq[((size_t)i * M + mm) * Dq + c] += tau * ds * k[((size_t)j * M + mm) * Dq + c];
-            dk[((size_t)j * M + mm) * Dq + c] += tau * ds * q[((size_t)i * M + mm) * Dq + c];
-          }
+        for (int h = 0; h < H; ++h) {
+          double sc = 0.0;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+              sc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
+          const double p = exp(tau * sc - lse[(size_t)i * H + h]);
+          double dp = 0.0;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * cvh; c < (h + 1) * cvh; ++c) dp += y[mm * Cv + c] * v[((size_t)j * M + mm) * Cv + c];
+          const double ds = p * (dp - Delta[h]);
+          P[((size_t)i * K + kk) * H + h] = p;
+          DS[((size_t)i * K + kk) * H + h] = ds;
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+              dqi[mm * Dq + c] += tau * ds * k[((size_t)j * M + mm) * Dq + c];
+        }
       }
     }
+#pragma omp single
+    { /* transposed relation (counting sort; ascending pair index per key) */
+      for (size_t e = 0; e < (size_t)N * K; ++e)
+        if (nbr[e] >= 0) rptr[nbr[e] + 1]++;
+      for (int j = 0; j < N; ++j) rptr[j + 1] += rptr[j];
+      int* cur = (int*)malloc(sizeof(int) * ((size_t)N + 1));
+      memcpy(cur, rptr, sizeof(int) * ((size_t)N + 1));
+      for (size_t e = 0; e < (size_t)N * K; ++e)
+        if (nbr[e] >= 0) rpair[cur[nbr[e]]++] = (int)e;
+      free(cur);
+    }
+#pragma omp for schedule(dynamic, 4)
+    for (int j = 0; j < N; ++j) {
+      double* dkj = dk + (size_t)j * M * Dq;
+      double* dvj = dv + (size_t)j * M * Cv;
+      memset(dkj, 0, sizeof(double) * M * Dq);
+      memset(dvj, 0, sizeof(double) * M * Cv);
+      for (int e = rptr[j]; e < rptr[j + 1]; ++e) {
+        const int pe = rpair[e], i = pe / K;
+        double r[3];
+        pair_vec(pos, i, j, d->box, r);
+        const double rn = sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]);
+        pair_T(d, r, phi_of(d, rn), T);
+        for (int a = 0; a < M; ++a)
+          for (int c = 0; c < Cv; ++c) {
+            double s = 0.0;
+            for (int o = 0; o < M; ++o) s += T[o * M + a] * dout[((size_t)i * M + o) * Cv + c];
+            y[a * Cv + c] = s;
+          }
+        for (int h = 0; h < H; ++h) {
+          const double p = P[(size_t)pe * H + h], ds = DS[(size_t)pe * H + h];
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * cvh; c < (h + 1) * cvh; ++c) dvj[mm * Cv + c] += p * y[mm * Cv + c];
+          for (int mm = 0; mm < M; ++mm)
+            for (int c = h * dqh; c < (h + 1) * dqh; ++c)
+              dkj[mm * Dq + c] += tau * ds * q[((size_t)i * M + mm) * Dq + c];
+        }
+      }
+    }
+    free(T); free(y); free(Delta);
   }
-  free(T); free(Delta); free(y);
+  free(P); free(DS); free(rptr); free(rpair);
 }
 
 /* Per-pair operator for tests (exposes pair_T). */

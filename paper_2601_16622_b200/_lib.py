@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libequistream_b200.so")
 ES_OK, ES_INVALID_ARGUMENT, ES_UNSUPPORTED, ES_CUDA_ERROR, ES_NCCL_ERROR = range(5)
 ES_F32, ES_BF16 = 0, 1
 ES_VALUE_PLAIN, ES_VALUE_EAAS = 0, 1
+ES_BIAS_NONE, ES_BIAS_POLY2 = 0, 1
 ES_PHI_COSINE, ES_PHI_ONE = 0, 1
 
 
@@ -21,12 +22,15 @@ class AttnDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("H", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32),
                 ("value_mode", ct.c_int32), ("phi_mode", ct.c_int32), ("dtype", ct.c_int32),
                 ("r_cut", ct.c_double), ("periodic", ct.c_int32), ("box", ct.c_double * 3),
-                ("row0", ct.c_int32), ("Nk", ct.c_int32)]
+                ("row0", ct.c_int32), ("Nk", ct.c_int32), ("bias_mode", ct.c_int32), ("bias", ct.c_double * 3)]
+
+
+ABI_VERSION = 7  # include/equistream_b200.h ES_ABI_VERSION
 
 
 class NbrDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("nseg", ct.c_int32), ("periodic", ct.c_int32),
-                ("r_cut", ct.c_double), ("box", ct.c_double * 3)]
+                ("r_cut", ct.c_double), ("box", ct.c_double * 3), ("row0", ct.c_int32), ("nrows", ct.c_int32)]
 
 
 class ProjDesc(ct.Structure):
@@ -87,7 +91,7 @@ def lib() -> ct.CDLL:
         L.es_cg_real.argtypes = [i32] * 6
         L.es_reindex_table.argtypes = [i32, i32, i32, i32, dp, dp]
         L.es_wigner_d_host.argtypes = [i32, dp, dp]
-        if L.es_abi_version() != 6:
+        if L.es_abi_version() != ABI_VERSION:
             raise EsError("libequistream_b200.so ABI mismatch: rebuild (python -m paper_2601_16622_b200.build)")
         _lib = L
     return _lib

@@ -44,8 +44,36 @@ def _need(t: torch.Tensor, name: str, dtype=None, shape=None) -> torch.Tensor:
     return t
 
 
+def aligned_positions(pos: torch.Tensor) -> torch.Tensor:
+    """pos, or a 16-byte-aligned copy of it (a view such as pos[a0:a1] with
+    odd a0 is only 8-byte aligned; es_attn_fwd requires 16)."""
+    return pos if pos.data_ptr() % 16 == 0 and pos.is_contiguous() else pos.contiguous().clone()
+
+
 def _workspace(nbytes: int, device) -> torch.Tensor:
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def wigner_d(l: int, R) -> "np.ndarray":
+    """D^l(R) [(2l+1)][(2l+1)] acting on value vectors (solid(l, R r) =
+    D solid(l, r)), from the library's host tables (es_wigner_d_host)."""
+    import numpy as np
+    Rm = np.ascontiguousarray(np.asarray(R, dtype=np.float64).reshape(9))
+    D = np.zeros((2 * l + 1) ** 2)
+    check(lib().es_wigner_d_host(int(l), Rm.ctypes.data_as(ct.POINTER(ct.c_double)),
+                                 D.ctypes.data_as(ct.POINTER(ct.c_double))), "es_wigner_d_host")
+    return D.reshape(2 * l + 1, 2 * l + 1)
+
+
+def rotate_features(x: torch.Tensor, L: int, R) -> torch.Tensor:
+    """rotate_feature (irreps.hpp:104-112) for the [N][M][C] layout: every
+    degree block's value vectors v -> D^l(R) v."""
+    out = torch.empty_like(x)
+    for l in range(L + 1):
+        D = torch.tensor(wigner_d(l, R), dtype=torch.float32, device=x.device)
+        blk = x[:, l * l:(l + 1) ** 2, :].float()
+        out[:, l * l:(l + 1) ** 2, :] = torch.einsum("ab,nbc->nac", D, blk).to(x.dtype)
+    return out
 
 
 def conventions_manifest() -> str:
@@ -100,10 +128,12 @@ class NeighborIndex:
 
 
 def build_neighbors(pos: torch.Tensor, K: int, r_cut: float, seg_ptr: torch.Tensor | None = None,
-                    box=None, with_distances: bool = True) -> NeighborIndex:
+                    box=None, with_distances: bool = True, rows: tuple[int, int] | None = None) -> NeighborIndex:
     """build_neighbors: K nearest j != i with |r_ij| < r_cut,
     inside the atom's segment (molecule batch) and under the minimum image
-    when `box` is given.  Bit-identical to the CPU oracle."""
+    when `box` is given.  Bit-identical to the CPU oracle.  rows=(a0, a1):
+    only query rows a0..a1-1 (a row shard; keys are all atoms) -- the
+    returned index holds a1 - a0 rows with global key ids."""
     pos = _need(pos, "pos", torch.float64)
     if pos.dim() != 2 or pos.shape[1] != 3:
         raise EsInvalidArgument("pos: expected [N, 3]")
@@ -121,14 +151,23 @@ def build_neighbors(pos: torch.Tensor, K: int, r_cut: float, seg_ptr: torch.Tens
     if box is not None:
         for a in range(3):
             d.box[a] = float(box[a])
-    nbr = torch.empty((N, K), dtype=torch.int32, device=dev)
-    dist = torch.empty((N, K), dtype=torch.float32, device=dev) if with_distances else None
-    cnt = torch.empty((N,), dtype=torch.int32, device=dev)
+    nr = N
+    if rows is not None:
+        a0, a1 = int(rows[0]), int(rows[1])
+        if not 0 <= a0 <= a1 <= N:
+            raise EsInvalidArgument("build_neighbors: rows must satisfy 0 <= a0 <= a1 <= N")
+        nr = a1 - a0
+        d.row0, d.nrows = (a0, nr) if nr > 0 else (0, 0)
+    nbr = torch.empty((nr, K), dtype=torch.int32, device=dev)
+    dist = torch.empty((nr, K), dtype=torch.float32, device=dev) if with_distances else None
+    cnt = torch.empty((nr,), dtype=torch.int32, device=dev)
+    if nr == 0:
+        return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box))
     ws = _workspace(lib().es_neighbors_workspace_size(ct.byref(d)), dev)
     check(lib().es_neighbors_build(ct.byref(d), _ptr(pos), _ptr(seg_ptr), _ptr(nbr), _ptr(dist), _ptr(cnt),
                                    _ptr(ws), ws.numel(), _stream()), "es_neighbors_build")
     return NeighborIndex(nbr, dist, cnt, float(r_cut), None if box is None else tuple(float(b) for b in box),
-                         seg_ptr=seg_ptr)
+                         seg_ptr=seg_ptr if rows is None else None)
 
 
 def neighbors_transpose(table: torch.Tensor, n_keys: int | None = None):
@@ -254,6 +293,8 @@ def _check_qkv(q, k, v, pos, idx, cfg, row0=0):
     N = q.shape[0]
     _need(k, "k", q.dtype, (Nk, M, 2 * C))
     _need(pos, "pos", torch.float64, (Nk, 3))
+    if pos.data_ptr() % 16:
+        raise EsInvalidArgument("pos: must be 16-byte aligned (use aligned_positions())")
     _need(idx.table, "idx.table", torch.int32)
     if idx.table.shape[0] != N:
         raise EsInvalidArgument("idx: row count != number of query rows")

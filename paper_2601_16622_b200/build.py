@@ -10,6 +10,7 @@ the GPU box with the repo snapshot and loads without a JIT cache.
 from __future__ import annotations
 
 import concurrent.futures as cf
+import hashlib
 import os
 import shutil
 import subprocess
@@ -37,13 +38,19 @@ def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
+def _flags() -> list[str]:
+    return [*ARCH, *NVCC_FLAGS, *os.environ.get("ES_NVCC_EXTRA", "").split()]
+
+
 def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    # objects are keyed by the flag set, so an experiment build (ES_NVCC_EXTRA) never leaks into a default one
+    tag = hashlib.sha1(" ".join(_flags()).encode()).hexdigest()[:10]
+    obj = os.path.join(BUILD, f"{os.path.basename(src)}.{tag}.o")
     deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     deps.append(os.path.join(INCLUDE, "equistream_b200.h"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *os.environ.get("ES_NVCC_EXTRA", "").split(), "-c", src, "-o", obj]
+    cmd = [nvcc(), *_flags(), "-c", src, "-o", obj]
     if verbose or os.environ.get("ES_PTXAS_V"):
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -73,11 +80,15 @@ def build(verbose: bool = False) -> str:
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
+    stamp = LIB + ".objs"
+    same_set = os.path.exists(stamp) and open(stamp).read() == "\n".join(objs)
+    if not same_set or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcuda"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+        with open(stamp, "w") as f:
+            f.write("\n".join(objs))
     return LIB
 
 

@@ -233,14 +233,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           if (g >= NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           const int nkeys = min(KC, a.Nk - k0);
-          const uint32_t pbytes = (uint32_t)((nkeys * 24 + 15) & ~15);
+          // bulk copies move multiples of 16 bytes: an odd key count leaves the last key's 24 bytes to a plain
+          // load (stored before the arrive, whose release orders it for the consumers) -- never past pos[3*Nk]
+          const uint32_t pbytes = (uint32_t)((nkeys & ~1) * 24);
+          if (nkeys & 1) {
+            double* tail = reinterpret_cast<double*>(sm + SM_POS + st * PBYTES) + 3 * (nkeys - 1);
+            const double* src = pos + 3 * ((size_t)k0 + nkeys - 1);
+            tail[0] = src[0]; tail[1] = src[1]; tail[2] = src[2];
+          }
           uint8_t* kb = sm + SM_K + st * KBYTES;
           umma::mbar_arrive_expect_tx(&full_kv[st], KBYTES + VBYTES + pbytes);
           for (int mm = 0; mm < MM; ++mm)
             umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
           umma::tma_load_3d(sm + SM_VST + st * VBYTES, &mv, &full_kv[st], HD * h, 0, k0);
         TC_TRACE(true, g_trace[0][g]);
-          umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
+          if (pbytes) umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
         }
         g0 += nch;
       }

@@ -49,6 +49,10 @@ es_status check_attn(const es_attn_desc* d) {
   if (d->H > 64) return fail(ES_UNSUPPORTED, "attn: H <= 64");
   if (d->Nk < 0 || d->row0 < 0) return fail(ES_INVALID_ARGUMENT, "attn: row0, Nk >= 0");
   if (d->Nk > 0 && d->row0 + d->N > d->Nk) return fail(ES_INVALID_ARGUMENT, "attn: row0 + N > Nk");
+  if (d->bias_mode != ES_BIAS_NONE && d->bias_mode != ES_BIAS_POLY2)
+    return fail(ES_INVALID_ARGUMENT, "attn: unknown bias_mode");
+  if (d->bias_mode == ES_BIAS_POLY2 && !(std::isfinite(d->bias[0]) && std::isfinite(d->bias[1]) && std::isfinite(d->bias[2])))
+    return fail(ES_INVALID_ARGUMENT, "attn: bias parameters must be finite");
   return ES_OK;
 }
 
@@ -167,6 +171,8 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: null buffer");
     if (d->N > 0 && !tiles && (!workspace || workspace_bytes < es_attn_fwd_workspace_size(d)))
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+    if (d->N > 0 && ((uintptr_t)pos & 15) != 0)  // the tensor-core kernels bulk-copy key positions (16-byte units)
+      return fail(ES_INVALID_ARGUMENT, "attn_fwd: pos must be 16-byte aligned");
     AttnArgs a = to_args(d);
     a.tiles = tiles;
     return attn_fwd_launch(a, q, k, v, pos, nbr, out, lse, workspace, workspace_bytes, (cudaStream_t)stream);
@@ -191,10 +197,23 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
     if (dpos && d->L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
-    if (d->N == 0)
-      return dpos ? attn_bwd_launch(to_args(d), q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv,
-                                    nullptr, nullptr, dpos, nullptr, 0, (cudaStream_t)stream)
+    if (d->N == 0) {
+      // No query rows: dk / dv are still [Nk] outputs (a row shard with an empty slab contributes zeros to the
+      // reduce-scatter), and dpos is overwritten.
+      const AttnArgs a0 = to_args(d);
+      const size_t es = d->dtype == ES_BF16 ? 2 : 4, M = (size_t)(d->L + 1) * (d->L + 1);
+      const size_t nk = d->Nk > 0 ? (size_t)d->Nk : 0;
+      if (nk > 0 && (!dk || !dv)) return fail(ES_INVALID_ARGUMENT, "attn_bwd: null dk/dv");
+      if (nk > 0) {
+        es_status z = cuda_status(cudaMemsetAsync(dk, 0, es * nk * M * 2 * d->C, (cudaStream_t)stream), "attn_bwd: dk");
+        if (z == ES_OK)
+          z = cuda_status(cudaMemsetAsync(dv, 0, es * nk * M * d->C, (cudaStream_t)stream), "attn_bwd: dv");
+        if (z != ES_OK) return z;
+      }
+      return dpos ? attn_bwd_launch(a0, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, nullptr,
+                                    nullptr, dpos, nullptr, 0, (cudaStream_t)stream)
                   : ES_OK;
+    }
     if (!q || !k || !v || !pos || !nbr || !rev_ptr || !rev_pair || !out || !lse || !dout || !dq || !dk || !dv)
       return fail(ES_INVALID_ARGUMENT, "attn_bwd: null buffer");
     if (!workspace || workspace_bytes < es_attn_bwd_workspace_size(d))
@@ -216,12 +235,16 @@ static es_status check_nbr(const es_nbr_desc* d) {
   if (d->periodic && !(d->box[0] > 0 && d->box[1] > 0 && d->box[2] > 0))
     return fail(ES_INVALID_ARGUMENT, "neighbors: periodic box must be positive");
   if (d->nseg < 0) return fail(ES_INVALID_ARGUMENT, "neighbors: nseg >= 0");
+  if (d->row0 < 0 || d->nrows < 0 || (d->nrows > 0 && d->row0 + d->nrows > d->N) || (d->nrows == 0 && d->row0 != 0))
+    return fail(ES_INVALID_ARGUMENT, "neighbors: rows [row0, row0 + nrows) must lie in [0, N)");
   return ES_OK;
 }
 
 static NbrArgs nbr_args(const es_nbr_desc* d) {
   NbrArgs a;
   a.N = d->N; a.K = d->K; a.nseg = d->nseg; a.periodic = d->periodic; a.r_cut = d->r_cut;
+  a.row0 = d->nrows > 0 ? d->row0 : 0;
+  a.nrows = d->nrows > 0 ? d->nrows : d->N;
   for (int x = 0; x < 3; ++x) a.box[x] = d->box[x];
   return a;
 }
@@ -265,6 +288,7 @@ es_status es_tile_mask(int32_t N, int32_t K, const int32_t* nbr, int32_t tq, int
                        void* stream) {
   return guarded([&] {
     if (N < 0 || K < 1) return fail(ES_INVALID_ARGUMENT, "tile_mask: N >= 0, K >= 1");
+    if (tq < 1 || tk < 1) return fail(ES_INVALID_ARGUMENT, "tile_mask: tq, tk >= 1");
     if (N > 0 && (!nbr || !mask)) return fail(ES_INVALID_ARGUMENT, "tile_mask: null buffer");
     return tile_mask_launch(N, K, nbr, tq, tk, (N + tk - 1) / tk, mask, (cudaStream_t)stream);
   });

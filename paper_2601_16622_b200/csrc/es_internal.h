@@ -71,6 +71,7 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
 
 struct NbrArgs {
   int N, K, nseg, periodic;
+  int row0, nrows;
   double r_cut;
   double box[3];
 };

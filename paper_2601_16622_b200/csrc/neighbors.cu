@@ -57,10 +57,12 @@ struct TopK {
 
 struct NbrK {
   int N, K, nseg, periodic;
+  int row0, nrows;  // query rows [row0, row0 + nrows) are searched; outputs are indexed by i - row0
   double rc2, bx, by, bz;
 };
 
 __device__ __forceinline__ void emit(const NbrK& p, int i, const TopK& t, int32_t* nbr, float* dist, int32_t* count) {
+  i -= p.row0;
   for (int s = 0; s < p.K; ++s) {
     nbr[(size_t)i * p.K + s] = s < t.n ? t.j[s] : -1;
     if (dist) dist[(size_t)i * p.K + s] = s < t.n ? (float)sqrt(t.d2[s]) : 0.f;
@@ -85,8 +87,9 @@ __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p
   __shared__ double cd[SEG_WARPS][SEG_WARP_MAX];
   __shared__ int cj[SEG_WARPS][SEG_WARP_MAX];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * SEG_WARPS + warp;
-  if (i >= p.N) return;
+  const int r = blockIdx.x * SEG_WARPS + warp;
+  if (r >= p.nrows) return;
+  const int i = p.row0 + r;
   int a0 = 0, a1 = p.N;
   if (seg_ptr) {
     int lo = 0, hi = p.nseg;
@@ -132,8 +135,8 @@ __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p
   }
   __syncwarp();
   const int K = p.K;
-  int32_t* orow = nbr + (size_t)i * K;
-  float* drow = dist ? dist + (size_t)i * K : nullptr;
+  int32_t* orow = nbr + (size_t)r * K;
+  float* drow = dist ? dist + (size_t)r * K : nullptr;
   for (int c = lane; c < n; c += 32) {
     const double d = cd[warp][c];
     const int j = cj[warp][c];
@@ -151,7 +154,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p
     orow[s] = -1;
     if (drow) drow[s] = 0.f;
   }
-  if (lane == 0) count[i] = min(n, K);
+  if (lane == 0) count[r] = min(n, K);
 }
 
 // ---------------------------------------------------------------- hashed grid
@@ -207,8 +210,9 @@ __global__ void __launch_bounds__(128) nbr_grid_kernel(NbrK p, GridK g, const do
                                                        const int* __restrict__ start, const int* __restrict__ end,
                                                        int32_t* __restrict__ nbr, float* __restrict__ dist,
                                                        int32_t* __restrict__ count) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.N) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= p.nrows) return;
+  const int i = p.row0 + r;
   TopK t;
   t.n = 0;
   const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
@@ -285,15 +289,16 @@ size_t nbr_workspace_bytes(const NbrArgs& a) {
 es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* seg_ptr, int32_t* nbr, float* dist,
                            int32_t* count, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (a.K > kMaxK) return fail(ES_UNSUPPORTED, "neighbors: K > 128");
-  if (a.N == 0) return ES_OK;
+  if (a.N == 0 || a.nrows == 0) return ES_OK;
   NbrK p;
   p.N = a.N; p.K = a.K; p.nseg = a.nseg; p.periodic = a.periodic;
+  p.row0 = a.row0; p.nrows = a.nrows;
   p.rc2 = a.r_cut * a.r_cut;
   p.bx = a.box[0]; p.by = a.box[1]; p.bz = a.box[2];
   const int tpb = 128, blocks = (a.N + tpb - 1) / tpb;
   if (!use_grid(a)) {
     const int32_t* sp = (seg_ptr && a.nseg >= 1) ? seg_ptr : nullptr;  // NULL: one segment [0, N)
-    nbr_segment_warp_kernel<<<(a.N + SEG_WARPS - 1) / SEG_WARPS, SEG_WARPS * 32, 0, st>>>(p, pos, sp, nbr, dist,
+    nbr_segment_warp_kernel<<<(a.nrows + SEG_WARPS - 1) / SEG_WARPS, SEG_WARPS * 32, 0, st>>>(p, pos, sp, nbr, dist,
                                                                                            count);
     return cuda_status(cudaGetLastError(), "nbr_segment_warp_kernel");
   }
@@ -329,7 +334,7 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
   cudaMemsetAsync(start, 0, sizeof(int) * nb, st);
   cudaMemsetAsync(end, 0, sizeof(int) * nb, st);
   grid_bounds_kernel<<<blocks, tpb, 0, st>>>(a.N, skey, start, end);
-  nbr_grid_kernel<<<blocks, tpb, 0, st>>>(p, g, pos, cell, sidx, start, end, nbr, dist, count);
+  nbr_grid_kernel<<<(a.nrows + tpb - 1) / tpb, tpb, 0, st>>>(p, g, pos, cell, sidx, start, end, nbr, dist, count);
   return cuda_status(cudaGetLastError(), "nbr_grid_kernel");
 }
 

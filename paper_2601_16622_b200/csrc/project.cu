@@ -184,7 +184,10 @@ es_status proj_fwd_launch(const ProjArgs& a, const void* h, const void* W, void*
 
 es_status proj_bwd_launch(const ProjArgs& a, const void* h, const void* W, const void* dq, const void* dk,
                           const void* dv, void* dh, float* dW, cudaStream_t st) {
-  if (a.N == 0) return ES_OK;
+  if (a.N == 0)  // dW is overwritten even with no rows (an empty shard all-reduces zeros)
+    return dW ? cuda_status(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)(a.L + 1) * a.C * (2 * a.Dq + a.Cv), st),
+                            "project_bwd: dW")
+              : ES_OK;
   if (!force_simt() && proj_tc_supported(a)) return proj_bwd_tc_launch(a, h, W, dq, dk, dv, dh, dW, st);
   return a.dtype == ES_BF16 ? bwd_t<__nv_bfloat16>(a, h, W, dq, dk, dv, dh, dW, st)
                             : bwd_t<float>(a, h, W, dq, dk, dv, dh, dW, st);

@@ -4,6 +4,7 @@ tensor-pipe / issue utilisation, occupancy and the top stall reasons.
 
     python profiles/tools/ncu_summary.py gpurun_out/prof.ncu-rep > profiles/rNN_ncu_summary.txt
     python profiles/tools/ncu_summary.py gpurun_out/prof.ncu-rep --json   (machine-readable)
+    python profiles/tools/ncu_summary.py gpurun_out/prof.ncu-rep --traffic > profiles/ncu_traffic.json
 """
 import csv
 import io
@@ -45,7 +46,7 @@ def num(x):
         return None
 
 
-def main(rep, as_json):
+def main(rep, as_json, traffic=False):
     res = []
     for hdr, units, v in rows(rep):
         d = dict(zip(hdr, v))
@@ -63,6 +64,18 @@ def main(rep, as_json):
     if as_json:
         print(json.dumps(res, indent=1))
         return
+    if traffic:  # profiles/ncu_traffic.json: what bench.py's roofline line reads (first launch of each kernel)
+        out = {"source": f"{rep} (ncu --set full)", "bytes_per_launch": {}}
+        for e in res:
+            name = e["kernel"].split("(")[0].split("::")[-1].split("<")[0].strip()
+            if name in out["bytes_per_launch"]:
+                continue
+            out["bytes_per_launch"][name] = {
+                "dram_read": e.get("dram_read"), "dram_write": e.get("dram_write"),
+                "total": (e.get("dram_read") or 0) + (e.get("dram_write") or 0),
+                "tensor_pipe_pct": e.get("tensor_pipe_pct"), "duration_ns": e.get("duration")}
+        print(json.dumps(out, indent=1))
+        return
     for e in res:
         print(e["kernel"])
         for _, name in KEYS:
@@ -72,4 +85,4 @@ def main(rep, as_json):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], "--json" in sys.argv)
+    main(sys.argv[1], "--json" in sys.argv, "--traffic" in sys.argv)
