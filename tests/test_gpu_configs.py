@@ -1,0 +1,217 @@
+"""GPU parity at the BASELINE configurations' own shapes:
+
+* configs[2] single systems at N = 1000 and 2048 (grid neighbours, uniform
+  128-row tiles on the tensor-core forward / backward), bf16;
+* configs[3] molecules of 350 atoms at L = 4, C = 128 (the L = 4 projection
+  and attention), bf16, including dh and dW;
+* equivariance of the bf16 tensor-core path (the benched one) on a
+  molecule batch: f(R pos, D h) = D f(pos, h) for out and dh;
+* the shard-invariance of row-range neighbour builds (es_neighbors_build
+  with row0 / nrows) and empty-shard gradients.
+
+Tolerances: bf16-input paths 2e-2 normwise against the fp64 oracle run on
+the GPU's own bf16 operands; neighbour lists bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import pyoracle as po
+from paper_2601_16622_b200 import systems as S
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")]
+
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def es():
+    import paper_2601_16622_b200 as es
+    from paper_2601_16622_b200 import _lib
+    assert _lib.lib().es_device_ok() == 1, "not an sm_100 device"
+    return es
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-30))
+
+
+def dev(x, dtype=None):
+    t = torch.as_tensor(np.ascontiguousarray(x)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+def d64(t):
+    return t.float().double().cpu().numpy()
+
+
+def layer_vs_oracle(es, pos, seg, box, L, C, H, seed):
+    """Full layer through the public API (neighbours, projections, attention
+    fwd + bwd, projection bwd) in bf16, against the oracle on the same bf16
+    operands.  Returns the error dict."""
+    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention
+    N = len(pos)
+    h = S.random_features(N, L, C, seed)
+    W = S.random_weights(L, C, seed)
+    cfg = AttentionConfig(heads=H, L=L, box=None if box is None else tuple(box))
+    tp = dev(pos)
+    ts = None if seg is None else dev(seg)
+    idx = es.build_neighbors(tp, 64, 6.0, ts, box)
+    th, tW = dev(h, torch.bfloat16), dev(W, torch.bfloat16)
+    q, k, v = es.project_qk(th, tW, L)
+    out, lse = es.stream_aggregate(q, k, v, tp, idx, cfg)
+    g = dev(np.random.default_rng(seed + 1).standard_normal(tuple(out.shape)), torch.bfloat16)
+    dq, dk, dv = es.stream_aggregate_backward(g, SavedAttention(q, k, v, tp, idx, out, lse, cfg))
+    dh, dW = es.project_qk_backward(th, tW, L, dq, dk, dv)
+    torch.cuda.synchronize()
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0, seg_ptr=seg, box=box)
+    errs = {"nbr_exact": bool(np.array_equal(idx.table.cpu().numpy(), nbr))}
+    hb, Wb = d64(th), d64(tW)
+    rq, rk, rv = po.project(hb, Wb, L)
+    errs["proj"] = max(rel(d64(q), rq), rel(d64(k), rk), rel(d64(v), rv))
+    qo, ko, vo = d64(q), d64(k), d64(v)
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, box=box)
+    ro, rl = po.attn_fwd(P, qo, ko, vo, pos, nbr)
+    errs["out"] = rel(d64(out), ro)
+    fin = np.isfinite(rl)
+    errs["lse"] = rel(lse.cpu().numpy()[fin], rl[fin])
+    rdq, rdk, rdv = po.attn_bwd(P, qo, ko, vo, pos, nbr, ro, rl, d64(g))
+    errs["dq"], errs["dk"], errs["dv"] = rel(d64(dq), rdq), rel(d64(dk), rdk), rel(d64(dv), rdv)
+    rdh, rdW = po.project_bwd(hb, Wb, L, d64(dq), d64(dk), d64(dv))
+    errs["dh"], errs["dW"] = rel(d64(dh), rdh), rel(dW.cpu().numpy(), rdW)
+    return errs
+
+
+def check(errs, tol=BF16_TOL):
+    assert errs.pop("nbr_exact"), "neighbour lists differ from the oracle"
+    bad = {k: v for k, v in errs.items() if not v < tol}
+    assert not bad, f"bf16 parity above {tol}: {errs}"
+
+
+@pytest.mark.parametrize("n", [1000, 2048])
+def test_config3_single_system(es, oracle, n):
+    """configs[2]: one FCC system (grid neighbour search, uniform query tiles)."""
+    check(layer_vs_oracle(es, S.gen_fcc_system(n, 3.8, n), None, None, 2, 128, 8, seed=n))
+
+
+def test_config4_l4_molecules(es, oracle):
+    """configs[3]: 350-atom molecules at L = 4, C = 128, H = 8 (d_k = 800)."""
+    b = S.molecule_batch(4, 350, 350, 2000, seed_offset=2000, fixed=350)
+    check(layer_vs_oracle(es, b.pos, b.seg_ptr, None, 4, 128, 8, seed=4))
+
+
+def test_config5_periodic_slab(es, oracle):
+    """configs[4] geometry (PBC minimum image) on a small box."""
+    b = S.periodic_box(1500, 8, 3.8, 3)
+    check(layer_vs_oracle(es, b.pos, None, b.box, 2, 128, 8, seed=5))
+
+
+def test_bf16_tensor_core_equivariance(es):
+    """The benched bf16 tcgen05 path: rotating positions and features rotates
+    out and dh (loss 1/2 ||out||^2 is invariant, so dh is equivariant)."""
+    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention, rotate_features
+    L, C, H = 2, 128, 8
+    b = S.molecule_batch(96, 40, 60, 12)
+    h = S.random_features(b.n_atoms, L, C, 12)
+    W = S.random_weights(L, C, 12)
+    cfg = AttentionConfig(heads=H, L=L)
+    th, tW, seg = dev(h, torch.bfloat16), dev(W, torch.bfloat16), dev(b.seg_ptr)
+    rng = np.random.default_rng(3)
+    qq = rng.standard_normal(4)
+    w, x, y, z = qq / np.linalg.norm(qq)
+    R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+
+    def run(pos, hh):
+        idx = es.build_neighbors(pos, 64, 6.0, seg)
+        q, k, v = es.project_qk(hh, tW, L)
+        out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
+        dq, dk, dv = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
+        dh, _ = es.project_qk_backward(hh, tW, L, dq, dk, dv)
+        return out, dh
+
+    out, dh = run(dev(b.pos), th)
+    out2, dh2 = run(dev(b.pos @ R.T), rotate_features(th, L, R))
+    assert rel(d64(out2), d64(rotate_features(out, L, R))) < BF16_TOL
+    assert rel(d64(dh2), d64(rotate_features(dh, L, R))) < BF16_TOL
+
+
+@pytest.mark.parametrize("kind", ["grid", "pbc", "batch"])
+def test_neighbor_row_range_matches_full(es, kind):
+    """es_neighbors_build with rows [a0, a1) equals rows a0..a1-1 of the full build."""
+    seg = box = None
+    if kind == "grid":
+        pos = S.gen_fcc_system(3000, 3.8, 1)
+    elif kind == "pbc":
+        b = S.periodic_box(4000, 10, 3.8, 2)
+        pos, box = b.pos, b.box
+    else:
+        b = S.molecule_batch(50, 40, 60, 3)
+        pos, seg = b.pos, dev(b.seg_ptr)
+    full = es.build_neighbors(dev(pos), 64, 6.0, seg, box)
+    N = len(pos)
+    for a0, a1 in ((0, N // 3), (N // 3, N - 7), (N - 5, N), (10, 10)):
+        part = es.build_neighbors(dev(pos), 64, 6.0, seg, box, rows=(a0, a1))
+        assert torch.equal(part.table, full.table[a0:a1])
+        assert torch.equal(part.count, full.count[a0:a1])
+        assert torch.allclose(part.distances, full.distances[a0:a1])
+
+
+def test_empty_row_shard_zeroes_gradients(es):
+    """A rank with no query rows (N = 0) still overwrites its dk / dv [Nk]
+    and dW outputs (uninitialised memory must not reach the
+    reduce-scatter / all-reduce)."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex
+    L, C, H, Nk = 2, 128, 8, 40
+    cfg = AttentionConfig(heads=H, L=L)
+    M = (L + 1) ** 2
+    q = torch.empty((0, M, 2 * C), dtype=torch.bfloat16, device="cuda")
+    k = torch.randn((Nk, M, 2 * C), device="cuda").bfloat16()
+    v = torch.randn((Nk, M, C), device="cuda").bfloat16()
+    pos = dev(S.gen_fcc_system(Nk, 3.8, 0))
+    idx = NeighborIndex(torch.empty((0, 64), dtype=torch.int32, device="cuda"), None, None, 6.0)
+    import ctypes as ct
+
+    from paper_2601_16622_b200 import _lib
+    d = cfg.desc(0, 64, C, torch.bfloat16, Nk, Nk)
+    dk = torch.full_like(k, float("nan"))  # the library must overwrite these
+    dv = torch.full_like(v, float("nan"))
+    ws = torch.empty(256, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    nil = None
+    _lib.check(_lib.lib().es_attn_bwd(ct.byref(d), q.data_ptr(), k.data_ptr(), v.data_ptr(), pos.data_ptr(),
+                                      idx.table.data_ptr(), nil, nil, nil, nil, nil, nil, dk.data_ptr(),
+                                      dv.data_ptr(), nil, nil, ws.data_ptr(), ws.numel(), st), "es_attn_bwd")
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(dk.float()) == 0 and torch.count_nonzero(dv.float()) == 0
+    h = torch.empty((0, M, C), dtype=torch.bfloat16, device="cuda")
+    W = torch.randn((L + 1, C, 5 * C), device="cuda").bfloat16()
+    _, dW = es.project_qk_backward(h, W, L, q, q, torch.empty((0, M, C), dtype=torch.bfloat16, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(dW) == 0
+
+
+def test_unaligned_positions_rejected(es):
+    """es_attn_fwd requires 16-byte-aligned positions (the tensor-core kernels
+    bulk-copy key positions); aligned_positions() makes a valid copy."""
+    from paper_2601_16622_b200._lib import EsInvalidArgument
+    from paper_2601_16622_b200.api import AttentionConfig, aligned_positions
+    L, C, H = 2, 128, 8
+    b = S.molecule_batch(3, 40, 60, 1)
+    big = dev(np.concatenate([np.zeros((1, 3)), b.pos]))
+    pos = big[1:]  # 24-byte offset: 8-byte aligned
+    assert pos.data_ptr() % 16 == 8
+    idx = es.build_neighbors(aligned_positions(pos), 64, 6.0, dev(b.seg_ptr))
+    M = (L + 1) ** 2
+    N = b.n_atoms
+    q = torch.randn((N, M, 2 * C), device="cuda").bfloat16()
+    v = torch.randn((N, M, C), device="cuda").bfloat16()
+    cfg = AttentionConfig(heads=H, L=L)
+    with pytest.raises(EsInvalidArgument):
+        es.stream_aggregate(q, q, v, pos, idx, cfg)
+    out, _ = es.stream_aggregate(q, q, v, aligned_positions(pos), idx, cfg)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
