@@ -276,8 +276,9 @@ class Workload:
         idx = es.build_neighbors(pos, K_, RCUT, seg, box=self.box, with_distances=False)
         idx.transpose()
         q, k, v = es.project_qk(h, W, self.L)
-        out, lse = es.stream_aggregate(q, k, v, pos, idx, self.cfg)
-        dq, dk, dv = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, self.cfg))
+        out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, self.cfg, return_scores=True)
+        dq, dk, dv = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, self.cfg,
+                                                                      scores=sc))
         dh, dW = es.project_qk_backward(h, W, self.L, dq, dk, dv)
         return idx, dh, dW
 
@@ -529,15 +530,15 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         q, k, v = es.project_qk(h, W, L)
         idx = es.build_neighbors(pos, K_, RCUT, seg, box=wl.box, with_distances=False)
         idx.transpose()
-        out, lse = es.stream_aggregate(q, k, v, pos, idx, wl.cfg)
-        saved = SavedAttention(q, k, v, pos, idx, out, lse, wl.cfg)
+        out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True)
+        saved = SavedAttention(q, k, v, pos, idx, out, lse, wl.cfg, scores=sc)
         dq, dk, dv = es.stream_aggregate_backward(out, saved)
-        t = {"attn_fwd": time_call(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg)),
+        t = {"attn_fwd": time_call(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True)),
              "attn_bwd": time_call(lambda: es.stream_aggregate_backward(out, saved)),
              "proj_fwd": time_call(lambda: es.project_qk(h, W, L)),
              "proj_bwd": time_call(lambda: es.project_qk_backward(h, W, L, dq, dk, dv))}
         kt_bwd = kernel_times(lambda: es.stream_aggregate_backward(out, saved))
-        kt_fwd = kernel_times(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg))
+        kt_fwd = kernel_times(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True))
         roof = roofline(wl, t, kt_fwd, kt_bwd, kt, n_loc, E, s_bytes, fl, ms)
     line = {
         "metric": METRIC,

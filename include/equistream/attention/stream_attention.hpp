@@ -50,6 +50,9 @@ struct AttentionProblem {
   bool periodic = false;
   double box[3] = {0, 0, 0};
   int32_t row0 = 0, n_keys = 0;  // query-row sharding (0 = unsharded)
+  // radial score bias b(r) = bias[0] + bias[1] r + bias[2] r^2 (RadialScalars b)
+  bool has_bias = false;
+  double bias[3] = {0, 0, 0};
 
   es_attn_desc desc() const {
     es_attn_desc d{};
@@ -62,6 +65,8 @@ struct AttentionProblem {
     for (int a = 0; a < 3; ++a) d.box[a] = box[a];
     d.row0 = row0;
     d.Nk = n_keys;
+    d.bias_mode = has_bias ? ES_BIAS_POLY2 : ES_BIAS_NONE;
+    for (int a = 0; a < 3; ++a) d.bias[a] = bias[a];
     return d;
   }
 };
@@ -103,7 +108,9 @@ inline std::size_t tiles_workspace_size(const AttentionProblem& p) {
 inline void build_tiles(const AttentionProblem& p, NeighborIndex& idx, void* buf, std::size_t bytes,
                         void* stream = nullptr, const int32_t* seg_ptr = nullptr, int32_t nseg = 0) {
   const es_attn_desc d = p.desc();
-  check(es_attn_tiles_build(&d, idx.table, seg_ptr, nseg, buf, bytes, stream), "build_tiles");
+  // the transposed relation (transpose()) lets the tiles carry the backward's key-side lists
+  check(es_attn_tiles_build(&d, idx.table, seg_ptr, nseg, idx.rev_ptr, idx.rev_pair, buf, bytes, stream),
+        "build_tiles");
   idx.tiles = bytes ? buf : nullptr;
 }
 
@@ -112,11 +119,13 @@ inline std::size_t forward_workspace_size(const AttentionProblem& p) {
   const es_attn_desc d = p.desc();
   return es_attn_fwd_workspace_size(&d);
 }
+// scores (optional): [N][K][H] float, kept for the backward (saves recomputing q.k)
 inline void stream_aggregate(const AttentionProblem& p, const void* q, const void* k, const void* v,
                              const double* pos, const NeighborIndex& idx, void* m, float* lse, void* workspace,
-                             std::size_t ws_bytes, void* stream = nullptr) {
+                             std::size_t ws_bytes, void* stream = nullptr, float* scores = nullptr) {
   const es_attn_desc d = p.desc();
-  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, idx.tiles, workspace, ws_bytes, stream), "stream_aggregate");
+  check(es_attn_fwd(&d, q, k, v, pos, idx.table, m, lse, scores, idx.tiles, workspace, ws_bytes, stream),
+        "stream_aggregate");
 }
 
 // stream_aggregate_backward
@@ -127,11 +136,20 @@ inline std::size_t backward_workspace_size(const AttentionProblem& p) {
 inline void stream_aggregate_backward(const AttentionProblem& p, const void* grad_m, const void* q, const void* k,
                                       const void* v, const double* pos, const NeighborIndex& idx, const void* m,
                                       const float* lse, void* grad_q, void* grad_k, void* grad_v, void* workspace,
-                                      std::size_t ws_bytes, void* stream = nullptr, double* grad_pos = nullptr) {
+                                      std::size_t ws_bytes, void* stream = nullptr, double* grad_pos = nullptr,
+                                      const float* scores = nullptr) {
   const es_attn_desc d = p.desc();
-  check(es_attn_bwd(&d, q, k, v, pos, idx.table, idx.rev_ptr, idx.rev_pair, m, lse, grad_m, grad_q, grad_k, grad_v,
-                    grad_pos, idx.tiles, workspace, ws_bytes, stream),
+  check(es_attn_bwd(&d, q, k, v, pos, idx.table, idx.rev_ptr, idx.rev_pair, m, lse, scores, grad_m, grad_q, grad_k,
+                    grad_v, grad_pos, idx.tiles, workspace, ws_bytes, stream),
         "stream_aggregate_backward");
+}
+
+// OpCounters / stats structure (counters.hpp:11-32)
+inline es_attn_stats stats(const AttentionProblem& p, int64_t n_pairs) {
+  const es_attn_desc d = p.desc();
+  es_attn_stats st{};
+  check(es_attn_stats_query(&d, n_pairs, &st), "stats");
+  return st;
 }
 
 inline std::string conventions_manifest() { return es_conventions_manifest(); }

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 7
+#define ES_ABI_VERSION 8
 
 typedef enum {
   ES_OK = 0,
@@ -115,15 +115,24 @@ typedef struct {
  * es_neighbors_build; NULL / 0 for one system): query tiles pack whole
  * segments, so a tile's key chunks cover only its own molecules. */
 size_t es_attn_tiles_workspace_size(const es_attn_desc* d);
+/* rev_ptr / rev_pair (optional, from es_neighbors_transpose on the same nbr):
+ * also build the key-side lists (key tiles, their query-chunk lists and
+ * per-key (chunk, query mask) entries) the tensor-core dk pass of the
+ * backward walks; without them es_attn_bwd builds those in its workspace. */
 es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const int32_t* seg_ptr, int32_t nseg,
-                              void* tiles, size_t bytes, void* stream);
+                              const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
+                              void* stream);
 
 /* Workspace: es_attn_fwd_workspace_size(d) bytes (the tile structures when
  * tiles == NULL; 256 bytes for the SIMT kernels).  Caller-owned, reusable
  * across calls on the same stream; the library allocates nothing. */
 size_t es_attn_fwd_workspace_size(const es_attn_desc* d);
+/* scores (optional, NULL = not kept): [N][K][H] float32, the scores s_ij =
+ * tau q_i.k_j + b(r_ij) of the valid slots (padding slots untouched) -- the
+ * O(N K H) scalars es_attn_bwd can reuse instead of recomputing q_i.k_j
+ * (never O(N K C)).  pos must be 16-byte aligned. */
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, const void* tiles, void* workspace,
+                      const int32_t* nbr, void* out, float* lse, float* scores, const void* tiles, void* workspace,
                       size_t workspace_bytes, void* stream);
 
 /* Workspace: es_attn_bwd_workspace_size(d) bytes (per-pair-head dscore
@@ -134,10 +143,30 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
  * 786) through phi(r_ij) and the solid harmonics of the value
  * map; L = 2 only (ES_UNSUPPORTED otherwise).  Overwritten, not accumulated. */
 size_t es_attn_bwd_workspace_size(const es_attn_desc* d);
+/* scores (optional): the forward's scores output for the same inputs; NULL
+ * recomputes them. */
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
-                      const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
-                      const void* tiles, void* workspace, size_t workspace_bytes, void* stream);
+                      const float* lse, const float* scores, const void* dout, void* dq, void* dk, void* dv,
+                      double* dpos, const void* tiles, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Operation and memory accounting (OpCounters / the stats structure,
+ * proj/include/equistream/core/counters.hpp:11-32) for one
+ * layer of `n_pairs` valid pairs: algorithmic multiply-adds of the forward and
+ * backward (score 2 d_k per pair-head ... counted as multiply-adds: d_k for
+ * the score, C_h M^2 for the value operator; backward 3 d_k + 2 C_h M^2) and
+ * the library's auxiliary device memory, split into floating-point
+ * activations (what scales with C) and integer index structures (what scales
+ * with the neighbour index, N K). */
+typedef struct {
+  uint64_t madds_fwd, madds_bwd;           /* attention (projections excluded) */
+  uint64_t madds_proj_fwd, madds_proj_bwd;
+  uint64_t aux_float_bytes_fwd;            /* floating-point scratch of es_attn_fwd (lse excluded: an output) */
+  uint64_t aux_float_bytes_bwd;            /* floating-point scratch of es_attn_bwd: O(N K H) scalars */
+  uint64_t aux_index_bytes;                /* tile lists / key-side lists (es_attn_tiles_workspace_size) */
+  uint64_t workspace_fwd_bytes, workspace_bwd_bytes;
+} es_attn_stats;
+es_status es_attn_stats_query(const es_attn_desc* d, int64_t n_pairs, es_attn_stats* out);
 
 /* Neighbour index: per atom the K nearest j != i with d^2 < r_cut^2, sorted
  * by (d^2, j), padded with -1, restricted to the atom's segment

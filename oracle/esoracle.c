@@ -642,11 +642,16 @@ typedef struct {
                         2 = EAAS per pair (the reference CPU path) */
   int phi_mode;      /* 0 = cosine cutoff, 1 = phi == 1 */
   const double* box; /* NULL or [3] minimum image */
+  int bias_mode;     /* RadialScalars b: 0 = b == 0, 1 = b0 + b1 r + b2 r^2 */
+  double bias[3];
 } eso_attn_desc;
 
 static inline void pair_vec(const double* pos, int i, int j, const double* box, double* r) {
   r[0] = pos[3 * j] - pos[3 * i]; r[1] = pos[3 * j + 1] - pos[3 * i + 1]; r[2] = pos[3 * j + 2] - pos[3 * i + 2];
   if (box) for (int a = 0; a < 3; ++a) r[a] = r[a] - box[a] * rint(r[a] / box[a]);
+}
+static inline double bias_of(const eso_attn_desc* d, double rn) { /* score(q,k,r) = tau q.k + b(r), Eq. 18 */
+  return d->bias_mode ? d->bias[0] + d->bias[1] * rn + d->bias[2] * rn * rn : 0.0;
 }
 static inline double phi_of(const eso_attn_desc* d, double rn) {
   if (d->phi_mode == 1) return 1.0;
@@ -758,7 +763,7 @@ void eso_attn_fwd(const eso_attn_desc* d, const double* q, const double* k, cons
           for (int mm = 0; mm < M; ++mm)
             for (int c = h * dqh; c < (h + 1) * dqh; ++c)
               acc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
-          s[h] = tau * acc; /* Eq. 18 with b == 0 */
+          s[h] = tau * acc + bias_of(d, rn); /* Eq. 18 */
         }
         pair_value(d, v, j, r, phi_of(d, rn), x, scr);
         for (int h = 0; h < H; ++h) { /* Eqs. 15-17 */
@@ -800,11 +805,13 @@ void eso_attn_dense_ref(const eso_attn_desc* d, const double* q, const double* k
       for (int h = 0; h < H; ++h) {
         double acc = -INFINITY;
         if (j >= 0) {
+          double r[3];
+          pair_vec(pos, i, j, d->box, r);
           acc = 0.0;
           for (int mm = 0; mm < M; ++mm)
             for (int c = h * dqh; c < (h + 1) * dqh; ++c)
               acc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
-          acc *= tau;
+          acc = acc * tau + bias_of(d, sqrt(r[0] * r[0] + r[1] * r[1] + r[2] * r[2]));
         }
         S[((size_t)i * K + kk) * H + h] = acc;
       }
@@ -921,7 +928,7 @@ void eso_attn_bwd(const eso_attn_desc* d, const double* q, const double* k, cons
           for (int mm = 0; mm < M; ++mm)
             for (int c = h * dqh; c < (h + 1) * dqh; ++c)
               sc += q[((size_t)i * M + mm) * Dq + c] * k[((size_t)j * M + mm) * Dq + c];
-          const double p = exp(tau * sc - lse[(size_t)i * H + h]);
+          const double p = exp(tau * sc + bias_of(d, rn) - lse[(size_t)i * H + h]);
           double dp = 0.0;
           for (int mm = 0; mm < M; ++mm)
             for (int c = h * cvh; c < (h + 1) * cvh; ++c) dp += y[mm * Cv + c] * v[((size_t)j * M + mm) * Cv + c];

@@ -197,7 +197,7 @@ VALUE_PLAIN, VALUE_DENSE, VALUE_EAAS = 0, 1, 2
 class _Desc(ct.Structure):
     _fields_ = [("N", ct.c_int), ("K", ct.c_int), ("H", ct.c_int), ("L", ct.c_int), ("Dq", ct.c_int),
                 ("Cv", ct.c_int), ("r_cut", ct.c_double), ("value_mode", ct.c_int), ("phi_mode", ct.c_int),
-                ("box", _dp)]
+                ("box", _dp), ("bias_mode", ct.c_int), ("bias", ct.c_double * 3)]
 
 
 @dataclass
@@ -208,11 +208,14 @@ class AttnProblem:
     value_mode: int = VALUE_DENSE
     phi_mode: int = 0
     box: np.ndarray | None = None
+    bias: tuple | None = None  # b(r) = b0 + b1 r + b2 r^2; None: b == 0
 
     def desc(self, N, K, Dq, Cv):
         self._box = None if self.box is None else _c(self.box)
+        b = (0.0, 0.0, 0.0) if self.bias is None else tuple(float(x) for x in self.bias) + (0.0,) * (3 - len(self.bias))
         return _Desc(N, K, self.H, self.L, Dq, Cv, self.r_cut, self.value_mode, self.phi_mode,
-                     None if self._box is None else _p(self._box))
+                     None if self._box is None else _p(self._box), 0 if self.bias is None else 1,
+                     (ct.c_double * 3)(*b))
 
 
 def project(h, W, L):

@@ -25,12 +25,18 @@ class AttnDesc(ct.Structure):
                 ("row0", ct.c_int32), ("Nk", ct.c_int32), ("bias_mode", ct.c_int32), ("bias", ct.c_double * 3)]
 
 
-ABI_VERSION = 7  # include/equistream_b200.h ES_ABI_VERSION
+ABI_VERSION = 8  # include/equistream_b200.h ES_ABI_VERSION
 
 
 class NbrDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("nseg", ct.c_int32), ("periodic", ct.c_int32),
                 ("r_cut", ct.c_double), ("box", ct.c_double * 3), ("row0", ct.c_int32), ("nrows", ct.c_int32)]
+
+
+class AttnStats(ct.Structure):
+    _fields_ = [(n, ct.c_uint64) for n in ("madds_fwd", "madds_bwd", "madds_proj_fwd", "madds_proj_bwd",
+                                           "aux_float_bytes_fwd", "aux_float_bytes_bwd", "aux_index_bytes",
+                                           "workspace_fwd_bytes", "workspace_bwd_bytes")]
 
 
 class ProjDesc(ct.Structure):
@@ -56,6 +62,7 @@ EXPORTS = [
     "es_neighbors_workspace_size", "es_neighbors_transpose", "es_neighbors_transpose_workspace_size",
     "es_tile_mask", "es_project_fwd", "es_project_bwd", "es_conventions_manifest", "es_cg_real",
     "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
+    "es_attn_stats_query",
 ]
 
 
@@ -67,13 +74,14 @@ def lib() -> ct.CDLL:
                           "(python -m paper_2601_16622_b200.build); there is no CPU fallback")
         L = ct.CDLL(LIB_PATH)
         vp, i32, sz, dp = ct.c_void_p, ct.c_int32, ct.c_size_t, ct.POINTER(ct.c_double)
-        L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 9 + [sz, vp]
+        L.es_attn_fwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 10 + [sz, vp]
         L.es_attn_tiles_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_tiles_workspace_size.restype = sz
-        L.es_attn_tiles_build.argtypes = [ct.POINTER(AttnDesc), vp, vp, i32, vp, sz, vp]
+        L.es_attn_tiles_build.argtypes = [ct.POINTER(AttnDesc), vp, vp, i32, vp, vp, vp, sz, vp]
         L.es_attn_fwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_fwd_workspace_size.restype = sz
-        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 16 + [sz, vp]
+        L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 17 + [sz, vp]
+        L.es_attn_stats_query.argtypes = [ct.POINTER(AttnDesc), ct.c_int64, ct.POINTER(AttnStats)]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]

@@ -115,8 +115,10 @@ class NeighborIndex:
             buf = torch.empty(int(nbytes), dtype=torch.uint8, device=self.table.device)
             seg = self.seg_ptr if (self.seg_ptr is not None and d.row0 == 0 and d.N == self.N) else None
             nseg = 0 if seg is None else seg.numel() - 1
-            check(lib().es_attn_tiles_build(ct.byref(d), _ptr(self.table), _ptr(seg), nseg, _ptr(buf), buf.numel(),
-                                            _stream()), "es_attn_tiles_build")
+            rev_ptr, rev_pair = self.transpose(d.Nk if d.Nk > 0 else self.N)  # key-side lists of the backward
+            check(lib().es_attn_tiles_build(ct.byref(d), _ptr(self.table), _ptr(seg), nseg, _ptr(rev_ptr),
+                                            _ptr(rev_pair), _ptr(buf), buf.numel(), _stream()),
+                  "es_attn_tiles_build")
             cache[key] = buf
         return cache[key]
 
@@ -244,6 +246,8 @@ class AttentionConfig:
     value_mode: str = "eaas"
     phi: str = "cosine"
     box: tuple | None = None
+    bias: tuple | None = None  # radial score bias b(r) = b0 + b1 r + b2 r^2 (None: b == 0)
+    keep_scores: bool = True   # the forward keeps the O(N K H) scores for the backward
 
     def desc(self, N: int, K: int, C: int, dtype: torch.dtype, row0: int = 0, Nk: int = 0) -> _lib.AttnDesc:
         if self.value_mode not in _VALUE:
@@ -256,6 +260,11 @@ class AttentionConfig:
         d.phi_mode = _PHI[self.phi]
         d.dtype = _DT[dtype]
         d.r_cut = float(self.r_cut)
+        if self.bias is not None:
+            b = tuple(float(x) for x in self.bias) + (0.0,) * (3 - len(self.bias))
+            d.bias_mode = _lib.ES_BIAS_POLY2
+            for a in range(3):
+                d.bias[a] = b[a]
         d.periodic = 0 if self.box is None else 1
         if self.box is not None:
             for a in range(3):
@@ -276,6 +285,7 @@ class SavedAttention:
     lse: torch.Tensor
     cfg: AttentionConfig
     row0: int = 0
+    scores: torch.Tensor | None = None  # the forward's [N][K][H] scores (optional)
 
 
 def _check_qkv(q, k, v, pos, idx, cfg, row0=0):
@@ -303,19 +313,33 @@ def _check_qkv(q, k, v, pos, idx, cfg, row0=0):
     return N, C, Nk
 
 
-def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row0: int = 0):
-    """stream_aggregate (SPEC.md:275; Alg. 1): returns (m [N][M][C], lse [N][H] f32).
+def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row0: int = 0,
+                     return_scores: bool = False):
+    """stream_aggregate (SPEC.md:275; Alg. 1): returns (m [N][M][C], lse [N][H] f32)
+    -- plus the [N][K][H] scores (padding slots undefined) with return_scores.
     With row0 / k, v, pos longer than q: the query rows are atoms row0..row0+N-1
     of the Nk-atom system (query-row sharding)."""
     N, C, Nk = _check_qkv(q, k, v, pos, idx, cfg, row0)
     out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
+    scores = torch.empty((N, idx.K, cfg.heads), dtype=torch.float32, device=v.device) if return_scores else None
     d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
     tiles = idx.tiles(d)
     ws = _workspace(256 if tiles is not None else lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)
     check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
-                            _ptr(lse), _ptr(tiles), _ptr(ws), ws.numel(), _stream()), "es_attn_fwd")
+                            _ptr(lse), _ptr(scores), _ptr(tiles), _ptr(ws), ws.numel(), _stream()), "es_attn_fwd")
+    if return_scores:
+        return out, lse, scores
     return out, lse
+
+
+def attn_stats(cfg: AttentionConfig, N: int, K: int, C: int, n_pairs: int, dtype=torch.bfloat16, Nk: int = 0):
+    """OpCounters / stats structure (counters.hpp:11-32):
+    algorithmic multiply-adds and the auxiliary device memory of one layer."""
+    d = cfg.desc(N, K, C, dtype, 0, Nk)
+    st = _lib.AttnStats()
+    check(lib().es_attn_stats_query(ct.byref(d), int(n_pairs), ct.byref(st)), "es_attn_stats_query")
+    return {n: int(getattr(st, n)) for n, _ in st._fields_}
 
 
 def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_grad: bool = False):
@@ -336,7 +360,8 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_g
     dpos = torch.empty((Nk, 3), dtype=torch.float64, device=s.q.device) if pos_grad else None
     tiles = s.idx.tiles(d)
     check(lib().es_attn_bwd(ct.byref(d), _ptr(s.q), _ptr(s.k), _ptr(s.v), _ptr(s.pos), _ptr(s.idx.table),
-                            _ptr(rev_ptr), _ptr(rev_pair), _ptr(s.out), _ptr(s.lse), _ptr(grad_m), _ptr(dq),
+                            _ptr(rev_ptr), _ptr(rev_pair), _ptr(s.out), _ptr(s.lse), _ptr(s.scores), _ptr(grad_m),
+                            _ptr(dq),
                             _ptr(dk), _ptr(dv), _ptr(dpos), _ptr(tiles), _ptr(ws), ws.numel(), _stream()),
           "es_attn_bwd")
     return (dq, dk, dv, dpos) if pos_grad else (dq, dk, dv)

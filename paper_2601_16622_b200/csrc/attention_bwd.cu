@@ -45,7 +45,10 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 #ifndef ES_BWD_MINB
 #define ES_BWD_MINB 0
 #endif
-template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0, bool FORCE = false>
+// DK = false: dk is left to the tensor-core dk pass (attn_dk_tc_kernel), so the
+// gathered q_i rows are needed only for the score -- and not at all when the
+// forward's scores are supplied (p.scores_in).
+template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0, bool FORCE = false, bool DK = true>
 __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 : (L <= 2 ? 192 : 256)),
                                   (ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? ES_BWD_MINB : (L <= 2 ? 2 : 1)))
     attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
@@ -75,7 +78,7 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
   // k_j / v_j: this thread's channels staged once as fp32 in shared memory
   // ([mm][thread][2 CPL] and [mm][thread][CPL], conflict-free vector LDS)
   // instead of registers (halves the live state) or per-pair bf16 re-reads.
-  float dkr[M][2 * CPL], dvr[M][CPL];
+  float dkr[DK ? M : 1][2 * CPL], dvr[M][CPL];
   double fj[3] = {0.0, 0.0, 0.0};  // FORCE: this warp's share of dL/dpos_j
   const int nthr = blockDim.x;
   float* ks = recs + BP * REC;
@@ -96,8 +99,10 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
   }
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
+    if constexpr (DK) {
 #pragma unroll
-    for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = 0.f;
+      for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = 0.f;
+    }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) dvr[mm][c] = 0.f;
   }
@@ -121,28 +126,39 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
       // packed FFMA2 forms only for even CPL: with CPL = 1 (L = 4) the
       // register pairing they impose costs spills
       constexpr bool PK = CPL % 2 == 0;
-      float qv[M][2 * CPL];
-      float sc[2 * CPL];
+      float qv[DK ? M : 1][2 * CPL];
+      float score;
+      if (!DK && p.scores_in) {
+        score = p.scores_in[(size_t)pr * PH + head];
+      } else {
+        float sc[2 * CPL];
 #pragma unroll
-      for (int c = 0; c < 2 * CPL; ++c) sc[c] = 0.f;
+        for (int c = 0; c < 2 * CPL; ++c) sc[c] = 0.f;
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm) {
-        ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qv[mm]);
-        float kr[2 * CPL];
+        for (int mm = 0; mm < M; ++mm) {
+          float qt[2 * CPL];
+          ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qt);
+          if constexpr (DK) {
 #pragma unroll
-        for (int c = 0; c < 2 * CPL; ++c) kr[c] = ks[(mm * nthr + threadIdx.x) * 2 * CPL + c];
-        if constexpr (PK) {
-          fmav<2 * CPL>(qv[mm], kr, sc);
-        } else {
+            for (int c = 0; c < 2 * CPL; ++c) qv[mm][c] = qt[c];
+          }
+          float kr[2 * CPL];
 #pragma unroll
-          for (int c = 0; c < 2 * CPL; ++c) sc[0] = fmaf(qv[mm][c], kr[c], sc[0]);
+          for (int c = 0; c < 2 * CPL; ++c) kr[c] = ks[(mm * nthr + threadIdx.x) * 2 * CPL + c];
+          if constexpr (PK) {
+            fmav<2 * CPL>(qt, kr, sc);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2 * CPL; ++c) sc[0] = fmaf(qt[c], kr[c], sc[0]);
+          }
         }
-      }
-      float s = 0.f;
+        float s = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2 * CPL; ++c) s += sc[c];
-      for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const float P = expf(s * p.tau - lse[(size_t)i * PH + head]);
+        for (int c = 0; c < 2 * CPL; ++c) s += sc[c];
+        for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        score = fmaf(s, p.tau, rec[LY::OFF_B]);
+      }
+      const float P = expf(score - lse[(size_t)i * PH + head]);
       const float phi = rec[LY::OFF_PHI];
       float g[M][CPL], y[M][CPL];
 #pragma unroll
@@ -218,6 +234,10 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
           const float a = P * dphi * inv * dpr;
           gx = a * rx; gy = a * ry; gz = a * rz;
         }
+        {  // the score's radial bias: dL/dr += dscore b'(r) r^
+          const float bb = ds * rec[LY::OFF_DB] * inv;
+          gx = fmaf(bb, rx, gx); gy = fmaf(bb, ry, gy); gz = fmaf(bb, rz, gz);
+        }
         // every lane holds its head's value: sum the heads of this warp
         for (int o = lph; o < 32; o <<= 1) {
           gx += __shfl_xor_sync(0xffffffffu, gx, o);
@@ -232,14 +252,16 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
           fj[0] += gx; fj[1] += gy; fj[2] += gz;
         }
       }
-      const float tds = p.tau * ds;
+      if constexpr (DK) {
+        const float tds = p.tau * ds;
 #pragma unroll
-      for (int mm = 0; mm < M; ++mm) {
-        if constexpr (PK) {
-          fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
-        } else {
+        for (int mm = 0; mm < M; ++mm) {
+          if constexpr (PK) {
+            fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
+          } else {
 #pragma unroll
-          for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+            for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+          }
         }
       }
       if ((lane % lph) == 0) dsbuf[(size_t)pr * PH + head] = ds;
@@ -254,7 +276,7 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
   }
 #pragma unroll
   for (int mm = 0; mm < M; ++mm) {
-    stvec<2 * CPL>(dk + ((size_t)j * M + mm) * Dq + 2 * c0, dkr[mm]);
+    if constexpr (DK) stvec<2 * CPL>(dk + ((size_t)j * M + mm) * Dq + 2 * c0, dkr[mm]);
     stvec<CPL>(dv + ((size_t)j * M + mm) * PC + c0, dvr[mm]);
   }
 }
@@ -341,7 +363,7 @@ template <int L, int CPL, bool EAAS, typename T>
 es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
                   const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
                   const float* lse, const void* dout, void* dq, void* dk, void* dv, float* delta, float* dsbuf,
-                  double* dpos, bool skip_dq, cudaStream_t st) {
+                  double* dpos, bool skip_dq, bool skip_dk, cudaStream_t st) {
   constexpr int M = Lay<L>::M;
   if (dpos && L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
   const int g8 = (kp.C / kp.H) / 8;
@@ -366,6 +388,16 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
       s = cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)kp.Nk, st), "attn_bwd: dpos");
       if (s != ES_OK) return s;
     }
+  }
+  // dk on the tensor cores (the tcgen05 shape): the key pass keeps dv and the dscores only
+  if constexpr (L == 2 && CPL == 2 && EAAS && sizeof(T) == 2) {
+    if (skip_dk) {
+      if (kp.C != 128 || kp.H != 8) return fail(ES_CUDA_ERROR, "attn_bwd: tensor-core dk outside its shape");
+      fn = dpos ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 0, 0, true, false>
+                : attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8, false, false>;
+    }
+  } else {
+    if (skip_dk) return fail(ES_CUDA_ERROR, "attn_bwd: tensor-core dk outside its shape");
   }
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.Nk, threads, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, rev_ptr, rev_pair, lse,
@@ -393,6 +425,8 @@ KParams make_params(const AttnArgs& a) {
   kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
   kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
   kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];
+  kp.bias_mode = a.bias_mode; kp.b0 = a.bias[0]; kp.b1 = a.bias[1]; kp.b2 = a.bias[2];
+  kp.scores_out = a.scores_out; kp.scores_in = a.scores_in;
   return kp;
 }
 
@@ -430,11 +464,16 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
     if (dpos) return cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)a.Nk, st), "attn_bwd: dpos");
     return ES_OK;
   }
-  const bool tc_dq = attn_dq_tc_applicable(a);
+  const bool tc_dq = attn_dq_tc_applicable(a), tc_dk = attn_dk_tc_applicable(a);
   s = dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
-                      tc_dq, st);
-  if (s != ES_OK || !tc_dq) return s;
-  return attn_dq_tc_launch(a, k, nbr, dsbuf, dq, ws_tc, ws_tc_bytes, st);
+                      tc_dq, tc_dk, st);
+  if (s != ES_OK) return s;
+  if (tc_dq) {
+    s = attn_dq_tc_launch(a, k, nbr, dsbuf, dq, ws_tc, ws_tc_bytes, st);
+    if (s != ES_OK) return s;
+  }
+  if (tc_dk) s = attn_dk_tc_launch(a, q, nbr, rev_ptr, rev_pair, dsbuf, dk, ws_tc, ws_tc_bytes, st);
+  return s;
 }
 
 }  // namespace es

@@ -73,7 +73,9 @@ struct Lay {
   static constexpr int OFF_X = OFF_PHI + 2;  // spare (query slot in backward)
   static constexpr int OFF_DPHI = OFF_PHI + 3;  // dphi/dr (position gradients)
   static constexpr int OFF_R = OFF_PHI + 4;     // r_ij as fp32 (3)
-  static constexpr int REC = ((OFF_PHI + 7) + 3) / 4 * 4;
+  static constexpr int OFF_B = OFF_PHI + 7;     // radial score bias b(r_ij)
+  static constexpr int OFF_DB = OFF_PHI + 8;    // db/dr (position gradients)
+  static constexpr int REC = ((OFF_PHI + 9) + 3) / 4 * 4;
   static constexpr int BP = (L <= 2) ? 64 : 32;  // pairs per batch
 };
 
@@ -265,7 +267,19 @@ struct KParams {
   int phi_mode, periodic;
   float tau, r_cut, inv_rcut;
   double bx, by, bz;
+  int bias_mode;       // 0: b == 0; 1: b(r) = b0 + b1 r + b2 r^2 (RadialScalars b)
+  float b0, b1, b2;
+  float* scores_out;        // optional [N][K][H] scores of the valid slots (forward)
+  const float* scores_in;   // optional saved scores (backward)
 };
+
+// radial score bias and its r-derivative
+__device__ __forceinline__ float bias_of(const KParams& p, float rn) {
+  return p.bias_mode ? fmaf(fmaf(p.b2, rn, p.b1), rn, p.b0) : 0.f;
+}
+__device__ __forceinline__ float dbias_of(const KParams& p, float rn) {
+  return p.bias_mode ? fmaf(2.f * p.b2, rn, p.b1) : 0.f;
+}
 
 // Per-pair preparation (one thread): r_ij = pos_j - pos_i (double difference,
 // minimum image if periodic), phi, and for EAAS the frame / D^l / reindex
@@ -293,6 +307,8 @@ __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, i
   rec[Lay<L>::OFF_R] = rx;
   rec[Lay<L>::OFF_R + 1] = ry;
   rec[Lay<L>::OFF_R + 2] = rz;
+  rec[Lay<L>::OFF_B] = bias_of(p, rn);
+  rec[Lay<L>::OFF_DB] = dbias_of(p, rn);
   if constexpr (EAAS) {
     float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
     if (rn > 1e-8f) {

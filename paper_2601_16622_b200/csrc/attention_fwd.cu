@@ -57,7 +57,11 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
       for (int w = 0; w < warp; ++w) before += cnt_w[w];
       int tot = 0;
       for (int w = 0; w < (tpq >> 5); ++w) tot += cnt_w[w];
-      if (j >= 0) pair_prepare<L, EAAS>(p, pos, i, j, recs + (before + __popc(m & ((1u << lane) - 1u))) * REC);
+      if (j >= 0) {
+        float* rec = recs + (before + __popc(m & ((1u << lane) - 1u))) * REC;
+        pair_prepare<L, EAAS>(p, pos, i, j, rec);
+        rec[LY::OFF_X] = __int_as_float(base + t);  // slot (score store)
+      }
       nb += tot;
       __syncthreads();
     }
@@ -84,8 +88,8 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         s1 += __shfl_xor_sync(0xffffffffu, s1, o);
       }
       if ((lane % lph) == 0) {
-        sc[e * PH + head] = s0 * p.tau;
-        sc[(e + 1) * PH + head] = s1 * p.tau;
+        sc[e * PH + head] = fmaf(s0, p.tau, recs[e * REC + LY::OFF_B]);
+        sc[(e + 1) * PH + head] = fmaf(s1, p.tau, recs[(e + 1) * REC + LY::OFF_B]);
       }
     }
     for (; e < nb; ++e) {
@@ -99,9 +103,12 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qr[mm][c], kv[c], s);
       }
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((lane % lph) == 0) sc[e * PH + head] = s * p.tau;
+      if ((lane % lph) == 0) sc[e * PH + head] = fmaf(s, p.tau, recs[e * REC + LY::OFF_B]);
     }
     __syncwarp();
+    if (p.scores_out && (lane % lph) == 0)
+      for (int e2 = 0; e2 < nb; ++e2)
+        p.scores_out[((size_t)i * p.K + __float_as_int(recs[e2 * REC + LY::OFF_X])) * PH + head] = sc[e2 * PH + head];
     float bm = -INFINITY;
     for (int e2 = 0; e2 < nb; ++e2) bm = fmaxf(bm, sc[e2 * PH + head]);
     const float mu2 = fmaxf(mu, bm);
@@ -168,6 +175,8 @@ KParams make_params(const AttnArgs& a) {
   kp.phi_mode = a.phi_mode; kp.periodic = a.periodic;
   kp.tau = a.tau; kp.r_cut = a.r_cut; kp.inv_rcut = 1.f / a.r_cut;
   kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];
+  kp.bias_mode = a.bias_mode; kp.b0 = a.bias[0]; kp.b1 = a.bias[1]; kp.b2 = a.bias[2];
+  kp.scores_out = a.scores_out; kp.scores_in = a.scores_in;
   return kp;
 }
 

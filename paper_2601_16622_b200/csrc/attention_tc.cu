@@ -91,6 +91,10 @@ __device__ long long g_trace_r[4][128];  // row thread 64: before / after the Wt
 
 struct TcArgs {
   int N, K, row0, Nk;
+  int bias_mode;
+  float b0, b1, b2;
+  float* scores;       // optional [N][K][8] score store
+  const int* slots;    // the rows' ascending-j slot order (needed with scores)
   int dbg;  // profiling switches (ES_TC_DBG): 1 skip Vg math, 2 skip Wt math, 4 skip value MMA, 8 skip S MMA
   float tau, r_cut, inv_rcut;
   int phi_mode, periodic;
@@ -316,6 +320,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     int g0 = 0;
     for (int h = 0; h < 8; ++h) {
       float mu = -INFINITY, z = 0.f;
+      int rbase = 0;  // valid keys of the row in earlier chunks (rank -> slot for the score store)
       // this row's (chunk, key-mask) list, ascending chunk, 0xffff terminator
       const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * a.K;
       int rp = 0;
@@ -336,11 +341,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::tmem_ld16(t_s0 + 32 * b + lane_base, sr);
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
-        // identical in both halves (same scores, same instructions)
+        // scores s = tau q.k + b(r): identical in both halves (same scores, same instructions)
+        float svv[KC];
+#pragma unroll
+        for (int t = 0; t < KC; ++t) svv[t] = a.tau * __uint_as_float(sr[t]);
+        if (a.bias_mode && vmask) {  // radial bias: r_ij from the staged positions
+          const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
+#pragma unroll
+          for (int t = 0; t < KC; ++t)
+            if (vmask >> t & 1) {
+              double dx = kpos[3 * t] - qpos[3 * row], dy = kpos[3 * t + 1] - qpos[3 * row + 1],
+                     dz = kpos[3 * t + 2] - qpos[3 * row + 2];
+              if (a.periodic) {
+                dx -= a.bx * rint(dx / a.bx);
+                dy -= a.by * rint(dy / a.by);
+                dz -= a.bz * rint(dz / a.bz);
+              }
+              const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+              const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+              svv[t] += fmaf(fmaf(a.b2, rn, a.b1), rn, a.b0);
+            }
+        }
+        if (a.scores && qvalid) {  // keep the scores of my half's valid keys (slot order of the row)
+          const unsigned hmask = (vmask >> (8 * half)) & 0xffu;
+          if (hmask) {
+            const int* srow = a.slots + (size_t)qi * a.K;
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+              if (hmask >> t & 1) {
+                const int kk = 8 * half + t;
+                const int slot = __ldg(srow + rbase + __popc(vmask & ((1u << kk) - 1u)));
+                a.scores[((size_t)qi * a.K + slot) * 8 + h] = svv[kk];
+              }
+          }
+        }
+        rbase += __popc(vmask);
         float mc = -INFINITY;
 #pragma unroll
         for (int t = 0; t < KC; ++t)
-          if (vmask >> t & 1) mc = fmaxf(mc, a.tau * __uint_as_float(sr[t]));
+          if (vmask >> t & 1) mc = fmaxf(mc, svv[t]);
         const bool need = (mu > -INFINITY) && (mc > mu + 5.f);
         float factor = 1.f;
         if (mu == -INFINITY && mc > -INFINITY) mu = mc;
@@ -363,8 +402,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         float pw[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const float sv = half ? __uint_as_float(sr[8 + t]) : __uint_as_float(sr[t]);
-          pw[t] = (hm >> t & 1) ? __expf(a.tau * sv - mu) : 0.f;
+          const float sv = half ? svv[8 + t] : svv[t];
+          pw[t] = (hm >> t & 1) ? __expf(sv - mu) : 0.f;
           z += pw[t];
         }
         // ---- phase 1 (row-bound): P row -> smem, zero my half of the Wt row,
@@ -783,6 +822,53 @@ __global__ void tc_mask_kernel(int N, int K, const int32_t* __restrict__ nbr, co
   atomicOr(&mask[(size_t)rtile[t / K] * words + kb / 32], 1u << (kb % 32));
 }
 
+// ---------------------------------------------------------------- key-side lists (dk pass)
+// The transposed relation tiled the other way round: key tiles (rows = key
+// atoms), 16-query chunks.  Mask bit (key tile, query chunk) from the forward
+// table; per-key (chunk index << 16 | 16-bit query mask) entries from the
+// key's ascending rev_pair segment, stored CSR at rev_ptr[j] (a key has at
+// most as many entries as queries), terminated by 0xffff0000 when shorter.
+__global__ void tc_maskT_kernel(int N, int K, const int32_t* __restrict__ nbr, const int* __restrict__ rtileT,
+                                int words, uint32_t* __restrict__ mask) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)N * K) return;
+  const int j = nbr[t];
+  if (j < 0) return;
+  const int qc = (int)(t / K) / KC;
+  atomicOr(&mask[(size_t)rtileT[j] * words + qc / 32], 1u << (qc % 32));
+}
+
+__global__ void tc_rowlistT_kernel(int Nk, int K, const int* __restrict__ rev_ptr, const int* __restrict__ rev_pair,
+                                   const int* __restrict__ cptr, const int* __restrict__ clist,
+                                   const int* __restrict__ rtileT, uint32_t* __restrict__ rl) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= Nk) return;
+  const int t = rtileT[j], lo = cptr[t], n = cptr[t + 1] - lo;
+  const int e0 = rev_ptr[j], e1 = rev_ptr[j + 1];
+  auto idx = [&](int qc) {
+    int a = 0, b = n;
+    while (a < b) {
+      const int m = (a + b) >> 1;
+      if (clist[lo + m] < qc) a = m + 1;
+      else b = m;
+    }
+    return a;
+  };
+  int u = 0, cur = -1;
+  uint32_t msk = 0u;
+  for (int e = e0; e < e1; ++e) {
+    const int i = rev_pair[e] / K, qc = i / KC;
+    if (qc != cur) {
+      if (cur >= 0) rl[e0 + u++] = ((uint32_t)idx(cur) << 16) | msk;
+      cur = qc;
+      msk = 0u;
+    }
+    msk |= 1u << (i % KC);
+  }
+  if (cur >= 0) rl[e0 + u++] = ((uint32_t)idx(cur) << 16) | msk;
+  if (e0 + u < e1) rl[e0 + u] = 0xffff0000u;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -886,7 +972,9 @@ TcScratch tc_scratch(const AttnArgs& a) {
 }
 }  // namespace
 
-size_t attn_fwd_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(a).total : 0; }
+size_t attn_fwd_tc_workspace(const AttnArgs& a) {
+  return a.N > 0 ? tc_scratch(a).total + align256((size_t)a.N * a.K * 4) : 0;  // + slot order (score store)
+}
 
 namespace {
 struct TcLists {
@@ -976,13 +1064,17 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
   TcLists lists;
+  const int* slots = nullptr;
   if (a.tiles) {  // lists prebuilt for this neighbour index (es_attn_tiles_build)
     const TcPtrs pp = tc_ptrs(const_cast<void*>(a.tiles), t);
     lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles, pp.tstart};
+    slots = pp.slots;
   } else {
-    if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
-    s = tc_build_lists(a, nbr, ws, t, nullptr, &lists, st);
+    if (!ws || ws_bytes < attn_fwd_tc_workspace(a)) return fail(ES_INVALID_ARGUMENT, "attn_fwd: workspace too small");
+    int* sl = a.scores_out ? (int*)((char*)ws + t.total) : nullptr;
+    s = tc_build_lists(a, nbr, ws, t, sl, &lists, st);
     if (s != ES_OK) return s;
+    slots = sl;
   }
   const int ntiles = lists.ntiles;
   const int* cptr = lists.cptr;
@@ -1001,6 +1093,9 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   } ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
   ta.phi_mode = a.phi_mode; ta.periodic = a.periodic;
   ta.bx = a.box[0]; ta.by = a.box[1]; ta.bz = a.box[2];
+  ta.bias_mode = a.bias_mode; ta.b0 = a.bias[0]; ta.b1 = a.bias[1]; ta.b2 = a.bias[2];
+  ta.scores = a.scores_out;
+  ta.slots = slots;
   const int smem = SM_TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
@@ -1033,10 +1128,17 @@ constexpr int DQ_SM_STG = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;  // [4 warps][32 rows
 constexpr int DQ_SM_BAR = DQ_SM_STG + 4 * 32 * 80;
 constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 
-__global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
+// KEYS = false: dq (rows = query rows, chunks = key chunks, B = K chunk, dscores
+//   gathered through the row's ascending-j slot order);
+// KEYS = true: dk = tau dS^T Q (rows = key atoms, chunks = 16-query chunks of the
+//   transposed relation, B = Q chunk, dscores gathered through the key's
+//   ascending rev_pair entries -- the same ascending (chunk, bit) order).
+template <bool KEYS>
+__global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
     const __grid_constant__ CUtensorMap mk, int N, int K, float tau, const int* __restrict__ cptr,
     const int* __restrict__ clist, const uint32_t* __restrict__ rowlist, const int* __restrict__ slots,
-    const int* __restrict__ tstart, const float* __restrict__ dsbuf, bf16* __restrict__ dq) {
+    const int* __restrict__ tstart, const int* __restrict__ rev_ptr, const float* __restrict__ dsbuf,
+    bf16* __restrict__ dq) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DQ_SM_BAR);
@@ -1126,23 +1228,40 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
     const int qi = q0 + row;
     const bool qin = qi < q1;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t* rl = rowlist + (size_t)(qin ? qi : 0) * K;
-    const int* sl = slots + (size_t)(qin ? qi : 0) * K;
+    // the row's (chunk, mask) list, its gather order and the dscore row base
+    const uint32_t* rl;
+    const int* sl;
+    size_t gbase;
+    int lmax, nv = 0;
+    if constexpr (KEYS) {
+      const int e0 = qin ? rev_ptr[qi] : 0;
+      nv = qin ? rev_ptr[qi + 1] - e0 : 0;
+      rl = rowlist + e0;
+      sl = slots + e0;
+      gbase = 0;
+      lmax = nv;
+    } else {
+      rl = rowlist + (size_t)(qin ? qi : 0) * K;
+      sl = slots + (size_t)(qin ? qi : 0) * K;
+      gbase = (size_t)(qin ? qi : 0) * K;
+      lmax = K;
+      if (qin)
+        for (int u = 0; u < K; ++u) {  // valid pairs of the row (popcount over its chunk list)
+          const uint32_t e = __ldg(rl + u);
+          if ((e >> 16) == 0xffffu) break;
+          nv += __popc(e & 0xffffu);
+        }
+    }
     // this row's dscores, double buffered by head: head h+1's values are
-    // copied (cp.async, no registers) while head h's chunks run
+    // copied (cp.async, no registers) while head h's chunks run; a key with
+    // more than DQ_KMAX queries reads the excess directly
     float* dsr0 = reinterpret_cast<float*>(sm + DQ_SM_DS) + row * DQ_KMAX;
-    int nv = 0;  // valid pairs of the row (popcount over its chunk list)
-    if (qin)
-      for (int u = 0; u < K; ++u) {
-        const uint32_t e = __ldg(rl + u);
-        if ((e >> 16) == 0xffffu) break;
-        nv += __popc(e & 0xffffu);
-      }
+    const int npf = nv < DQ_KMAX ? nv : DQ_KMAX;
     auto fetch = [&](int hh) {
       float* dst = dsr0 + (hh & 1) * TQ * DQ_KMAX;
-      for (int r0 = 0; r0 < nv; ++r0)
+      for (int r0 = 0; r0 < npf; ++r0)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(umma::smem_u32(dst + r0)),
-                     "l"(dsbuf + ((size_t)qi * K + __ldg(sl + r0)) * 8 + hh)
+                     "l"(dsbuf + (gbase + __ldg(sl + r0)) * 8 + hh)
                      : "memory");
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -1157,20 +1276,23 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
       }
       const float* dsr = dsr0 + (h & 1) * TQ * DQ_KMAX;
       int rp = 0, r = 0;
-      uint32_t ent = qin ? __ldg(rl) : 0xffff0000u;
+      uint32_t ent = (qin && lmax > 0) ? __ldg(rl) : 0xffff0000u;
       for (int c = 0; c < nch; ++c, ++g) {
         const int b = g & 1;
         unsigned vmask = 0u;
         if ((int)(ent >> 16) == c) {
           vmask = ent & 0xffffu;
           ++rp;
-          ent = rp < K ? __ldg(rl + rp) : 0xffff0000u;
+          ent = rp < lmax ? __ldg(rl + rp) : 0xffff0000u;
         }
         float d[KC];
 #pragma unroll
         for (int t = 0; t < KC; ++t) {
           d[t] = 0.f;
-          if (vmask >> t & 1) d[t] = dsr[r++];
+          if (vmask >> t & 1) {
+            d[t] = r < DQ_KMAX ? dsr[r] : __ldg(dsbuf + (gbase + __ldg(sl + r)) * 8 + h);
+            ++r;
+          }
         }
         if (g >= 2) umma::mbar_wait(&a_free[b], ((g >> 1) - 1) & 1);
         uint8_t* at = sm + DQ_SM_A + b * DQ_ABYTES + (row >> 3) * 256 + (row & 7) * 16;
@@ -1179,7 +1301,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dq_tc_kernel(
         umma::fence_proxy_async();
         umma::mbar_arrive(&a_full[b]);
       }
-      // epilogue: dq[qi][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..]
+      // epilogue: out[row][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..]
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
       // staged, coalesced stores: 4 lanes write one row's 64 bytes
@@ -1260,30 +1382,107 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
   const int smem = DQ_SM_TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_dq_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_dqk_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_dq_tc_kernel<<<lists.ntiles, DQ_THREADS, smem, st>>>(mk, a.N, a.K, a.tau, lists.cptr, lists.clist,
-                                                           lists.rowlist, slots, lists.tstart, dsbuf, (bf16*)dq);
+  attn_dqk_tc_kernel<false><<<lists.ntiles, DQ_THREADS, smem, st>>>(mk, a.N, a.K, a.tau, lists.cptr, lists.clist,
+                                                                   lists.rowlist, slots, lists.tstart, nullptr,
+                                                                   dsbuf, (bf16*)dq);
   return cuda_status(cudaGetLastError(), "attn_dq_tc_kernel");
+}
+
+namespace {
+// the key-side problem: rows = the Nk key atoms, chunks over the N query rows
+AttnArgs key_side(const AttnArgs& a) {
+  AttnArgs b = a;
+  b.N = a.Nk;
+  b.Nk = a.N;
+  return b;
+}
+
+es_status tc_build_key_lists(const AttnArgs& a, const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair,
+                             void* ws, TcLists* out, cudaStream_t st, const int32_t* seg = nullptr, int nseg = 0) {
+  const AttnArgs b = key_side(a);
+  const TcScratch t = tc_scratch(b);
+  const TcPtrs pp = tc_ptrs(ws, t);
+  size_t cub_bytes = t.cub_bytes;
+  // key tiles: the query tiles' packing when keys and queries are the same atoms (molecule batches)
+  if (seg && nseg > 0 && a.N == a.Nk) tc_tiles_packed_kernel<<<1, 1024, 0, st>>>(b.N, nseg, seg, t.ntiles, pp.tstart);
+  else tc_tiles_uniform_kernel<<<(t.ntiles + 256) / 256, 256, 0, st>>>(b.N, t.ntiles, pp.tstart);
+  tc_rowtile_kernel<<<t.ntiles, 128, 0, st>>>(t.ntiles, pp.tstart, pp.rtile);
+  cudaMemsetAsync(pp.mask, 0, (size_t)t.ntiles * t.words * 4, st);
+  cudaMemsetAsync(pp.cnt, 0, (size_t)(t.ntiles + 1) * 4, st);
+  const size_t np = (size_t)a.N * a.K;
+  if (np > 0) tc_maskT_kernel<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, pp.rtile, t.words, pp.mask);
+  tc_count_kernel<<<(t.ntiles + 7) / 8, 256, 0, st>>>(t.ntiles, t.words, pp.mask, pp.cnt);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(pp.cub, cub_bytes, pp.cnt, pp.cptr, t.ntiles + 1, st);
+  if (e != cudaSuccess) return cuda_status(e, "attn_tc key scan");
+  tc_fill_kernel<<<(t.ntiles + 7) / 8, 256, 0, st>>>(t.ntiles, t.words, pp.mask, pp.cptr, pp.clist);
+  tc_rowlistT_kernel<<<(b.N + 127) / 128, 128, 0, st>>>(b.N, a.K, rev_ptr, rev_pair, pp.cptr, pp.clist, pp.rtile,
+                                                        pp.rowlist);
+  *out = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles, pp.tstart};
+  return cuda_status(cudaGetLastError(), "attn_tc key lists");
+}
+
+size_t tiles_query_bytes(const AttnArgs& a) { return tc_scratch(a).total + align256((size_t)a.N * a.K * 4); }
+
+}  // namespace
+
+bool attn_dk_tc_applicable(const AttnArgs& a) { return attn_dq_tc_applicable(a); }
+
+size_t attn_dk_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(key_side(a)).total : 0; }
+
+es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr, const int32_t* rev_ptr,
+                            const int32_t* rev_pair, const float* dsbuf, void* dk, void* ws, size_t ws_bytes,
+                            cudaStream_t st) {
+  if (a.N == 0) return ES_OK;
+  const TcScratch t = tc_scratch(key_side(a));
+  TcLists lists;
+  if (a.tiles) {  // key-side lists prebuilt after the query-side ones
+    const TcPtrs pp = tc_ptrs(const_cast<char*>(static_cast<const char*>(a.tiles)) + tiles_query_bytes(a), t);
+    lists = TcLists{pp.cptr, pp.clist, pp.rowlist, t.ntiles, pp.tstart};
+  } else {
+    if (!ws || ws_bytes < t.total) return fail(ES_INVALID_ARGUMENT, "attn_bwd: workspace too small (dk)");
+    es_status s = tc_build_key_lists(a, nbr, rev_ptr, rev_pair, ws, &lists, st);
+    if (s != ES_OK) return s;
+  }
+  CUtensorMap mq;
+  if (!map3(&mq, q, 256, MM, a.N, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B))
+    return fail(ES_CUDA_ERROR, "attn_dk_tc: tensor map encode failed");
+  const int smem = DQ_SM_TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_dqk_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  attn_dqk_tc_kernel<true><<<lists.ntiles, DQ_THREADS, smem, st>>>(mq, a.Nk, a.K, a.tau, lists.cptr, lists.clist,
+                                                                  lists.rowlist, rev_pair, lists.tstart, rev_ptr,
+                                                                  dsbuf, (bf16*)dk);
+  return cuda_status(cudaGetLastError(), "attn_dk_tc_kernel");
 }
 
 bool attn_tc_tiles_used(const AttnArgs& a) { return attn_dq_tc_applicable(a) || attn_fwd_workspace(a) > 0; }
 
 size_t attn_tc_tiles_bytes(const AttnArgs& a) {
   if (a.N <= 0) return 0;
-  return tc_scratch(a).total + align256((size_t)a.N * a.K * 4);
+  return tiles_query_bytes(a) + (attn_dk_tc_applicable(a) ? attn_dk_tc_workspace(a) : 0);
 }
 
 // The tile structures of one neighbour index, built once and reused by every
 // forward / backward (and every layer) that uses the same index.
-es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg, void* tiles,
-                              size_t bytes, cudaStream_t st) {
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg,
+                              const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
+                              cudaStream_t st) {
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
   if (!tiles || bytes < attn_tc_tiles_bytes(a)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: buffer too small");
+  const bool keys = attn_dk_tc_applicable(a);
+  if (keys && (!rev_ptr || !rev_pair))
+    return fail(ES_INVALID_ARGUMENT, "attn_tiles: the tensor-core backward needs rev_ptr / rev_pair (key-side lists)");
   TcLists lists;
-  return tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st, seg, nseg);
+  es_status s = tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st, seg, nseg);
+  if (s != ES_OK || !keys) return s;
+  return tc_build_key_lists(a, nbr, rev_ptr, rev_pair, (char*)tiles + tiles_query_bytes(a), &lists, st, seg, nseg);
 }
 
 }  // namespace es

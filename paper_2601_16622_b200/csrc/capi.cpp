@@ -66,6 +66,8 @@ AttnArgs to_args(const es_attn_desc* d) {
   a.tau = (float)(1.0 / std::sqrt((double)M * (a.Dq / d->H)));
   a.r_cut = (float)d->r_cut;
   for (int x = 0; x < 3; ++x) a.box[x] = d->box[x];
+  a.bias_mode = d->bias_mode;
+  for (int x = 0; x < 3; ++x) a.bias[x] = d->bias_mode ? (float)d->bias[x] : 0.f;
   return a;
 }
 
@@ -149,7 +151,8 @@ size_t es_attn_tiles_workspace_size(const es_attn_desc* d) {
 }
 
 es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const int32_t* seg_ptr, int32_t nseg,
-                              void* tiles, size_t bytes, void* stream) {
+                              const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
+                              void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
@@ -157,12 +160,13 @@ es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const i
     if (!attn_tc_tiles_used(a)) return ES_OK;  // the SIMT kernels need no tile lists
     if (d->N > 0 && !nbr) return fail(ES_INVALID_ARGUMENT, "attn_tiles: null buffer");
     if (nseg < 0 || (nseg > 0 && !seg_ptr)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: nseg > 0 needs seg_ptr");
-    return attn_tc_tiles_build(a, nbr, nseg > 0 ? seg_ptr : nullptr, nseg, tiles, bytes, (cudaStream_t)stream);
+    return attn_tc_tiles_build(a, nbr, nseg > 0 ? seg_ptr : nullptr, nseg, rev_ptr, rev_pair, tiles, bytes,
+                               (cudaStream_t)stream);
   });
 }
 
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
-                      const int32_t* nbr, void* out, float* lse, const void* tiles, void* workspace,
+                      const int32_t* nbr, void* out, float* lse, float* scores, const void* tiles, void* workspace,
                       size_t workspace_bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
@@ -175,6 +179,7 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
       return fail(ES_INVALID_ARGUMENT, "attn_fwd: pos must be 16-byte aligned");
     AttnArgs a = to_args(d);
     a.tiles = tiles;
+    a.scores_out = scores;
     return attn_fwd_launch(a, q, k, v, pos, nbr, out, lse, workspace, workspace_bytes, (cudaStream_t)stream);
   });
 }
@@ -186,13 +191,16 @@ static size_t bwd_base_bytes(const es_attn_desc* d) {
 size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
   if (!d || d->N <= 0 || check_attn(d) != ES_OK) return 256;
   const AttnArgs a = to_args(d);
-  return bwd_base_bytes(d) + (attn_dq_tc_applicable(a) ? attn_dq_tc_workspace(a) : 0);
+  size_t tc = 0;
+  if (attn_dq_tc_applicable(a)) tc = attn_dq_tc_workspace(a);
+  if (attn_dk_tc_applicable(a) && attn_dk_tc_workspace(a) > tc) tc = attn_dk_tc_workspace(a);  // run one after the other
+  return bwd_base_bytes(d) + tc;
 }
 
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair, const void* out,
-                      const float* lse, const void* dout, void* dq, void* dk, void* dv, double* dpos,
-                      const void* tiles, void* workspace, size_t workspace_bytes, void* stream) {
+                      const float* lse, const float* scores, const void* dout, void* dq, void* dk, void* dv,
+                      double* dpos, const void* tiles, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
@@ -223,6 +231,7 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
     const size_t base = bwd_base_bytes(d);
     AttnArgs a = to_args(d);
     a.tiles = tiles;
+    a.scores_in = scores;
     return attn_bwd_launch(a, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
                            (char*)workspace + base, workspace_bytes - base, (cudaStream_t)stream);
   });
@@ -300,6 +309,29 @@ static es_status check_proj(const es_proj_desc* d) {
   if (d->L < 0 || d->L > kMaxL) return fail(ES_UNSUPPORTED, "project: L must be in [0, 4]");
   if (d->dtype != ES_F32 && d->dtype != ES_BF16) return fail(ES_INVALID_ARGUMENT, "project: unknown dtype");
   return ES_OK;
+}
+
+es_status es_attn_stats_query(const es_attn_desc* d, int64_t n_pairs, es_attn_stats* out) {
+  return guarded([&] {
+    es_status s = check_attn(d);
+    if (s != ES_OK) return s;
+    if (!out || n_pairs < 0) return fail(ES_INVALID_ARGUMENT, "attn_stats: null output or negative pair count");
+    const uint64_t M = (uint64_t)(d->L + 1) * (d->L + 1), H = d->H, C = d->C, ch = C / H;
+    const uint64_t dk = 2 * M * C / H, E = (uint64_t)n_pairs, N = (uint64_t)d->N, K = (uint64_t)d->K;
+    std::memset(out, 0, sizeof(*out));
+    out->madds_fwd = E * H * (dk + ch * M * M);
+    out->madds_bwd = E * H * (3 * dk + 2 * ch * M * M);
+    out->madds_proj_fwd = N * M * C * 5 * C;
+    out->madds_proj_bwd = 2 * out->madds_proj_fwd;
+    // forward: (mu, z, A) live on chip (registers / TMEM), no floating-point scratch in HBM
+    out->aux_float_bytes_fwd = 0;
+    // backward: Delta [N][H] and the per-pair-head dscore [N][K][H] -- O(N K H), never O(N K C)
+    out->aux_float_bytes_bwd = 4 * N * H + 4 * N * K * H;
+    out->aux_index_bytes = es_attn_tiles_workspace_size(d);
+    out->workspace_fwd_bytes = es_attn_fwd_workspace_size(d);
+    out->workspace_bwd_bytes = es_attn_bwd_workspace_size(d);
+    return ES_OK;
+  });
 }
 
 es_status es_project_fwd(const es_proj_desc* d, const void* h, const void* W, void* q, void* k, void* v,

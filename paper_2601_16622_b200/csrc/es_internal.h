@@ -44,7 +44,11 @@ struct AttnArgs {
   int value_mode, phi_mode, dtype, periodic;
   float tau, r_cut;
   double box[3];
+  int bias_mode = 0;                 // es_bias_mode
+  float bias[3] = {0.f, 0.f, 0.f};   // b(r) = bias[0] + bias[1] r + bias[2] r^2
   const void* tiles = nullptr;  // prebuilt tile lists (es_attn_tiles_build) or NULL
+  float* scores_out = nullptr;       // es_attn_fwd: optional [N][K][H] scores
+  const float* scores_in = nullptr;  // es_attn_bwd: optional saved scores
 };
 
 size_t attn_fwd_workspace(const AttnArgs& a);
@@ -62,8 +66,15 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
 bool attn_dq_tc_applicable(const AttnArgs& a);
 bool attn_tc_tiles_used(const AttnArgs& a);    // the tcgen05 forward or dq would consume tile lists
 size_t attn_tc_tiles_bytes(const AttnArgs& a);
-es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg, void* tiles,
-                              size_t bytes, cudaStream_t st);
+es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg,
+                              const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
+                              cudaStream_t st);
+// tensor-core dk = tau dS^T Q over key tiles (key-side lists in the tiles buffer or the workspace)
+bool attn_dk_tc_applicable(const AttnArgs& a);
+size_t attn_dk_tc_workspace(const AttnArgs& a);
+es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr, const int32_t* rev_ptr,
+                            const int32_t* rev_pair, const float* dsbuf, void* dk, void* ws, size_t ws_bytes,
+                            cudaStream_t st);
 size_t attn_dq_tc_workspace(const AttnArgs& a);
 es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
                             void* ws, size_t ws_bytes, cudaStream_t st);

@@ -114,11 +114,13 @@ class CudaBackend:
 
     def attn_fwd(self, q_loc, k, v, pos, table_loc, row0):
         idx = self.api.NeighborIndex(table_loc, None, None, self.cfg.r_cut)
-        out, lse = self.api.stream_aggregate(q_loc, k, v, pos, idx, self.cfg, row0=row0)
+        out, lse, sc = self.api.stream_aggregate(q_loc, k, v, pos, idx, self.cfg, row0=row0, return_scores=True)
+        idx._scores = sc  # the forward's scores travel with the index to the backward
         return out, lse, idx
 
     def attn_bwd(self, g_loc, q_loc, k, v, pos, idx, out, lse, row0):
-        saved = self.api.SavedAttention(q_loc, k, v, pos, idx, out, lse, self.cfg, row0=row0)
+        saved = self.api.SavedAttention(q_loc, k, v, pos, idx, out, lse, self.cfg, row0=row0,
+                                        scores=getattr(idx, "_scores", None))
         return self.api.stream_aggregate_backward(g_loc, saved)
 
 

@@ -14,15 +14,16 @@ class _AttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, h, W, pos, idx: NeighborIndex, cfg: AttentionConfig):
         q, k, v = project_qk(h.contiguous(), W.contiguous(), cfg.L)
-        out, lse = stream_aggregate(q, k, v, pos, idx, cfg)
+        out, lse, scores = stream_aggregate(q, k, v, pos, idx, cfg, return_scores=cfg.keep_scores)
         ctx.save_for_backward(h, W, q, k, v, out, lse, pos)
+        ctx.scores = scores
         ctx.idx, ctx.cfg = idx, cfg
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
         h, W, q, k, v, out, lse, pos = ctx.saved_tensors
-        saved = SavedAttention(q, k, v, pos, ctx.idx, out, lse, ctx.cfg)
+        saved = SavedAttention(q, k, v, pos, ctx.idx, out, lse, ctx.cfg, scores=ctx.scores)
         want_pos = ctx.needs_input_grad[2]  # positions require grad: forces (L = 2)
         grads = stream_aggregate_backward(grad_out.contiguous().to(q.dtype), saved, pos_grad=want_pos)
         dq, dk, dv = grads[:3]

@@ -101,12 +101,45 @@ def test_invalid_arguments_and_no_cpu_fallback(eslib):
     from paper_2601_16622_b200 import _lib
     d = _lib.AttnDesc()
     d.N, d.K, d.H, d.L, d.C, d.r_cut = 4, 4, 3, 2, 64, 6.0  # C % H != 0
-    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 9), 0, None) == _lib.ES_INVALID_ARGUMENT
+    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 10), 0, None) == _lib.ES_INVALID_ARGUMENT
     assert b"multiple of H" in eslib.es_last_error()
     d.H, d.L = 8, 7
-    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 9), 0, None) == _lib.ES_UNSUPPORTED
+    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 10), 0, None) == _lib.ES_UNSUPPORTED
+    d.L, d.bias_mode = 2, 7  # unknown radial-bias form
+    assert eslib.es_attn_fwd(ct.byref(d), *([None] * 10), 0, None) == _lib.ES_INVALID_ARGUMENT
+    d.bias_mode = 0
     if not eslib.es_device_ok():
         import torch
         import paper_2601_16622_b200 as es
         with pytest.raises(ValueError):
             es.build_neighbors(torch.zeros(4, 3, dtype=torch.float64), 4, 6.0)  # CPU tensor: no fallback
+
+
+def test_stats_accounting(eslib):
+    """OpCounters / stats structure (counters.hpp:11-32):
+    algorithmic multiply-adds, forward floating-point scratch independent of K
+    (and zero: (mu, z, A) live on chip), backward scratch O(N K H) -- never
+    O(N K C) -- and every memory term exactly linear in N."""
+    from paper_2601_16622_b200 import api
+    cfg = api.AttentionConfig(heads=8, L=2)
+    st = api.attn_stats(cfg, 1000, 64, 128, 13600)
+    dk, ch, M = 2 * 9 * 128 // 8, 16, 9
+    assert st["madds_fwd"] == 13600 * 8 * (dk + ch * M * M)
+    assert st["madds_bwd"] == 13600 * 8 * (3 * dk + 2 * ch * M * M)
+    assert st["madds_proj_fwd"] == 1000 * 9 * 128 * 5 * 128
+    for K in (16, 32, 64):
+        assert api.attn_stats(cfg, 1000, K, 128, 13600)["aux_float_bytes_fwd"] == 0
+    # backward scratch: no C dependence (C = 64 vs 128), linear in K * H
+    b64 = api.attn_stats(cfg, 1000, 64, 64, 0)["aux_float_bytes_bwd"]
+    b128 = api.attn_stats(cfg, 1000, 64, 128, 0)["aux_float_bytes_bwd"]
+    assert b64 == b128 == 4 * 1000 * 8 + 4 * 1000 * 64 * 8
+    # linear in N with R^2 > 0.999 (SPEC.md:462) for every byte count
+    Ns = np.array([1000, 5000, 20000, 50000, 100000], dtype=np.float64)
+    for key in ("aux_float_bytes_bwd", "workspace_bwd_bytes", "workspace_fwd_bytes", "aux_index_bytes"):
+        ys = np.array([api.attn_stats(cfg, int(n), 64, 128, 0)[key] for n in Ns], dtype=np.float64)
+        if ys.max() == ys.min():  # constant (e.g. no tensor-core tiles without a device): trivially K-free
+            continue
+        A = np.vstack([Ns, np.ones_like(Ns)]).T
+        coef, res, *_ = np.linalg.lstsq(A, ys, rcond=None)
+        r2 = 1 - float(((A @ coef - ys) ** 2).sum()) / float(((ys - ys.mean()) ** 2).sum())
+        assert r2 > 0.999, (key, r2)

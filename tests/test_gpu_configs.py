@@ -215,3 +215,101 @@ def test_unaligned_positions_rejected(es):
     out, _ = es.stream_aggregate(q, q, v, aligned_positions(pos), idx, cfg)
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
+
+
+# ------------------------------------------------------------------ radial bias b(r) and kept scores
+def _attn_case(N, L, C, H, seed, seg=False):
+    if seg:
+        b = S.molecule_batch(N, 40, 60, seed)
+        pos, sp = b.pos, b.seg_ptr
+    else:
+        pos, sp = S.gen_fcc_system(N, 3.8, seed), None
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0, seg_ptr=sp)
+    n = len(pos)
+    q, k, v = po.project(S.random_features(n, L, C, seed), S.random_weights(L, C, seed), L)
+    return pos, sp, nbr, q, k, v
+
+
+@pytest.mark.parametrize("dtype,tol,seg", [(torch.float32, 1e-5, False), (torch.bfloat16, BF16_TOL, True)])
+def test_radial_bias_fwd_bwd(es, oracle, dtype, tol, seg):
+    """s_ij = tau q.k + b(r_ij), b(r) = b0 + b1 r + b2 r^2 (RadialScalars,
+    SPEC.md:247-250, Eq. 18): SIMT fp32 path and the bf16 tcgen05 path
+    (forward, kept scores, dq / dk tensor-core passes) against the oracle."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    L, C, H = 2, 128 if seg else 64, 8
+    pos, sp, nbr, q, k, v = _attn_case(12 if seg else 90, L, C, H, 7, seg)
+    if dtype == torch.bfloat16:
+        q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    bias = (0.4, -0.3, 0.06)
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, bias=bias)
+    ro, rl = po.attn_fwd(P, q, k, v, pos, nbr)
+    g = np.random.default_rng(2).standard_normal(ro.shape)
+    if dtype == torch.bfloat16:
+        g = torch.tensor(g).bfloat16().double().numpy()
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, ro, rl, g)
+    cfg = AttentionConfig(heads=H, L=L, bias=bias)
+    idx = NeighborIndex(dev(nbr), None, None, 6.0, seg_ptr=None if sp is None else dev(sp))
+    tq, tk, tv, tp = dev(q, dtype), dev(k, dtype), dev(v, dtype), dev(pos)
+    out, lse, sc = es.stream_aggregate(tq, tk, tv, tp, idx, cfg, return_scores=True)
+    grads = es.stream_aggregate_backward(dev(g, dtype), SavedAttention(tq, tk, tv, tp, idx, out, lse, cfg, scores=sc))
+    torch.cuda.synchronize()
+    assert rel(d64(out), ro) < tol
+    for a_, b_ in zip(grads, (rdq, rdk, rdv)):
+        assert rel(d64(a_), b_) < tol
+    # the kept scores are the oracle's scores on the valid slots
+    valid = nbr >= 0
+    i_idx, s_idx = np.nonzero(valid)
+    j_idx = nbr[valid]
+    rs = np.empty((len(i_idx), H))
+    M = (L + 1) ** 2
+    dqh = 2 * C // H
+    tau = 1.0 / np.sqrt(M * dqh)
+    rvec = pos[j_idx] - pos[i_idx]
+    rn = np.linalg.norm(rvec, axis=1)
+    for h in range(H):
+        sl = slice(h * dqh, (h + 1) * dqh)
+        rs[:, h] = tau * np.einsum("pmc,pmc->p", q[i_idx][:, :, sl], k[j_idx][:, :, sl]) + bias[0] + bias[1] * rn \
+            + bias[2] * rn ** 2
+    got = sc.cpu().numpy()[i_idx, s_idx]
+    assert np.abs(got - rs).max() < (1e-4 if dtype == torch.float32 else 2e-2 * np.abs(rs).max())
+
+
+def test_softmax_shift_invariance_through_bias(es, oracle):
+    """scores shifted by a constant b absorb into the softmax --
+    the stream output equals the unshifted one (oracle: double, 1e-10; fp32
+    GPU: 1e-5 at a shift of 10, finite and 5e-3 at 1e4, where an fp32 score
+    keeps ~1e-3 absolute resolution)."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex
+    L, C, H = 2, 64, 8
+    pos, sp, nbr, q, k, v = _attn_case(80, L, C, H, 3)
+    r0, _ = po.attn_fwd(po.AttnProblem(L=L, H=H), q, k, v, pos, nbr)
+    r1, _ = po.attn_fwd(po.AttnProblem(L=L, H=H, bias=(1e4,)), q, k, v, pos, nbr)
+    assert rel(r1, r0) < 1e-10
+    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    args = (dev(q, torch.float32), dev(k, torch.float32), dev(v, torch.float32), dev(pos), idx)
+    o0, _ = es.stream_aggregate(*args, AttentionConfig(heads=H, L=L))
+    for shift, tol in ((10.0, 1e-5), (1e4, 5e-3)):
+        o1, l1 = es.stream_aggregate(*args, AttentionConfig(heads=H, L=L, bias=(shift,)))
+        torch.cuda.synchronize()
+        assert torch.isfinite(o1).all() and torch.isfinite(l1[l1 > -1e30]).all()
+        assert rel(d64(o1), d64(o0)) < tol
+
+
+def test_tensor_core_backward_without_prebuilt_tiles(es, oracle):
+    """es_attn_bwd with tiles = NULL builds the query- and key-side lists in its
+    workspace (dq and dk tcgen05 passes) -- same gradients as with prebuilt tiles."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    L, C, H = 2, 128, 8
+    pos, sp, nbr, q, k, v = _attn_case(14, L, C, H, 9, seg=True)
+    cfg = AttentionConfig(heads=H, L=L)
+    tq, tk, tv, tp = dev(q, torch.bfloat16), dev(k, torch.bfloat16), dev(v, torch.bfloat16), dev(pos)
+    idx = NeighborIndex(dev(nbr), None, None, 6.0, seg_ptr=dev(sp))
+    out, lse = es.stream_aggregate(tq, tk, tv, tp, idx, cfg)
+    g = dev(np.random.default_rng(1).standard_normal(tuple(out.shape)), torch.bfloat16)
+    ref = es.stream_aggregate_backward(g, SavedAttention(tq, tk, tv, tp, idx, out, lse, cfg))
+    bare = NeighborIndex(dev(nbr), None, None, 6.0)
+    bare.tiles = lambda d: None  # no prebuilt lists: the backward builds them per call
+    got = es.stream_aggregate_backward(g, SavedAttention(tq, tk, tv, tp, bare, out, lse, cfg))
+    torch.cuda.synchronize()
+    for a_, b_ in zip(got, ref):  # uniform vs segment-packed tiles: same sums, other fp32 order, bf16 outputs
+        assert rel(d64(a_), d64(b_)) < 1e-2
