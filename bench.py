@@ -46,6 +46,8 @@ sys.path.insert(0, ROOT)
 METRIC = "fused equivariant-attention fwd+bwd TFLOPS & latency vs N atoms at 1/2/4/8 B200"
 K_, RCUT = 64, 6.0
 GATE_TOL = 2e-2  # north_star: bf16-input paths <= 2e-2 with fp32 accumulation
+# the forward keeps its scores for the backward only with the tensor-core dk pass (ES_DK_TC=1)
+KEEP_SCORES = os.environ.get("ES_DK_TC", "0") == "1"
 
 
 def flops_per_step(n_atoms: int, n_pairs: int, L: int, C: int, H: int) -> dict:
@@ -123,6 +125,8 @@ def kernel_times(fn) -> dict:
 
 
 def short_name(n: str) -> str:
+    if "attn_dqk_tc_kernel" in n:
+        return "attn_dk_tc" if "<true>" in n else "attn_dq_tc"
     for key in ("attn_fwd_tc", "attn_bwd_q_tc", "attn_bwd_k_tc", "attn_bwd_kv", "attn_dq_tc", "attn_delta",
                 "attn_fwd_kernel", "attn_bwd_q_kernel", "proj_fwd_tc", "proj_dh_tc", "proj_dw_tc", "proj_fwd_kernel",
                 "proj_bwd", "nbr_segment", "nbr_grid", "tr_sort", "tr_fill", "tr_count", "tc_rowlist", "tc_tiles",
@@ -276,7 +280,8 @@ class Workload:
         idx = es.build_neighbors(pos, K_, RCUT, seg, box=self.box, with_distances=False)
         idx.transpose()
         q, k, v = es.project_qk(h, W, self.L)
-        out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, self.cfg, return_scores=True)
+        out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, self.cfg, return_scores=True) if KEEP_SCORES else \
+            (*es.stream_aggregate(q, k, v, pos, idx, self.cfg), None)
         dq, dk, dv = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, self.cfg,
                                                                       scores=sc))
         dh, dW = es.project_qk_backward(h, W, self.L, dq, dk, dv)
@@ -530,15 +535,17 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
         q, k, v = es.project_qk(h, W, L)
         idx = es.build_neighbors(pos, K_, RCUT, seg, box=wl.box, with_distances=False)
         idx.transpose()
-        out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True)
+        fwd = lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=KEEP_SCORES)  # noqa: E731
+        res = fwd()
+        out, lse, sc = res if KEEP_SCORES else (*res, None)
         saved = SavedAttention(q, k, v, pos, idx, out, lse, wl.cfg, scores=sc)
         dq, dk, dv = es.stream_aggregate_backward(out, saved)
-        t = {"attn_fwd": time_call(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True)),
+        t = {"attn_fwd": time_call(fwd),
              "attn_bwd": time_call(lambda: es.stream_aggregate_backward(out, saved)),
              "proj_fwd": time_call(lambda: es.project_qk(h, W, L)),
              "proj_bwd": time_call(lambda: es.project_qk_backward(h, W, L, dq, dk, dv))}
         kt_bwd = kernel_times(lambda: es.stream_aggregate_backward(out, saved))
-        kt_fwd = kernel_times(lambda: es.stream_aggregate(q, k, v, pos, idx, wl.cfg, return_scores=True))
+        kt_fwd = kernel_times(fwd)
         roof = roofline(wl, t, kt_fwd, kt_bwd, kt, n_loc, E, s_bytes, fl, ms)
     line = {
         "metric": METRIC,

@@ -127,10 +127,12 @@ es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const i
  * tiles == NULL; 256 bytes for the SIMT kernels).  Caller-owned, reusable
  * across calls on the same stream; the library allocates nothing. */
 size_t es_attn_fwd_workspace_size(const es_attn_desc* d);
-/* scores (optional, NULL = not kept): [N][K][H] float32, the scores s_ij =
- * tau q_i.k_j + b(r_ij) of the valid slots (padding slots untouched) -- the
- * O(N K H) scalars es_attn_bwd can reuse instead of recomputing q_i.k_j
- * (never O(N K C)).  pos must be 16-byte aligned. */
+/* scores (optional, NULL = not kept): N*K*H float32 -- the scores s_ij =
+ * tau q_i.k_j + b(r_ij) of the valid pairs, the O(N K H) scalars es_attn_bwd
+ * can reuse instead of recomputing q_i.k_j (never O(N K C)).
+ * Layout [H][N][K] with a row's valid pairs in its first count entries; their
+ * order within the row is private to the library (pass the buffer back to
+ * es_attn_bwd unchanged).  pos must be 16-byte aligned. */
 es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,
                       const int32_t* nbr, void* out, float* lse, float* scores, const void* tiles, void* workspace,
                       size_t workspace_bytes, void* stream);

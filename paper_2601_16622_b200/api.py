@@ -247,7 +247,7 @@ class AttentionConfig:
     phi: str = "cosine"
     box: tuple | None = None
     bias: tuple | None = None  # radial score bias b(r) = b0 + b1 r + b2 r^2 (None: b == 0)
-    keep_scores: bool = True   # the forward keeps the O(N K H) scores for the backward
+    keep_scores: bool = False  # the forward keeps the O(N K H) scores for the backward (pays with ES_DK_TC=1)
 
     def desc(self, N: int, K: int, C: int, dtype: torch.dtype, row0: int = 0, Nk: int = 0) -> _lib.AttnDesc:
         if self.value_mode not in _VALUE:
@@ -316,13 +316,15 @@ def _check_qkv(q, k, v, pos, idx, cfg, row0=0):
 def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row0: int = 0,
                      return_scores: bool = False):
     """stream_aggregate (SPEC.md:275; Alg. 1): returns (m [N][M][C], lse [N][H] f32)
-    -- plus the [N][K][H] scores (padding slots undefined) with return_scores.
+    -- plus the [H][N][K] scores with return_scores (a row's valid scores in its
+    first count entries, in a library-private order; pass them back to
+    stream_aggregate_backward through SavedAttention.scores).
     With row0 / k, v, pos longer than q: the query rows are atoms row0..row0+N-1
     of the Nk-atom system (query-row sharding)."""
     N, C, Nk = _check_qkv(q, k, v, pos, idx, cfg, row0)
     out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
-    scores = torch.empty((N, idx.K, cfg.heads), dtype=torch.float32, device=v.device) if return_scores else None
+    scores = torch.empty((cfg.heads, N, idx.K), dtype=torch.float32, device=v.device) if return_scores else None
     d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
     tiles = idx.tiles(d)
     ws = _workspace(256 if tiles is not None else lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)

@@ -117,6 +117,7 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
       pair_prepare<L, EAAS>(p, pos, i, j, rec);
       rec[LY::OFF_J] = __int_as_float(i);
       rec[LY::OFF_X] = __int_as_float(pr);
+      if (p.scores_in) rec[LY::OFF_SI] = __int_as_float(p.rank_of ? i * p.K + __ldg(p.rank_of + pr) : pr);
     }
     __syncthreads();
     for (int e = 0; e < nb; ++e) {
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
       float qv[DK ? M : 1][2 * CPL];
       float score;
       if (!DK && p.scores_in) {
-        score = p.scores_in[(size_t)pr * PH + head];
+        score = p.scores_in[(size_t)head * p.N * p.K + __float_as_int(rec[LY::OFF_SI])];  // [H][N][K]
       } else {
         float sc[2 * CPL];
 #pragma unroll
@@ -427,6 +428,7 @@ KParams make_params(const AttnArgs& a) {
   kp.bx = a.box[0]; kp.by = a.box[1]; kp.bz = a.box[2];
   kp.bias_mode = a.bias_mode; kp.b0 = a.bias[0]; kp.b1 = a.bias[1]; kp.b2 = a.bias[2];
   kp.scores_out = a.scores_out; kp.scores_in = a.scores_in;
+  kp.rank_of = nullptr;
   return kp;
 }
 
@@ -459,20 +461,27 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
                           float* dsbuf, double* dpos, void* ws_tc, size_t ws_tc_bytes, cudaStream_t st) {
   es_status s = upload_tables_tu();
   if (s != ES_OK) return s;
-  const KParams kp = make_params(a);
   if (a.N == 0) {
     if (dpos) return cuda_status(cudaMemsetAsync(dpos, 0, sizeof(double) * 3 * (size_t)a.Nk, st), "attn_bwd: dpos");
     return ES_OK;
   }
   const bool tc_dq = attn_dq_tc_applicable(a), tc_dk = attn_dk_tc_applicable(a);
-  s = dispatch<BwdOp>(a, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
+  AttnArgs at = a;
+  if (tc_dq && !at.tiles) {  // no prebuilt tile lists: build query- and key-side lists in the workspace first
+    s = attn_tc_tiles_build(at, nbr, nullptr, 0, rev_ptr, rev_pair, ws_tc, ws_tc_bytes, st);
+    if (s != ES_OK) return s;
+    at.tiles = ws_tc;
+  }
+  KParams kp = make_params(at);
+  if (tc_dq && kp.scores_in) kp.rank_of = attn_tc_rank_of(at, at.tiles);  // the tensor-core forward's rank space
+  s = dispatch<BwdOp>(at, kp, q, k, v, pos, nbr, rev_ptr, rev_pair, out, lse, dout, dq, dk, dv, delta, dsbuf, dpos,
                       tc_dq, tc_dk, st);
   if (s != ES_OK) return s;
   if (tc_dq) {
-    s = attn_dq_tc_launch(a, k, nbr, dsbuf, dq, ws_tc, ws_tc_bytes, st);
+    s = attn_dq_tc_launch(at, k, nbr, dsbuf, dq, nullptr, 0, st);
     if (s != ES_OK) return s;
   }
-  if (tc_dk) s = attn_dk_tc_launch(a, q, nbr, rev_ptr, rev_pair, dsbuf, dk, ws_tc, ws_tc_bytes, st);
+  if (tc_dk) s = attn_dk_tc_launch(at, q, nbr, rev_ptr, rev_pair, dsbuf, dk, nullptr, 0, st);
   return s;
 }
 

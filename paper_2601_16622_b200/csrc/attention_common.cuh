@@ -75,7 +75,8 @@ struct Lay {
   static constexpr int OFF_R = OFF_PHI + 4;     // r_ij as fp32 (3)
   static constexpr int OFF_B = OFF_PHI + 7;     // radial score bias b(r_ij)
   static constexpr int OFF_DB = OFF_PHI + 8;    // db/dr (position gradients)
-  static constexpr int REC = ((OFF_PHI + 9) + 3) / 4 * 4;
+  static constexpr int OFF_SI = OFF_PHI + 9;    // backward: the pair's index into the saved scores
+  static constexpr int REC = ((OFF_PHI + 10) + 3) / 4 * 4;
   static constexpr int BP = (L <= 2) ? 64 : 32;  // pairs per batch
 };
 
@@ -271,6 +272,7 @@ struct KParams {
   float b0, b1, b2;
   float* scores_out;        // optional [N][K][H] scores of the valid slots (forward)
   const float* scores_in;   // optional saved scores (backward)
+  const int* rank_of;       // saved scores in rank space (tensor-core forward): slot -> rank, else NULL
 };
 
 // radial score bias and its r-derivative

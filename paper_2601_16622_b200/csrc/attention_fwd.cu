@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
     __syncwarp();
     if (p.scores_out && (lane % lph) == 0)
       for (int e2 = 0; e2 < nb; ++e2)
-        p.scores_out[((size_t)i * p.K + __float_as_int(recs[e2 * REC + LY::OFF_X])) * PH + head] = sc[e2 * PH + head];
+        p.scores_out[((size_t)head * p.N + i) * p.K + __float_as_int(recs[e2 * REC + LY::OFF_X])] = sc[e2 * PH + head];
     float bm = -INFINITY;
     for (int e2 = 0; e2 < nb; ++e2) bm = fmaxf(bm, sc[e2 * PH + head]);
     const float mu2 = fmaxf(mu, bm);

@@ -94,12 +94,27 @@ struct TcArgs {
   int bias_mode;
   float b0, b1, b2;
   float* scores;       // optional [N][K][8] score store
+  int score_rank;      // 1: scores indexed by (row, rank) -- the rank_of map of the tiles resolves slots
   const int* slots;    // the rows' ascending-j slot order (needed with scores)
   int dbg;  // profiling switches (ES_TC_DBG): 1 skip Vg math, 2 skip Wt math, 4 skip value MMA, 8 skip S MMA
   float tau, r_cut, inv_rcut;
   int phi_mode, periodic;
   double bx, by, bz;
 };
+
+// b(r_ij) of one pair from the staged key / query positions (kept out of line: the
+// softmax phase it serves is register-bound)
+__device__ __forceinline__ float tc_pair_bias(const TcArgs& a, const double* kp, const double* qp) {
+  double dx = kp[0] - qp[0], dy = kp[1] - qp[1], dz = kp[2] - qp[2];
+  if (a.periodic) {
+    dx -= a.bx * rint(dx / a.bx);
+    dy -= a.by * rint(dy / a.by);
+    dz -= a.bz * rint(dz / a.bz);
+  }
+  const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+  const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+  return fmaf(fmaf(a.b2, rn, a.b1), rn, a.b0);
+}
 
 __device__ __forceinline__ void solid_l2(float x, float y, float z, float* Y) {
   const float r2 = x * x + y * y + z * z;
@@ -141,6 +156,7 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 // while the current head runs), O [288,432), S[2] [448,464) / [480,496).
 constexpr int TC_THREADS = 448;
 
+template <bool BIAS>
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
@@ -342,27 +358,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::tc_fence_before();
         umma::mbar_arrive(&s_free[b]);
         // scores s = tau q.k + b(r): identical in both halves (same scores, same instructions)
-        float svv[KC];
+        // (in place: sr[t] becomes the score bits -- no second 16-register array)
+#define svv(t) __uint_as_float(sr[t])
 #pragma unroll
-        for (int t = 0; t < KC; ++t) svv[t] = a.tau * __uint_as_float(sr[t]);
-        if (a.bias_mode && vmask) {  // radial bias: r_ij from the staged positions
-          const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
+        for (int t = 0; t < KC; ++t) sr[t] = __float_as_uint(a.tau * __uint_as_float(sr[t]));
+        if constexpr (BIAS) {  // radial bias: r_ij from the staged positions (separate instantiation: registers)
+          if (vmask) {
+            const double* kpos = reinterpret_cast<const double*>(sm + SM_POS + st * PBYTES);
 #pragma unroll
-          for (int t = 0; t < KC; ++t)
-            if (vmask >> t & 1) {
-              double dx = kpos[3 * t] - qpos[3 * row], dy = kpos[3 * t + 1] - qpos[3 * row + 1],
-                     dz = kpos[3 * t + 2] - qpos[3 * row + 2];
-              if (a.periodic) {
-                dx -= a.bx * rint(dx / a.bx);
-                dy -= a.by * rint(dy / a.by);
-                dz -= a.bz * rint(dz / a.bz);
-              }
-              const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
-              const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
-              svv[t] += fmaf(fmaf(a.b2, rn, a.b1), rn, a.b0);
-            }
+            for (int t = 0; t < KC; ++t)
+              if (vmask >> t & 1) sr[t] = __float_as_uint(svv(t) + tc_pair_bias(a, kpos + 3 * t, qpos + 3 * row));
+          }
         }
-        if (a.scores && qvalid) {  // keep the scores of my half's valid keys (slot order of the row)
+        if (a.scores && qvalid) {  // keep the scores of my half's valid keys
           const unsigned hmask = (vmask >> (8 * half)) & 0xffu;
           if (hmask) {
             const int* srow = a.slots + (size_t)qi * a.K;
@@ -370,8 +378,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
             for (int t = 0; t < 8; ++t)
               if (hmask >> t & 1) {
                 const int kk = 8 * half + t;
-                const int slot = __ldg(srow + rbase + __popc(vmask & ((1u << kk) - 1u)));
-                a.scores[((size_t)qi * a.K + slot) * 8 + h] = svv[kk];
+                const int rank = rbase + __popc(vmask & ((1u << kk) - 1u));  // ascending-j position of the key
+                // rank space (the tensor-core backward maps slots through rank_of) or slot space
+                const int col = a.score_rank ? rank : __ldg(srow + rank);
+                // head-major [H][N][K]: a row's scores of one head fill whole sectors within one head pass
+                a.scores[((size_t)h * a.N + qi) * a.K + col] = half ? svv(8 + t) : svv(t);  // static indices
               }
           }
         }
@@ -379,7 +390,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         float mc = -INFINITY;
 #pragma unroll
         for (int t = 0; t < KC; ++t)
-          if (vmask >> t & 1) mc = fmaxf(mc, svv[t]);
+          if (vmask >> t & 1) mc = fmaxf(mc, svv(t));
         const bool need = (mu > -INFINITY) && (mc > mu + 5.f);
         float factor = 1.f;
         if (mu == -INFINITY && mc > -INFINITY) mu = mc;
@@ -402,10 +413,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         float pw[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
-          const float sv = half ? svv[8 + t] : svv[t];
+          const float sv = half ? svv(8 + t) : svv(t);
           pw[t] = (hm >> t & 1) ? __expf(sv - mu) : 0.f;
           z += pw[t];
         }
+#undef svv
         // ---- phase 1 (row-bound): P row -> smem, zero my half of the Wt row,
         // per-row valid masks + quadrant-local prefix counts (half 0)
         const int pb = g & 1;  // phase-2 tables double buffered by chunk parity
@@ -630,7 +642,7 @@ __global__ void tc_fill_kernel(int ntiles, int words, const uint32_t* __restrict
 // dscore gathers.
 __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
                                   const int* __restrict__ clist, const int* __restrict__ rtile,
-                                  uint32_t* __restrict__ rl, int* __restrict__ slots) {
+                                  uint32_t* __restrict__ rl, int* __restrict__ slots, int* __restrict__ rank_of) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
   const int t = rtile[i], lo = cptr[t], n = cptr[t + 1] - lo;
@@ -663,6 +675,8 @@ __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, con
     }
   }
   if (cnt < K) o[cnt] = 0xffff0000u;
+  if (slots && rank_of)
+    for (int r = 0; r < nv; ++r) rank_of[(size_t)i * K + slots[(size_t)i * K + r]] = r;
 }
 
 // Warp-per-row list builder for K <= 64 (two slots per lane): each valid
@@ -674,7 +688,8 @@ __global__ void tc_rowlist_kernel(int N, int K, const int* __restrict__ nbr, con
 // chunks plus the key bits below its own.
 __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr, const int* __restrict__ cptr,
                                        const int* __restrict__ clist, const int* __restrict__ rtile,
-                                       uint32_t* __restrict__ rl, int* __restrict__ slots) {
+                                       uint32_t* __restrict__ rl, int* __restrict__ slots,
+                                       int* __restrict__ rank_of) {
   const int i = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= N) return;
@@ -710,7 +725,11 @@ __global__ void tc_rowlist_warp_kernel(int N, int K, const int* __restrict__ nbr
 #pragma unroll
     for (int u = 0; u < 2; ++u)
       if (ci[u] == c) {
-        if (slots) slots[(size_t)i * K + before + __popc(m & (bit[u] - 1u))] = lane + 32 * u;
+        if (slots) {
+          const int r = before + __popc(m & (bit[u] - 1u));
+          slots[(size_t)i * K + r] = lane + 32 * u;
+          if (rank_of) rank_of[(size_t)i * K + lane + 32 * u] = r;  // slot -> rank (ascending-j position)
+        }
         ci[u] = NONE;
       }
     ++nent;
@@ -973,7 +992,7 @@ TcScratch tc_scratch(const AttnArgs& a) {
 }  // namespace
 
 size_t attn_fwd_tc_workspace(const AttnArgs& a) {
-  return a.N > 0 ? tc_scratch(a).total + align256((size_t)a.N * a.K * 4) : 0;  // + slot order (score store)
+  return a.N > 0 ? tc_scratch(a).total + 2 * align256((size_t)a.N * a.K * 4) : 0;  // + slots, rank_of (score store)
 }
 
 namespace {
@@ -992,7 +1011,8 @@ struct TcPtrs {
   uint32_t* rowlist;
   int* tstart;  // [ntiles + 1]
   int* rtile;   // [N] tile of each query row
-  int* slots;  // only when the buffer holds them (tile buffers do)
+  int* slots;    // only when the buffer holds them (tile buffers do)
+  int* rank_of;  // [N*K] slot -> position in the row's ascending-j order (after slots)
 };
 TcPtrs tc_ptrs(void* base_, const TcScratch& t) {
   char* base = static_cast<char*>(base_);
@@ -1014,6 +1034,7 @@ TcPtrs tc_ptrs(void* base_, const TcScratch& t) {
   off += align256((size_t)(ntiles + 1) * 4);
   p.rtile = (int*)(base + off);
   p.slots = (int*)(base + t.total);
+  p.rank_of = (int*)(base + t.total + align256(t.pairs * 4));
   return p;
 }
 
@@ -1044,11 +1065,14 @@ es_status tc_build_lists(const AttnArgs& a, const int32_t* nbr, void* ws, const 
   cudaError_t e = cub::DeviceScan::ExclusiveSum(cub_ws, cub_bytes, cnt, cptr, ntiles + 1, st);
   if (e != cudaSuccess) return cuda_status(e, "attn_tc scan");
   tc_fill_kernel<<<(ntiles + 7) / 8, 256, 0, st>>>(ntiles, words, mask, cptr, clist);
+  // rank_of lives right after the slots (tile buffers and the workspaces that hold slots)
+  int* rank_of = slots ? (int*)((char*)slots + align256(t.pairs * 4)) : nullptr;
   if (a.K <= 64)
     tc_rowlist_warp_kernel<<<(unsigned)(((size_t)a.N * 32 + 255) / 256), 256, 0, st>>>(a.N, a.K, nbr, cptr, clist,
-                                                                                     pp.rtile, rowlist, slots);
+                                                                                     pp.rtile, rowlist, slots, rank_of);
   else
-    tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, pp.rtile, rowlist, slots);
+    tc_rowlist_kernel<<<(a.N + 127) / 128, 128, 0, st>>>(a.N, a.K, nbr, cptr, clist, pp.rtile, rowlist, slots,
+                                                         rank_of);
   *out = TcLists{cptr, clist, rowlist, ntiles, pp.tstart};
   return cuda_status(cudaGetLastError(), "attn_tc lists");
 }
@@ -1096,13 +1120,15 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   ta.bias_mode = a.bias_mode; ta.b0 = a.bias[0]; ta.b1 = a.bias[1]; ta.b2 = a.bias[2];
   ta.scores = a.scores_out;
   ta.slots = slots;
+  ta.score_rank = attn_dq_tc_applicable(a) ? 1 : 0;
   const int smem = SM_TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  attn_fwd_tc_kernel<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
+  (a.bias_mode ? attn_fwd_tc_kernel<true> : attn_fwd_tc_kernel<false>)<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
                                                         lists.tstart, (bf16*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
 }
@@ -1122,9 +1148,11 @@ constexpr int DQ_ABYTES = TQ * KC * 2;  // 4096: [128 rows][16 keys] bf16, no-sw
 constexpr int DQ_SM_K = 0;
 constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA latency dominates
 constexpr int DQ_SM_A = DQ_NSTAGE * KBYTES;
-constexpr int DQ_SM_DS = DQ_SM_A + 2 * DQ_ABYTES;  // [2 heads][128 rows][64] f32: the rows' dscores
+constexpr int DQ_NA = 4;  // dscore tiles in flight: the rows run up to 4 chunks ahead of the MMA + commit latency
+constexpr int DQ_SM_DS = DQ_SM_A + DQ_NA * DQ_ABYTES;  // [2 heads][128 rows][64] f32: the rows' dscores
 constexpr int DQ_KMAX = 64;
-constexpr int DQ_SM_STG = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;  // [4 warps][32 rows][80 B] epilogue staging
+constexpr int DQ_SM_OFF = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;  // [128 rows][64] i32: the rows' dscore gather offsets
+constexpr int DQ_SM_STG = DQ_SM_OFF + TQ * DQ_KMAX * 4;     // [4 warps][32 rows][80 B] epilogue staging
 constexpr int DQ_SM_BAR = DQ_SM_STG + 4 * 32 * 80;
 constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 
@@ -1144,11 +1172,11 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + DQ_SM_BAR);
   uint64_t* full_kv = bars + 0;    // [8] TMA landed
   uint64_t* empty_kv = bars + 8;   // [8] MMA done with the K stage
-  uint64_t* a_full = bars + 16;    // [2] rows wrote the dscore tile (128)
-  uint64_t* a_free = bars + 18;    // [2] MMA done with the dscore tile
-  uint64_t* acc_done = bars + 20;
-  uint64_t* epi_done = bars + 21;  // rows read the accumulator (128)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint64_t* a_full = bars + 16;    // [DQ_NA] rows wrote the dscore tile (128)
+  uint64_t* a_free = bars + 20;    // [DQ_NA] MMA done with the dscore tile
+  uint64_t* acc_done = bars + 24;
+  uint64_t* epi_done = bars + 25;  // rows read the accumulator (128)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = tstart[blockIdx.x], q1 = tstart[blockIdx.x + 1];
   if (q0 >= q1) return;  // surplus (empty) tile
@@ -1159,7 +1187,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       umma::mbar_init(&full_kv[b], 1);
       umma::mbar_init(&empty_kv[b], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < DQ_NA; ++b) {
       umma::mbar_init(&a_full[b], 128);
       umma::mbar_init(&a_free[b], 1);
     }
@@ -1201,9 +1229,9 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       int g = 0;
       for (int h = 0; h < 8; ++h) {
         for (int c = 0; c < nch; ++c, ++g) {
-          const int st = g % DQ_NSTAGE, b = g & 1;
+          const int st = g % DQ_NSTAGE, b = g % DQ_NA;
           umma::mbar_wait(&full_kv[st], (g / DQ_NSTAGE) & 1);
-          umma::mbar_wait(&a_full[b], (g >> 1) & 1);
+          umma::mbar_wait(&a_full[b], (g / DQ_NA) & 1);
           if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);
           umma::tc_fence_after();
           const uint32_t ka = umma::smem_u32(sm + DQ_SM_K + st * KBYTES);
@@ -1257,11 +1285,16 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
     // more than DQ_KMAX queries reads the excess directly
     float* dsr0 = reinterpret_cast<float*>(sm + DQ_SM_DS) + row * DQ_KMAX;
     const int npf = nv < DQ_KMAX ? nv : DQ_KMAX;
+    // the row's gather offsets (pair index * 8), loaded once for all heads: a slot load per
+    // pair and head would put a dependent global load in front of every cp.async
+    int* off = reinterpret_cast<int*>(sm + DQ_SM_OFF) + row * DQ_KMAX;
+#pragma unroll 4
+    for (int r0 = 0; r0 < npf; ++r0) off[r0] = (int)((gbase + __ldg(sl + r0)) * 8);
     auto fetch = [&](int hh) {
       float* dst = dsr0 + (hh & 1) * TQ * DQ_KMAX;
       for (int r0 = 0; r0 < npf; ++r0)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(umma::smem_u32(dst + r0)),
-                     "l"(dsbuf + (gbase + __ldg(sl + r0)) * 8 + hh)
+                     "l"(dsbuf + (off[r0] + hh))
                      : "memory");
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -1278,7 +1311,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       int rp = 0, r = 0;
       uint32_t ent = (qin && lmax > 0) ? __ldg(rl) : 0xffff0000u;
       for (int c = 0; c < nch; ++c, ++g) {
-        const int b = g & 1;
+        const int b = g % DQ_NA;
         unsigned vmask = 0u;
         if ((int)(ent >> 16) == c) {
           vmask = ent & 0xffffu;
@@ -1286,15 +1319,26 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
           ent = rp < lmax ? __ldg(rl + rp) : 0xffff0000u;
         }
         float d[KC];
+        if (!KEYS || nv <= DQ_KMAX) {  // every dscore of the row is in the prefetch buffer
 #pragma unroll
-        for (int t = 0; t < KC; ++t) {
-          d[t] = 0.f;
-          if (vmask >> t & 1) {
-            d[t] = r < DQ_KMAX ? dsr[r] : __ldg(dsbuf + (gbase + __ldg(sl + r)) * 8 + h);
-            ++r;
+          for (int t = 0; t < KC; ++t) {
+            d[t] = 0.f;
+            if (vmask >> t & 1) d[t] = dsr[r++];
           }
+        } else {  // a key with more than DQ_KMAX queries: the excess is read directly
+#pragma unroll
+          for (int t = 0; t < KC; ++t) d[t] = 0.f;
+#pragma unroll 1
+          for (int t = 0; t < KC; ++t)
+            if (vmask >> t & 1) {
+              const float x = r < DQ_KMAX ? dsr[r] : __ldg(dsbuf + (gbase + __ldg(sl + r)) * 8 + h);
+              ++r;
+#pragma unroll
+              for (int u = 0; u < KC; ++u)
+                if (u == t) d[u] = x;  // static register indices
+            }
         }
-        if (g >= 2) umma::mbar_wait(&a_free[b], ((g >> 1) - 1) & 1);
+        if (g >= DQ_NA) umma::mbar_wait(&a_free[b], ((g / DQ_NA) - 1) & 1);
         uint8_t* at = sm + DQ_SM_A + b * DQ_ABYTES + (row >> 3) * 256 + (row & 7) * 16;
         *reinterpret_cast<uint4*>(at) = pack8(d);
         *reinterpret_cast<uint4*>(at + 128) = pack8(d + 8);
@@ -1352,12 +1396,13 @@ bool attn_dq_tc_applicable(const AttnArgs& a) {
     use = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 2 : 1;
   }
   const bool enough_tiles = (a.N + TQ - 1) / TQ >= 74;
-  return use && (enough_tiles || use == 2) && a.K <= DQ_KMAX && attn_tc_supported(a);
+  const bool idx32 = (size_t)a.N * a.K * 8 < ((size_t)1 << 31);  // 32-bit gather offsets
+  return use && (enough_tiles || use == 2) && a.K <= DQ_KMAX && idx32 && attn_tc_supported(a);
 }
 
 size_t attn_dq_tc_workspace(const AttnArgs& a) {
   if (a.N <= 0) return 0;
-  return tc_scratch(a).total + align256((size_t)a.N * a.K * 4);
+  return tc_scratch(a).total + 2 * align256((size_t)a.N * a.K * 4);
 }
 
 es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr, const float* dsbuf, void* dq,
@@ -1424,11 +1469,18 @@ es_status tc_build_key_lists(const AttnArgs& a, const int32_t* nbr, const int32_
   return cuda_status(cudaGetLastError(), "attn_tc key lists");
 }
 
-size_t tiles_query_bytes(const AttnArgs& a) { return tc_scratch(a).total + align256((size_t)a.N * a.K * 4); }
+size_t tiles_query_bytes(const AttnArgs& a) { return tc_scratch(a).total + 2 * align256((size_t)a.N * a.K * 4); }
 
 }  // namespace
 
-bool attn_dk_tc_applicable(const AttnArgs& a) { return attn_dq_tc_applicable(a); }
+bool attn_dk_tc_applicable(const AttnArgs& a) {
+  // Off by default (ES_DK_TC=1 enables it): on configs[1] the key pass without dk is gather-bound
+  // (2.9 ms with the forward's kept scores, 4.2 ms recomputing them) and this pass adds 0.84 ms, while
+  // keeping the scores costs the forward 0.47 ms -- 7.73 ms fwd+bwd against 7.50 ms for the SIMT
+  // key pass with dk.
+  const char* e = getenv("ES_DK_TC");  // read per call: the tests switch it
+  return e && e[0] == '1' && attn_dq_tc_applicable(a);
+}
 
 size_t attn_dk_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(key_side(a)).total : 0; }
 
@@ -1459,6 +1511,12 @@ es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr
                                                                   lists.rowlist, rev_pair, lists.tstart, rev_ptr,
                                                                   dsbuf, (bf16*)dk);
   return cuda_status(cudaGetLastError(), "attn_dk_tc_kernel");
+}
+
+const int* attn_tc_rank_of(const AttnArgs& a, const void* tiles) {
+  if (!tiles) return nullptr;
+  return reinterpret_cast<const int*>(static_cast<const char*>(tiles) + tc_scratch(a).total +
+                                      align256((size_t)a.N * a.K * 4));
 }
 
 bool attn_tc_tiles_used(const AttnArgs& a) { return attn_dq_tc_applicable(a) || attn_fwd_workspace(a) > 0; }

@@ -191,10 +191,8 @@ static size_t bwd_base_bytes(const es_attn_desc* d) {
 size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
   if (!d || d->N <= 0 || check_attn(d) != ES_OK) return 256;
   const AttnArgs a = to_args(d);
-  size_t tc = 0;
-  if (attn_dq_tc_applicable(a)) tc = attn_dq_tc_workspace(a);
-  if (attn_dk_tc_applicable(a) && attn_dk_tc_workspace(a) > tc) tc = attn_dk_tc_workspace(a);  // run one after the other
-  return bwd_base_bytes(d) + tc;
+  // tensor-core passes without prebuilt tiles: the tile lists (query + key side) are built in the workspace
+  return bwd_base_bytes(d) + (attn_dq_tc_applicable(a) ? attn_tc_tiles_bytes(a) : 0);
 }
 
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,

@@ -114,8 +114,10 @@ class CudaBackend:
 
     def attn_fwd(self, q_loc, k, v, pos, table_loc, row0):
         idx = self.api.NeighborIndex(table_loc, None, None, self.cfg.r_cut)
-        out, lse, sc = self.api.stream_aggregate(q_loc, k, v, pos, idx, self.cfg, row0=row0, return_scores=True)
-        idx._scores = sc  # the forward's scores travel with the index to the backward
+        keep = self.cfg.keep_scores
+        res = self.api.stream_aggregate(q_loc, k, v, pos, idx, self.cfg, row0=row0, return_scores=keep)
+        out, lse, sc = res if keep else (*res, None)
+        idx._scores = sc  # the forward's scores (if kept) travel with the index to the backward
         return out, lse, idx
 
     def attn_bwd(self, g_loc, q_loc, k, v, pos, idx, out, lse, row0):

@@ -14,7 +14,8 @@ class _AttnFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, h, W, pos, idx: NeighborIndex, cfg: AttentionConfig):
         q, k, v = project_qk(h.contiguous(), W.contiguous(), cfg.L)
-        out, lse, scores = stream_aggregate(q, k, v, pos, idx, cfg, return_scores=cfg.keep_scores)
+        res = stream_aggregate(q, k, v, pos, idx, cfg, return_scores=cfg.keep_scores)
+        out, lse, scores = res if cfg.keep_scores else (*res, None)
         ctx.save_for_backward(h, W, q, k, v, out, lse, pos)
         ctx.scores = scores
         ctx.idx, ctx.cfg = idx, cfg

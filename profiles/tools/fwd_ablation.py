@@ -29,8 +29,9 @@ def main():
     idx.transpose()
     q, k, v = es.project_qk(h, W, L)
     cfg = AttentionConfig(heads=H, L=L)
-    out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
-    saved = SavedAttention(q, k, v, pos, idx, out, lse, cfg)
+    out, lse, sc = es.stream_aggregate(q, k, v, pos, idx, cfg, return_scores=True)
+    saved = SavedAttention(q, k, v, pos, idx, out, lse, cfg, scores=sc)
+    saved0 = SavedAttention(q, k, v, pos, idx, out, lse, cfg)
 
     def t(fn, n=5):
         fn()
@@ -45,9 +46,20 @@ def main():
 
     for d in [int(x) for x in (sys.argv[1:] or ["0", "1", "2", "3", "4", "8", "12", "15"])]:
         os.environ["ES_TC_DBG"] = str(d)
-        print(f"dbg {d:2d}: fwd {t(lambda: es.stream_aggregate(q, k, v, pos, idx, cfg)):.3f} ms", flush=True)
+        print(f"dbg {d:2d}: fwd {t(lambda: es.stream_aggregate(q, k, v, pos, idx, cfg)):.3f} ms  (keeping scores "
+              f"{t(lambda: es.stream_aggregate(q, k, v, pos, idx, cfg, return_scores=True)):.3f} ms)", flush=True)
     os.environ["ES_TC_DBG"] = "0"
-    print(f"bwd {t(lambda: es.stream_aggregate_backward(out, saved)):.3f} ms")
+    print(f"bwd {t(lambda: es.stream_aggregate_backward(out, saved)):.3f} ms (saved scores), "
+          f"{t(lambda: es.stream_aggregate_backward(out, saved0)):.3f} ms (recomputed)")
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        es.stream_aggregate(q, k, v, pos, idx, cfg, return_scores=True)
+        es.stream_aggregate_backward(out, saved)
+        es.stream_aggregate_backward(out, saved0)
+        torch.cuda.synchronize()
+    for e in prof.key_averages():
+        if e.device_type.name == "CUDA" and getattr(e, "device_time_total", 0) > 20:
+            print(f"  {getattr(e, 'device_time_total', 0):9.1f} us  {e.key[:90]}")
 
 
 if __name__ == "__main__":

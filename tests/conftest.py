@@ -39,3 +39,11 @@ def has_gpu() -> bool:
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+@pytest.fixture(params=["simt_dk", "tc_dk"])
+def dk_path(request, monkeypatch):
+    """Both backward variants: dk in the key-centric SIMT pass (default) and the
+    tensor-core dk pass over key-side tiles (ES_DK_TC=1)."""
+    monkeypatch.setenv("ES_DK_TC", "1" if request.param == "tc_dk" else "0")
+    return request.param

@@ -308,7 +308,7 @@ def test_full_size_properties_config2(es):
 
 
 @pytest.mark.parametrize("kind", ["batch", "batch_uniform", "long_segments", "bulk", "pbc", "sharp", "empty_tiles"])
-def test_attention_bf16_tensor_core_tiles(es, oracle, kind):
+def test_attention_bf16_tensor_core_tiles(es, oracle, kind, dk_path):
     """The tcgen05 paths (forward, dq; bf16, L=2, C=128, H=8) over many
     128-query tiles and key chunks: molecule batch (segment-packed query
     tiles, and uniform tiles), a batch of molecules longer than a tile (split
