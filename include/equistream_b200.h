@@ -115,6 +115,18 @@ typedef struct {
  * es_neighbors_build; NULL / 0 for one system): query tiles pack whole
  * segments, so a tile's key chunks cover only its own molecules. */
 size_t es_attn_tiles_workspace_size(const es_attn_desc* d);
+/* Byte offsets of the arrays inside a tile buffer (introspection and the
+ * bit-exact tests; the kernels need nothing but the buffer).  ntiles is the
+ * tile-count bound of the layout; a side that is absent has ntiles = 0. */
+typedef struct {
+  int64_t ntiles, words, nchunk_max;      /* tiles, mask words per tile, clist capacity */
+  int64_t mask, cptr, clist, rowlist, tstart, rtile;
+  int64_t slots, rank_of;                  /* query side only (-1 on the key side) */
+} es_attn_tiles_side;
+typedef struct {
+  es_attn_tiles_side query, key;           /* key side: rows = key atoms, chunks of 16 queries */
+} es_attn_tiles_layout;
+es_status es_attn_tiles_layout_query(const es_attn_desc* d, es_attn_tiles_layout* out);
 /* rev_ptr / rev_pair (optional, from es_neighbors_transpose on the same nbr):
  * also build the key-side lists (key tiles, their query-chunk lists and
  * per-key (chunk, query mask) entries) the tensor-core dk pass of the

@@ -39,6 +39,15 @@ class AttnStats(ct.Structure):
                                            "workspace_fwd_bytes", "workspace_bwd_bytes")]
 
 
+class TilesSide(ct.Structure):
+    _fields_ = [(n, ct.c_int64) for n in ("ntiles", "words", "nchunk_max", "mask", "cptr", "clist", "rowlist",
+                                          "tstart", "rtile", "slots", "rank_of")]
+
+
+class TilesLayout(ct.Structure):
+    _fields_ = [("query", TilesSide), ("key", TilesSide)]
+
+
 class ProjDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32), ("dtype", ct.c_int32)]
 
@@ -62,7 +71,7 @@ EXPORTS = [
     "es_neighbors_workspace_size", "es_neighbors_transpose", "es_neighbors_transpose_workspace_size",
     "es_tile_mask", "es_project_fwd", "es_project_bwd", "es_conventions_manifest", "es_cg_real",
     "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
-    "es_attn_stats_query",
+    "es_attn_stats_query", "es_attn_tiles_layout_query",
 ]
 
 
@@ -82,6 +91,7 @@ def lib() -> ct.CDLL:
         L.es_attn_fwd_workspace_size.restype = sz
         L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 17 + [sz, vp]
         L.es_attn_stats_query.argtypes = [ct.POINTER(AttnDesc), ct.c_int64, ct.POINTER(AttnStats)]
+        L.es_attn_tiles_layout_query.argtypes = [ct.POINTER(AttnDesc), ct.POINTER(TilesLayout)]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]

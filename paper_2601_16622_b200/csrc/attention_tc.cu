@@ -22,6 +22,7 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include <cub/cub.cuh>
 
@@ -156,7 +157,7 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 // while the current head runs), O [288,432), S[2] [448,464) / [480,496).
 constexpr int TC_THREADS = 448;
 
-template <bool BIAS>
+template <bool BIAS, bool SCORES>
 __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
     const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, TcArgs a,
     const bf16* __restrict__ q, const double* __restrict__ pos, const int* __restrict__ nbr,
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
               if (vmask >> t & 1) sr[t] = __float_as_uint(svv(t) + tc_pair_bias(a, kpos + 3 * t, qpos + 3 * row));
           }
         }
-        if (a.scores && qvalid) {  // keep the scores of my half's valid keys
+        if (SCORES && qvalid) {  // keep the scores of my half's valid keys
           const unsigned hmask = (vmask >> (8 * half)) & 0xffu;
           if (hmask) {
             const int* srow = a.slots + (size_t)qi * a.K;
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
               }
           }
         }
-        rbase += __popc(vmask);
+        if constexpr (SCORES) rbase += __popc(vmask);
         float mc = -INFINITY;
 #pragma unroll
         for (int t = 0; t < KC; ++t)
@@ -1124,11 +1125,16 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   const int smem = SM_TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_fwd_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_tc_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  (a.bias_mode ? attn_fwd_tc_kernel<true> : attn_fwd_tc_kernel<false>)<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
+  // bias and score store are separate instantiations: the default kernel carries neither
+  auto kfn = a.bias_mode ? (ta.scores ? attn_fwd_tc_kernel<true, true> : attn_fwd_tc_kernel<true, false>)
+                         : (ta.scores ? attn_fwd_tc_kernel<false, true> : attn_fwd_tc_kernel<false, false>);
+  kfn<<<ntiles, TC_THREADS, smem, st>>>(mk, mv, ta, (const bf16*)q, pos, nbr, cptr, clist, rowlist,
                                                         lists.tstart, (bf16*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_tc_kernel");
 }
@@ -1511,6 +1517,29 @@ es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr
                                                                   lists.rowlist, rev_pair, lists.tstart, rev_ptr,
                                                                   dsbuf, (bf16*)dk);
   return cuda_status(cudaGetLastError(), "attn_dk_tc_kernel");
+}
+
+void attn_tc_tiles_layout(const AttnArgs& a, es_attn_tiles_layout* out) {
+  std::memset(out, 0, sizeof(*out));
+  if (a.N <= 0 || !attn_tc_tiles_used(a)) return;
+  auto side = [](const AttnArgs& b, int64_t base, es_attn_tiles_side* o, bool query) {
+    const TcScratch t = tc_scratch(b);
+    const TcPtrs p = tc_ptrs(nullptr, t);
+    const char* z = nullptr;
+    o->ntiles = t.ntiles;
+    o->words = t.words;
+    o->nchunk_max = (int64_t)t.chunks;
+    o->mask = base + ((const char*)p.mask - z);
+    o->cptr = base + ((const char*)p.cptr - z);
+    o->clist = base + ((const char*)p.clist - z);
+    o->rowlist = base + ((const char*)p.rowlist - z);
+    o->tstart = base + ((const char*)p.tstart - z);
+    o->rtile = base + ((const char*)p.rtile - z);
+    o->slots = query ? base + ((const char*)p.slots - z) : -1;
+    o->rank_of = query ? base + ((const char*)p.rank_of - z) : -1;
+  };
+  side(a, 0, &out->query, true);
+  if (attn_dk_tc_applicable(a)) side(key_side(a), (int64_t)tiles_query_bytes(a), &out->key, false);
 }
 
 const int* attn_tc_rank_of(const AttnArgs& a, const void* tiles) {

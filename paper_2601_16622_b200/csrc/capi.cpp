@@ -150,6 +150,16 @@ size_t es_attn_tiles_workspace_size(const es_attn_desc* d) {
   return attn_tc_tiles_used(a) ? attn_tc_tiles_bytes(a) : 0;
 }
 
+es_status es_attn_tiles_layout_query(const es_attn_desc* d, es_attn_tiles_layout* out) {
+  return guarded([&] {
+    es_status s = check_attn(d);
+    if (s != ES_OK) return s;
+    if (!out) return fail(ES_INVALID_ARGUMENT, "attn_tiles_layout: null output");
+    attn_tc_tiles_layout(to_args(d), out);
+    return ES_OK;
+  });
+}
+
 es_status es_attn_tiles_build(const es_attn_desc* d, const int32_t* nbr, const int32_t* seg_ptr, int32_t nseg,
                               const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
                               void* stream) {

@@ -69,6 +69,7 @@ size_t attn_tc_tiles_bytes(const AttnArgs& a);
 es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32_t* seg, int nseg,
                               const int32_t* rev_ptr, const int32_t* rev_pair, void* tiles, size_t bytes,
                               cudaStream_t st);
+void attn_tc_tiles_layout(const AttnArgs& a, es_attn_tiles_layout* out);
 // slot -> rank map inside a tile buffer (the tensor-core forward keeps scores in rank space)
 const int* attn_tc_rank_of(const AttnArgs& a, const void* tiles);
 // tensor-core dk = tau dS^T Q over key tiles (key-side lists in the tiles buffer or the workspace)

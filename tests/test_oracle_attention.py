@@ -191,3 +191,25 @@ def test_fcc_geometry(oracle):
     cell = S.gen_fcc_system(4, 3.8, 0, n_cells=1)
     d = np.linalg.norm(cell[:, None] - cell[None], axis=-1)[np.triu_indices(4, 1)]
     np.testing.assert_allclose(d, 3.8 / np.sqrt(2))
+
+
+def test_tiles_ref_packing_properties():
+    """oracle/tiles_ref.py: packed query tiles hold whole segments (a segment
+    longer than a tile is split at 128-row boundaries), never exceed 128 rows,
+    and cover every row once; uniform tiles are 128-row blocks."""
+    from oracle import tiles_ref as TR
+    rng = np.random.default_rng(0)
+    sizes = rng.integers(20, 300, size=200)
+    seg = np.concatenate([[0], np.cumsum(sizes)])
+    N = int(seg[-1])
+    ts = TR.tile_starts(N, seg)
+    assert ts[0] == 0 and ts[-1] == N and all(b > a for a, b in zip(ts, ts[1:]))
+    assert all(b - a <= TR.TQ for a, b in zip(ts, ts[1:]))
+    cuts = set(ts)
+    for a, b in zip(seg[:-1], seg[1:]):
+        inner = [c for c in cuts if a < c < b]
+        if b - a <= TR.TQ:
+            assert not inner or TR.pack_parts(N) > 1  # only a part boundary may cut a short segment
+        else:
+            assert all((c - a) % TR.TQ == 0 or c - a < TR.TQ for c in inner) or TR.pack_parts(N) > 1
+    assert TR.tile_starts(300) == [0, 128, 256, 300]
