@@ -230,6 +230,33 @@ es_status es_project_fwd(const es_proj_desc* d, const void* h, const void* W, vo
 es_status es_project_bwd(const es_proj_desc* d, const void* h, const void* W, const void* dq, const void* dk,
                          const void* dv, void* dh, float* dW, void* stream);
 
+/* Node-centric factorized message (Eq. 5
+ * PAPER.md:228-235; three-stage flow PAPER.md:299-322), fp64:
+ *   m_i = sum_j alpha_ij sum_paths (h_j^li (x) R^lf(r_j - r_i))^lo
+ * (== edge_centric_message SPEC.md:342-350 with the attention's path set)
+ * evaluated as source term -> alpha aggregation -> target coupling through
+ * the binomial translation identity R^lf(a+b) = sum_u w(lf,u)
+ * (R^u(a) (x) R^{lf-u}(b))^lf (conventions.hpp:32-34) and the 6j recoupling,
+ * so per edge only the scalar alpha_ij multiplies.  h, out: [N][M][C] f64;
+ * alpha: [N][K][H] f64 (head h weights channels [h C/H, (h+1) C/H));
+ * S, A (source terms, aggregates): [N][(L+1)^4][C] f64; origin: the
+ * recentring point (SPEC ledger: the centroid), positions are absolute.
+ * L <= 2 (SPEC ledger "degree budget"). */
+typedef struct {
+  int32_t N, K, H, L, C;
+  double origin[3];
+} es_msg_desc;
+/* translation_coefficients: w[u], u = 0..l, solved from the identity (host) */
+es_status es_translation_coefficients(int32_t l, double* w);
+es_status es_source_term(const es_msg_desc* d, const double* pos, const double* h, double* S, void* stream);
+es_status es_message_aggregate(const es_msg_desc* d, const int32_t* nbr, const double* alpha, const double* S,
+                               double* A, void* stream);
+es_status es_target_couple(const es_msg_desc* d, const double* pos, const double* A, double* out, void* stream);
+size_t es_factorized_workspace_size(const es_msg_desc* d);
+es_status es_factorized_message(const es_msg_desc* d, const double* pos, const double* h, const int32_t* nbr,
+                                const double* alpha, double* out, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* Host-side introspection of the tables the kernels use. */
 const char* es_conventions_manifest(void);
 double es_cg_real(int32_t l1, int32_t m1, int32_t l2, int32_t m2, int32_t lo, int32_t mo);

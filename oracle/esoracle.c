@@ -1009,3 +1009,230 @@ void eso_set_threads(int n) {
   (void)n;
 #endif
 }
+
+/* ------------------------------------------------------------------ */
+/* Node-centric factorized message (Eq. 5 PAPER.md:   */
+/* 228-235; three-stage flow PAPER.md:299-322).                         */
+/*   m_i = sum_j alpha_ij sum_paths (h_j^li (x) R^lf(r_j - r_i))^lo     */
+/* with R^lf(a + b) = sum_u w(lf,u) (R^u(a) (x) R^{lf-u}(b))^lf         */
+/* (translation weights, conventions.hpp:32-34), a = -(r_i - o),        */
+/* b = r_j - o, and (h (x) (A (x) B)^lf)^lo recoupled to                */
+/* sum_l' c_l' ((h (x) B)^l' (x) A)^lo (Wigner-6j recoupling; the       */
+/* coefficients solved by least squares, SPEC ledger "6j-vs-solve").    */
+/* Source terms depend on j only, targets on i only: per edge only the  */
+/* scalar alpha_ij multiplies.                            */
+/* ------------------------------------------------------------------ */
+static double binom_d(int n, int k) {
+  double r = 1.0;
+  for (int a = 1; a <= k; ++a) r = r * (n - k + a) / a;
+  return r;
+}
+/* closed form printed by the reference manifest (conventions.hpp:32-34) */
+double eso_translation_weight(int l, int u) {
+  return sqrt(binom_d(2 * l, 2 * u) * 4.0 * ESO_PI * (2 * l + 1) / ((2.0 * u + 1.0) * (2.0 * (l - u) + 1.0)));
+}
+
+static unsigned long long g_lcg = 88172645463325252ull;
+static double lcg_unit(void) { /* deterministic sample points for the least-squares solves */
+  g_lcg = g_lcg * 6364136223846793005ull + 1442695040888963407ull;
+  return ((g_lcg >> 11) * (1.0 / 9007199254740992.0)) * 2.0 - 1.0;
+}
+
+/* translation_coefficients: least-squares w[u], u = 0..l, of
+ * R^l(a+b) = sum_u w[u] (R^u(a) (x) R^{l-u}(b))^l over 8(l+1)(2l+1) samples. */
+int eso_translation_coefficients(int l, double* w) {
+  cg_cache_init();
+  const int d = 2 * l + 1, nu = l + 1, ns = 8 * nu * d;
+  double* A = (double*)calloc((size_t)nu * nu, sizeof(double));
+  double* B = (double*)calloc((size_t)nu, sizeof(double));
+  double ya[2 * ESO_LT + 1], yb[2 * ESO_LT + 1], yab[2 * ESO_LT + 1], cp[ESO_LT + 1][2 * ESO_LT + 1];
+  for (int s = 0; s < ns / d; ++s) {
+    const double a[3] = {lcg_unit(), lcg_unit(), lcg_unit()}, b[3] = {lcg_unit(), lcg_unit(), lcg_unit()};
+    const double ab[3] = {a[0] + b[0], a[1] + b[1], a[2] + b[2]};
+    eso_solid_harmonics(l, ab, yab);
+    for (int u = 0; u <= l; ++u) {
+      eso_solid_harmonics(u, a, ya);
+      eso_solid_harmonics(l - u, b, yb);
+      tp_dense_tab(cgt(u, l - u, l), ya, u, 1, yb, l - u, 1, l, cp[u]);
+    }
+    for (int m = 0; m < d; ++m)
+      for (int p = 0; p < nu; ++p) {
+        B[p] += cp[p][m] * yab[m];
+        for (int q = 0; q < nu; ++q) A[p * nu + q] += cp[p][m] * cp[q][m];
+      }
+  }
+  const int st = solve_inplace(A, B, nu, 1);
+  for (int u = 0; u <= l; ++u) w[u] = B[u];
+  free(A); free(B);
+  return st;
+}
+
+/* recoupling (h^li (x) (A^u (x) B^lb)^lf)^lo = sum_l' c[l'] ((h (x) B)^l' (x) A)^lo;
+ * c indexed by l' (entries outside |li-lb|..li+lb or not triangle with (l', u, lo) are 0). */
+int eso_recouple(int li, int u, int lb, int lf, int lo, double* c) {
+  cg_cache_init();
+  const int lmin = abs(li - lb), lmax = li + lb;
+  int nl = 0, ls[2 * ESO_LT + 1];
+  for (int l2 = lmin; l2 <= lmax; ++l2)
+    if (l2 < ESO_LT && tri_ok(l2, u, lo)) ls[nl++] = l2;
+  for (int l2 = 0; l2 <= 2 * (ESO_LT - 1); ++l2) c[l2] = 0.0;
+  if (!tri_ok(u, lb, lf) || !tri_ok(li, lf, lo) || nl == 0) return -1;
+  const int dl = 2 * lo + 1;
+  double* A = (double*)calloc((size_t)nl * nl, sizeof(double));
+  double* B = (double*)calloc((size_t)nl, sizeof(double));
+  double h[2 * ESO_LT + 1], av[2 * ESO_LT + 1], bv[2 * ESO_LT + 1], ab[2 * ESO_LT + 1], lhs[2 * ESO_LT + 1];
+  double hb[4 * ESO_LT + 1], rhs[2 * ESO_LT + 1][2 * ESO_LT + 1];
+  for (int s = 0; s < 12 * nl + 4; ++s) {
+    for (int m = 0; m < 2 * li + 1; ++m) h[m] = lcg_unit();
+    for (int m = 0; m < 2 * u + 1; ++m) av[m] = lcg_unit();
+    for (int m = 0; m < 2 * lb + 1; ++m) bv[m] = lcg_unit();
+    tp_dense_tab(cgt(u, lb, lf), av, u, 1, bv, lb, 1, lf, ab);
+    tp_dense_tab(cgt(li, lf, lo), h, li, 1, ab, lf, 1, lo, lhs);
+    for (int p = 0; p < nl; ++p) {
+      tp_dense_tab(cgt(li, lb, ls[p]), h, li, 1, bv, lb, 1, ls[p], hb);
+      tp_dense_tab(cgt(ls[p], u, lo), hb, ls[p], 1, av, u, 1, lo, rhs[p]);
+    }
+    for (int m = 0; m < dl; ++m)
+      for (int p = 0; p < nl; ++p) {
+        B[p] += rhs[p][m] * lhs[m];
+        for (int q = 0; q < nl; ++q) A[p * nl + q] += rhs[p][m] * rhs[q][m];
+      }
+  }
+  const int st = solve_inplace(A, B, nl, 1);
+  for (int p = 0; p < nl; ++p) c[ls[p]] = B[p];
+  free(A); free(B);
+  return st;
+}
+
+/* source-term component layout: for li = 0..L, lb = 0..L, l' = |li-lb|..li+lb:
+ * (2l'+1) rows; M^2 rows in total. */
+static int src_ncomp(int L) { return (L + 1) * (L + 1) * (L + 1) * (L + 1); }
+static int src_offset(int L, int li, int lb, int l2) {
+  int o = 0;
+  for (int a = 0; a <= L; ++a)
+    for (int b = 0; b <= L; ++b)
+      for (int c = abs(a - b); c <= a + b; ++c) {
+        if (a == li && b == lb && c == l2) return o;
+        o += 2 * c + 1;
+      }
+  return -1;
+}
+
+/* source_term: S_j^(li,lb,l') = (h_j^li (x) R^lb(r_j - o))^l'  [N][M^2][C] */
+void eso_source_term(int N, int L, int C, const double* pos, const double* origin, const double* h, double* S) {
+  cg_cache_init();
+  const int M = (L + 1) * (L + 1), NS = src_ncomp(L);
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < N; ++j) {
+    const double r[3] = {pos[3 * j] - origin[0], pos[3 * j + 1] - origin[1], pos[3 * j + 2] - origin[2]};
+    double y[2 * ESO_LT + 1];
+    for (int li = 0; li <= L; ++li)
+      for (int lb = 0; lb <= L; ++lb) {
+        eso_solid_harmonics(lb, r, y);
+        for (int l2 = abs(li - lb); l2 <= li + lb; ++l2)
+          tp_dense_tab(cgt(li, lb, l2), h + ((size_t)j * M + li * li) * C, li, C, y, lb, 1, l2,
+                       S + ((size_t)j * NS + src_offset(L, li, lb, l2)) * C);
+      }
+  }
+}
+
+/* alpha-weighted aggregation: A_i = sum_j alpha_ij^{head(c)} S_j (only scalar work per edge) */
+void eso_aggregate(int N, int K, int H, int NS, int C, const int* nbr, const double* alpha, const double* S,
+                   double* A) {
+  const int ch = C / H;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < N; ++i) {
+    double* a = A + (size_t)i * NS * C;
+    memset(a, 0, sizeof(double) * NS * C);
+    for (int kk = 0; kk < K; ++kk) {
+      const int j = nbr[(size_t)i * K + kk];
+      if (j < 0) continue;
+      const double* s = S + (size_t)j * NS * C;
+      for (int t = 0; t < NS; ++t)
+        for (int c = 0; c < C; ++c) a[t * C + c] += alpha[((size_t)i * K + kk) * H + c / ch] * s[t * C + c];
+    }
+  }
+}
+
+/* target_couple + translation (Eq. 5):
+ * m_i^lo = sum_(li,lf) sum_u w(lf,u) sum_l' c (A_i^(li, lf-u, l') (x) R^u(o - r_i))^lo */
+void eso_target_couple(int N, int L, int C, const double* pos, const double* origin, const double* A, double* out) {
+  cg_cache_init();
+  const int M = (L + 1) * (L + 1), NS = src_ncomp(L);
+  double w[ESO_LT][ESO_LT];
+  for (int lf = 0; lf <= L; ++lf) eso_translation_coefficients(lf, w[lf]);
+  static double cc[ESO_LT][ESO_LT][ESO_LT][ESO_LT][2 * ESO_LT]; /* [li][u][lb][lo][l'] (lf = u + lb) */
+#pragma omp critical(eso_recouple_cache)
+  for (int li = 0; li <= L; ++li)
+    for (int u = 0; u <= L; ++u)
+      for (int lb = 0; lb + u <= L; ++lb)
+        for (int lo = 0; lo <= L; ++lo) eso_recouple(li, u, lb, u + lb, lo, cc[li][u][lb][lo]);
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < N; ++i) {
+    const double a[3] = {origin[0] - pos[3 * i], origin[1] - pos[3 * i + 1], origin[2] - pos[3 * i + 2]};
+    double ya[ESO_LT][2 * ESO_LT + 1];
+    for (int u = 0; u <= L; ++u) eso_solid_harmonics(u, a, ya[u]);
+    double* o = out + (size_t)i * M * C;
+    memset(o, 0, sizeof(double) * M * C);
+    double* tmp = (double*)malloc(sizeof(double) * (2 * L + 1) * C);
+    for (int li = 0; li <= L; ++li)
+      for (int lf = 0; lf <= L; ++lf)
+        for (int lo = 0; lo <= L; ++lo) {
+          if (!tri_ok(li, lf, lo)) continue;
+          for (int u = 0; u <= lf; ++u) {
+            const int lb = lf - u;
+            for (int l2 = abs(li - lb); l2 <= li + lb; ++l2) {
+              const double coef = w[lf][u] * cc[li][u][lb][lo][l2];
+              if (coef == 0.0 || !tri_ok(l2, u, lo)) continue;
+              tp_dense_tab(cgt(l2, u, lo), A + ((size_t)i * NS + src_offset(L, li, lb, l2)) * C, l2, C, ya[u], u, 1,
+                           lo, tmp);
+              for (int t = 0; t < (2 * lo + 1) * C; ++t) o[lo * lo * C + t] += coef * tmp[t];
+            }
+          }
+        }
+    free(tmp);
+  }
+}
+
+/* factorized_message: source -> aggregate -> target */
+void eso_factorized_message(int N, int K, int H, int L, int C, const double* pos, const double* origin, const double* h,
+                            const int* nbr, const double* alpha, double* out) {
+  const int NS = src_ncomp(L);
+  double* S = (double*)malloc(sizeof(double) * (size_t)N * NS * C);
+  double* A = (double*)malloc(sizeof(double) * (size_t)N * NS * C);
+  eso_source_term(N, L, C, pos, origin, h, S);
+  eso_aggregate(N, K, H, NS, C, nbr, alpha, S, A);
+  eso_target_couple(N, L, C, pos, origin, A, out);
+  free(S); free(A);
+}
+
+/* edge_centric_message: the oracle -- per edge the dense CG
+ * product h_j (x) R^lf(r_j - r_i) over all paths, weighted by alpha_ij. */
+void eso_edge_message(int N, int K, int H, int L, int C, const double* pos, const double* h, const int* nbr,
+                      const double* alpha, double* out) {
+  eso_attn_desc d;
+  memset(&d, 0, sizeof(d));
+  d.N = N; d.K = K; d.H = H; d.L = L; d.Cv = C; d.value_mode = 1; d.phi_mode = 1; d.r_cut = 1e300;
+  cg_cache_init();
+  const int M = (L + 1) * (L + 1), ch = C / H;
+#pragma omp parallel
+  {
+    double* x = (double*)malloc(sizeof(double) * M * C);
+    double* scr = (double*)malloc(sizeof(double) * 2 * M * C);
+#pragma omp for schedule(dynamic, 4)
+    for (int i = 0; i < N; ++i) {
+      double* o = out + (size_t)i * M * C;
+      memset(o, 0, sizeof(double) * M * C);
+      for (int kk = 0; kk < K; ++kk) {
+        const int j = nbr[(size_t)i * K + kk];
+        if (j < 0) continue;
+        double r[3];
+        pair_vec(pos, i, j, NULL, r);
+        pair_value(&d, h, j, r, 1.0, x, scr);
+        for (int t = 0; t < M; ++t)
+          for (int c = 0; c < C; ++c) o[t * C + c] += alpha[((size_t)i * K + kk) * H + c / ch] * x[t * C + c];
+      }
+    }
+    free(x); free(scr);
+  }
+}

@@ -291,3 +291,51 @@ def default_seed(fallback: int = 0) -> int:
         return int(os.environ.get("EQUISTREAM_SEED", fallback))
     except ValueError:
         return fallback
+
+
+# ------------------------------------------------------------------ factorized message
+def translation_weight(l: int, u: int) -> float:
+    """Closed form printed by the reference manifest (conventions.hpp:32-34)."""
+    f = lib().eso_translation_weight
+    f.restype = ct.c_double
+    f.argtypes = [ct.c_int, ct.c_int]
+    return float(f(l, u))
+
+
+def translation_coefficients(l: int) -> np.ndarray:
+    """Least-squares weights w[u] of R^l(a+b) = sum_u w[u] (R^u(a) x R^{l-u}(b))^l."""
+    w = np.zeros(l + 1)
+    assert lib().eso_translation_coefficients(int(l), _p(w)) == 0
+    return w
+
+
+def recouple(li, u, lb, lf, lo) -> np.ndarray:
+    c = np.zeros(9)
+    lib().eso_recouple(int(li), int(u), int(lb), int(lf), int(lo), _p(c))
+    return c
+
+
+def edge_message(pos, h, nbr, alpha, L):
+    """edge_centric_message: m_i = sum_j alpha_ij sum_paths (h_j (x) R^lf(r_j - r_i))^lo."""
+    pos, h, alpha = _c(pos), _c(h), _c(alpha)
+    nbr = _c(nbr, np.int32)
+    N, K = nbr.shape
+    H = alpha.shape[2]
+    C = h.shape[2]
+    out = np.zeros_like(h)
+    lib().eso_edge_message(N, K, H, int(L), C, _p(pos), _p(h), nbr.ctypes.data_as(_ip), _p(alpha), _p(out))
+    return out
+
+
+def factorized_message(pos, h, nbr, alpha, L, origin=None):
+    """factorized_message (Eq. 5); origin defaults to the centroid."""
+    pos, h, alpha = _c(pos), _c(h), _c(alpha)
+    nbr = _c(nbr, np.int32)
+    N, K = nbr.shape
+    H = alpha.shape[2]
+    C = h.shape[2]
+    o = _c(pos.mean(axis=0) if origin is None else np.asarray(origin, np.float64))
+    out = np.zeros_like(h)
+    lib().eso_factorized_message(N, K, H, int(L), C, _p(pos), _p(o), _p(h), nbr.ctypes.data_as(_ip), _p(alpha),
+                                 _p(out))
+    return out

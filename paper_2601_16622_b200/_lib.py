@@ -48,6 +48,11 @@ class TilesLayout(ct.Structure):
     _fields_ = [("query", TilesSide), ("key", TilesSide)]
 
 
+class MsgDesc(ct.Structure):
+    _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("H", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32),
+                ("origin", ct.c_double * 3)]
+
+
 class ProjDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32), ("dtype", ct.c_int32)]
 
@@ -71,7 +76,8 @@ EXPORTS = [
     "es_neighbors_workspace_size", "es_neighbors_transpose", "es_neighbors_transpose_workspace_size",
     "es_tile_mask", "es_project_fwd", "es_project_bwd", "es_conventions_manifest", "es_cg_real",
     "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
-    "es_attn_stats_query", "es_attn_tiles_layout_query",
+    "es_attn_stats_query", "es_attn_tiles_layout_query", "es_translation_coefficients", "es_source_term",
+    "es_message_aggregate", "es_target_couple", "es_factorized_workspace_size", "es_factorized_message",
 ]
 
 
@@ -92,6 +98,14 @@ def lib() -> ct.CDLL:
         L.es_attn_bwd.argtypes = [ct.POINTER(AttnDesc)] + [vp] * 17 + [sz, vp]
         L.es_attn_stats_query.argtypes = [ct.POINTER(AttnDesc), ct.c_int64, ct.POINTER(AttnStats)]
         L.es_attn_tiles_layout_query.argtypes = [ct.POINTER(AttnDesc), ct.POINTER(TilesLayout)]
+        md = ct.POINTER(MsgDesc)
+        L.es_translation_coefficients.argtypes = [i32, dp]
+        L.es_source_term.argtypes = [md, vp, vp, vp, vp]
+        L.es_message_aggregate.argtypes = [md, vp, vp, vp, vp, vp]
+        L.es_target_couple.argtypes = [md, vp, vp, vp, vp]
+        L.es_factorized_workspace_size.argtypes = [md]
+        L.es_factorized_workspace_size.restype = sz
+        L.es_factorized_message.argtypes = [md, vp, vp, vp, vp, vp, vp, sz, vp]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]

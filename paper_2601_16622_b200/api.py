@@ -69,9 +69,10 @@ def rotate_features(x: torch.Tensor, L: int, R) -> torch.Tensor:
     """rotate_feature (irreps.hpp:104-112) for the [N][M][C] layout: every
     degree block's value vectors v -> D^l(R) v."""
     out = torch.empty_like(x)
+    wd = torch.float64 if x.dtype == torch.float64 else torch.float32
     for l in range(L + 1):
-        D = torch.tensor(wigner_d(l, R), dtype=torch.float32, device=x.device)
-        blk = x[:, l * l:(l + 1) ** 2, :].float()
+        D = torch.tensor(wigner_d(l, R), dtype=wd, device=x.device)
+        blk = x[:, l * l:(l + 1) ** 2, :].to(wd)
         out[:, l * l:(l + 1) ** 2, :] = torch.einsum("ab,nbc->nac", D, blk).to(x.dtype)
     return out
 
@@ -367,3 +368,51 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_g
                             _ptr(dk), _ptr(dv), _ptr(dpos), _ptr(tiles), _ptr(ws), ws.numel(), _stream()),
           "es_attn_bwd")
     return (dq, dk, dv, dpos) if pos_grad else (dq, dk, dv)
+
+
+# ------------------------------------------------------------------ factorized message
+def translation_coefficients(l: int):
+    """translation_coefficients: w[u] of R^l(a+b) = sum_u w[u] (R^u(a) x R^{l-u}(b))^l."""
+    import numpy as np
+    w = np.zeros(l + 1)
+    check(lib().es_translation_coefficients(int(l), w.ctypes.data_as(ct.POINTER(ct.c_double))),
+          "es_translation_coefficients")
+    return w
+
+
+def _msg_desc(pos, h, K, H, L, origin):
+    d = _lib.MsgDesc()
+    d.N, d.K, d.H, d.L, d.C = h.shape[0], int(K), int(H), int(L), h.shape[2]
+    o = pos.mean(dim=0).tolist() if origin is None else [float(x) for x in origin]
+    for a in range(3):
+        d.origin[a] = o[a]
+    return d
+
+
+def factorized_message(pos: torch.Tensor, h: torch.Tensor, nbr: torch.Tensor, alpha: torch.Tensor, L: int,
+                       origin=None, stages: bool = False):
+    """factorized_message (SPEC.md:369-382; Eq. 5): source_term -> alpha
+    aggregation -> target_couple on the GPU in fp64.  pos [N,3], h [N,M,C],
+    nbr [N,K] int32, alpha [N,K,H] (all float64 except nbr); origin defaults
+    to the centroid (the SPEC's recentring).  stages=True also returns the
+    source terms S and aggregates A ([N, (L+1)^4, C])."""
+    _need(pos, "pos", torch.float64)
+    _need(h, "h", torch.float64)
+    _need(nbr, "nbr", torch.int32)
+    _need(alpha, "alpha", torch.float64)
+    N, K = nbr.shape
+    H = alpha.shape[2]
+    d = _msg_desc(pos, h, K, H, L, origin)
+    out = torch.empty_like(h)
+    if stages:
+        S = torch.empty((N, (L + 1) ** 4, h.shape[2]), dtype=torch.float64, device=h.device)
+        A = torch.empty_like(S)
+        check(lib().es_source_term(ct.byref(d), _ptr(pos), _ptr(h), _ptr(S), _stream()), "es_source_term")
+        check(lib().es_message_aggregate(ct.byref(d), _ptr(nbr), _ptr(alpha), _ptr(S), _ptr(A), _stream()),
+              "es_message_aggregate")
+        check(lib().es_target_couple(ct.byref(d), _ptr(pos), _ptr(A), _ptr(out), _stream()), "es_target_couple")
+        return out, S, A
+    ws = _workspace(lib().es_factorized_workspace_size(ct.byref(d)), h.device)
+    check(lib().es_factorized_message(ct.byref(d), _ptr(pos), _ptr(h), _ptr(nbr), _ptr(alpha), _ptr(out), _ptr(ws),
+                                      ws.numel(), _stream()), "es_factorized_message")
+    return out

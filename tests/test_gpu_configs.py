@@ -326,3 +326,39 @@ def test_tensor_core_backward_without_prebuilt_tiles(es, oracle, dk_path):
     torch.cuda.synchronize()
     for a_, b_ in zip(got, ref):  # uniform vs segment-packed tiles: same sums, other fp32 order, bf16 outputs
         assert rel(d64(a_), d64(b_)) < 1e-2
+
+
+# ------------------------------------------------------------------ factorized message
+@pytest.mark.parametrize("L", [1, 2])
+def test_factorized_message_gpu_equals_edge_centric(es, oracle, L):
+    """GPU factorized_message (fp64 source -> aggregate -> target) equals the
+    oracle's edge_centric_message < 1e-9, after translating by
+    |t| = 100 and 1000 (recentred at the centroid), and is
+    rotation-equivariant (SPEC.md:391)."""
+    from paper_2601_16622_b200 import api
+    n, C, H = 40, 16, 2
+    pos = S.gen_fcc_system(n, 3.8, L)
+    nbr, _, _ = po.build_neighbors(pos, 32, 6.0)
+    rng = np.random.default_rng(L)
+    h = rng.standard_normal((n, (L + 1) ** 2, C))
+    alpha = rng.random((n, 32, H))
+    ref = po.edge_message(pos, h, nbr, alpha, L)
+    scale = np.abs(ref).max()
+    for t in (0.0, 100.0, 1000.0):
+        shift = np.array([0.6, -0.48, 0.64]) * t
+        got = api.factorized_message(dev(pos + shift), dev(h), dev(nbr), dev(alpha), L)
+        torch.cuda.synchronize()
+        assert np.abs(got.cpu().numpy() - ref).max() < 1e-9 * scale, t
+    # translation weights: solved on the device side's host tables == the manifest closed form
+    for l in range(3):
+        np.testing.assert_allclose(api.translation_coefficients(l),
+                                   [po.translation_weight(l, u) for u in range(l + 1)], rtol=1e-10)
+    # stages == fused call; equivariance under a rotation
+    o2, Sg, Ag = api.factorized_message(dev(pos), dev(h), dev(nbr), dev(alpha), L, stages=True)
+    o1 = api.factorized_message(dev(pos), dev(h), dev(nbr), dev(alpha), L)
+    assert torch.equal(o1, o2)
+    R = np.linalg.qr(rng.standard_normal((3, 3)))[0]
+    R *= np.sign(np.linalg.det(R))
+    hr = api.rotate_features(dev(h), L, R)
+    orot = api.factorized_message(dev(pos @ R.T), hr, dev(nbr), dev(alpha), L)
+    assert rel(orot.cpu().numpy(), api.rotate_features(o1, L, R).cpu().numpy()) < 1e-9

@@ -213,3 +213,50 @@ def test_tiles_ref_packing_properties():
         else:
             assert all((c - a) % TR.TQ == 0 or c - a < TR.TQ for c in inner) or TR.pack_parts(N) > 1
     assert TR.tile_starts(300) == [0, 128, 256, 300]
+
+
+# ------------------------------------------------------------------ factorized message
+def test_translation_coefficients_match_manifest_closed_form(oracle):
+    """translation_coefficients: the least-squares weights of
+    R^l(a+b) = sum_u w(l,u) (R^u(a) x R^{l-u}(b))^l equal the closed form of the
+    reference manifest (conventions.hpp:32-34); l=1 is vector additivity."""
+    for l in range(5):
+        w = oracle.translation_coefficients(l)
+        ref = np.array([oracle.translation_weight(l, u) for u in range(l + 1)])
+        np.testing.assert_allclose(w, ref, rtol=1e-10, atol=1e-12)
+    rng = np.random.default_rng(0)
+    for _ in range(200):  # l = 2 reconstruction on random (a, b)
+        a, b = rng.standard_normal(3), rng.standard_normal(3)
+        rec = sum(oracle.translation_weight(2, u) * oracle.tensor_product_dense(
+            oracle.solid_harmonics(u, a), u, oracle.solid_harmonics(2 - u, b), 2 - u, 2).ravel() for u in range(3))
+        assert np.abs(rec - oracle.solid_harmonics(2, a + b)).max() < 1e-10
+
+
+def _msg_case(n, L, C, H, seed):
+    pos = S.gen_fcc_system(n, 3.8, seed)
+    nbr, _, _ = po.build_neighbors(pos, 32, 6.0)
+    rng = np.random.default_rng(seed)
+    h = rng.standard_normal((n, (L + 1) ** 2, C))
+    alpha = rng.random((n, 32, H))
+    return pos, nbr, h, alpha
+
+
+@pytest.mark.parametrize("L", [1, 2])
+def test_factorized_equals_edge_centric(oracle, L):
+    """factorized_message == edge_centric_message < 1e-9 (SPEC.md:385), also
+    after translating the whole system by |t| = 100 and 1000 (the binomial
+    expansion's stress test), with and without recentring."""
+    pos, nbr, h, alpha = _msg_case(24, L, 8, 2, L)
+    ref = oracle.edge_message(pos, h, nbr, alpha, L)
+    scale = np.abs(ref).max()
+    got = oracle.factorized_message(pos, h, nbr, alpha, L)
+    assert np.abs(got - ref).max() < 1e-9 * scale
+    for t in (100.0, 1000.0):
+        shift = np.array([0.6, -0.48, 0.64]) * t
+        ref_t = oracle.edge_message(pos + shift, h, nbr, alpha, L)
+        assert np.abs(ref_t - ref).max() < 1e-9 * scale  # edge-centric is translation invariant
+        got_c = oracle.factorized_message(pos + shift, h, nbr, alpha, L)  # recentred at the centroid
+        assert np.abs(got_c - ref).max() < 1e-9 * scale
+        if t == 100.0:  # absolute coordinates (no recentring): conditioning grows like |t|^(2L)
+            got_abs = oracle.factorized_message(pos + shift, h, nbr, alpha, L, origin=np.zeros(3))
+            assert np.abs(got_abs - ref).max() < 1e-6 * scale
