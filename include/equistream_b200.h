@@ -257,6 +257,14 @@ es_status es_factorized_message(const es_msg_desc* d, const double* pos, const d
                                 const double* alpha, double* out, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/* Dense-CG vs EAAS tensor-product microbenchmark (run_tp_bench
+ * SPEC.md:449-457, Figure 2): P independent pairs, x = sum over
+ * the path set of (v^li (x) R^lf(r))^lo; v, x: [P][M][C] f32, r: [P][3] f32;
+ * L in {2, 4}.  es_tp_madds: multiply-adds per pair-channel of each form. */
+es_status es_tp_bench_dense(int32_t L, int32_t C, int32_t P, const float* v, const float* r, float* x, void* stream);
+es_status es_tp_bench_eaas(int32_t L, int32_t C, int32_t P, const float* v, const float* r, float* x, void* stream);
+es_status es_tp_madds(int32_t L, int64_t* dense_per_channel, int64_t* eaas_per_channel);
+
 /* Host-side introspection of the tables the kernels use. */
 const char* es_conventions_manifest(void);
 double es_cg_real(int32_t l1, int32_t m1, int32_t l2, int32_t m2, int32_t lo, int32_t mo);

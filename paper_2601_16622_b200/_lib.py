@@ -78,6 +78,7 @@ EXPORTS = [
     "es_reindex_table", "es_wigner_d_host", "es_last_error", "es_abi_version", "es_device_ok",
     "es_attn_stats_query", "es_attn_tiles_layout_query", "es_translation_coefficients", "es_source_term",
     "es_message_aggregate", "es_target_couple", "es_factorized_workspace_size", "es_factorized_message",
+    "es_tp_bench_dense", "es_tp_bench_eaas", "es_tp_madds",
 ]
 
 
@@ -106,6 +107,9 @@ def lib() -> ct.CDLL:
         L.es_factorized_workspace_size.argtypes = [md]
         L.es_factorized_workspace_size.restype = sz
         L.es_factorized_message.argtypes = [md, vp, vp, vp, vp, vp, vp, sz, vp]
+        L.es_tp_bench_dense.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+        L.es_tp_bench_eaas.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+        L.es_tp_madds.argtypes = [i32, ct.POINTER(ct.c_int64), ct.POINTER(ct.c_int64)]
         L.es_attn_bwd_workspace_size.argtypes = [ct.POINTER(AttnDesc)]
         L.es_attn_bwd_workspace_size.restype = sz
         L.es_neighbors_build.argtypes = [ct.POINTER(NbrDesc)] + [vp] * 6 + [sz, vp]

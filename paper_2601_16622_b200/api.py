@@ -416,3 +416,22 @@ def factorized_message(pos: torch.Tensor, h: torch.Tensor, nbr: torch.Tensor, al
     check(lib().es_factorized_message(ct.byref(d), _ptr(pos), _ptr(h), _ptr(nbr), _ptr(alpha), _ptr(out), _ptr(ws),
                                       ws.numel(), _stream()), "es_factorized_message")
     return out
+
+
+# ------------------------------------------------------------------ tensor-product microbenchmark
+def tp_madds(L: int):
+    """(dense, EAAS) multiply-adds per pair-channel of the path-set product (run_tp_bench)."""
+    a, b = ct.c_int64(), ct.c_int64()
+    check(lib().es_tp_madds(int(L), ct.byref(a), ct.byref(b)), "es_tp_madds")
+    return a.value, b.value
+
+
+def tensor_product_pairs(v: torch.Tensor, r: torch.Tensor, L: int, method: str = "eaas") -> torch.Tensor:
+    """x_p = sum_paths (v_p^li (x) R^lf(r_p))^lo for P independent pairs, by the dense
+    CG product or by EAAS (the fused kernels' per-pair device code); f32."""
+    _need(v, "v", torch.float32)
+    _need(r, "r", torch.float32, (v.shape[0], 3))
+    x = torch.empty_like(v)
+    fn = lib().es_tp_bench_eaas if method == "eaas" else lib().es_tp_bench_dense
+    check(fn(int(L), v.shape[2], v.shape[0], _ptr(v), _ptr(r), _ptr(x), _stream()), f"es_tp_bench_{method}")
+    return x

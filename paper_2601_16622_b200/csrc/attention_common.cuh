@@ -289,6 +289,9 @@ __device__ __forceinline__ float dbias_of(const KParams& p, float rn) {
 // the closed-form frame R' (rows e1, e2, u') is used only for u'_z >= 0 --
 // branch-stable; any gauge gives the same composite.
 template <int L, bool EAAS>
+__device__ void pair_prepare_vec(const KParams& p, float rx, float ry, float rz, int j, float* rec);
+
+template <int L, bool EAAS>
 __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, int i, int j, float* rec) {
   const int ia = p.row0 + i;
   double dx = pos[3 * j] - pos[3 * ia], dy = pos[3 * j + 1] - pos[3 * ia + 1], dz = pos[3 * j + 2] - pos[3 * ia + 2];
@@ -297,7 +300,12 @@ __device__ void pair_prepare(const KParams& p, const double* __restrict__ pos, i
     dy -= p.by * rint(dy / p.by);
     dz -= p.bz * rint(dz / p.bz);
   }
-  const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+  pair_prepare_vec<L, EAAS>(p, (float)dx, (float)dy, (float)dz, j, rec);
+}
+
+// the per-pair record from the relative vector r_ij itself
+template <int L, bool EAAS>
+__device__ void pair_prepare_vec(const KParams& p, float rx, float ry, float rz, int j, float* rec) {
   const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
   float phi = 1.f;
   if (p.phi_mode == 0) phi = rn < p.r_cut ? 0.5f * (cospif(rn * p.inv_rcut) + 1.f) : 0.f;

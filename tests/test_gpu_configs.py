@@ -362,3 +362,24 @@ def test_factorized_message_gpu_equals_edge_centric(es, oracle, L):
     hr = api.rotate_features(dev(h), L, R)
     orot = api.factorized_message(dev(pos @ R.T), hr, dev(nbr), dev(alpha), L)
     assert rel(orot.cpu().numpy(), api.rotate_features(o1, L, R).cpu().numpy()) < 1e-9
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_tp_microbench_dense_equals_eaas(es, oracle, L):
+    """run_tp_bench: the dense CG product and EAAS agree with
+    the oracle's per-pair operator on the same pairs (fp32), and the madd
+    counts are the survey's: dense 615 / 13075 per pair-channel at L = 2 / 4."""
+    from paper_2601_16622_b200 import api
+    M = (L + 1) ** 2
+    rng = np.random.default_rng(L)
+    v = rng.standard_normal((40, M, 64)).astype(np.float32)
+    r = (rng.standard_normal((40, 3)) * 2.0).astype(np.float32)
+    r[0] = 0.0  # coincident pair: only l_f = 0 paths survive
+    ref = np.stack([po.pair_operator(L, r[p].astype(np.float64), 1, 1e30, 1) @ v[p].astype(np.float64)
+                    for p in range(40)])
+    for method in ("dense", "eaas"):
+        x = api.tensor_product_pairs(dev(v), dev(r), L, method)
+        torch.cuda.synchronize()
+        assert rel(x.cpu().numpy(), ref) < 1e-4, method
+    dm, em = api.tp_madds(L)
+    assert dm == {2: 615, 4: 13075}[L] and dm / em > 5
