@@ -53,6 +53,7 @@ struct AttentionProblem {
   // radial score bias b(r) = bias[0] + bias[1] r + bias[2] r^2 (RadialScalars b)
   bool has_bias = false;
   double bias[3] = {0, 0, 0};
+  int32_t nseg = 0;  // molecule segments of the neighbour index (0: one system) -- picks the kernel family
 
   es_attn_desc desc() const {
     es_attn_desc d{};
@@ -67,6 +68,7 @@ struct AttentionProblem {
     d.Nk = n_keys;
     d.bias_mode = has_bias ? ES_BIAS_POLY2 : ES_BIAS_NONE;
     for (int a = 0; a < 3; ++a) d.bias[a] = bias[a];
+    d.nseg = nseg;
     return d;
   }
 };

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ES_ABI_VERSION 8
+#define ES_ABI_VERSION 9
 
 typedef enum {
   ES_OK = 0,
@@ -99,6 +99,12 @@ typedef struct {
    * b(r) = bias[0] + bias[1] r + bias[2] r^2. */
   int32_t bias_mode;
   double bias[3];
+  /* Segments of the neighbour index (molecule batches: the nseg given to
+   * es_neighbors_build; 0 for one system).  Picks the kernel family: the
+   * tensor-core tiles pay off where a 128-row tile's keys are its own few
+   * molecules; one bulk system (~50 neighbours spread over ~150 key chunks
+   * per tile) runs faster on the per-atom SIMT kernels. */
+  int32_t nseg;
 } es_attn_desc;
 
 /* Compiled kernel set: L in [0, 4]; C a multiple of 32 up to 256; C/H in

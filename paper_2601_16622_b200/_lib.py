@@ -22,10 +22,11 @@ class AttnDesc(ct.Structure):
     _fields_ = [("N", ct.c_int32), ("K", ct.c_int32), ("H", ct.c_int32), ("L", ct.c_int32), ("C", ct.c_int32),
                 ("value_mode", ct.c_int32), ("phi_mode", ct.c_int32), ("dtype", ct.c_int32),
                 ("r_cut", ct.c_double), ("periodic", ct.c_int32), ("box", ct.c_double * 3),
-                ("row0", ct.c_int32), ("Nk", ct.c_int32), ("bias_mode", ct.c_int32), ("bias", ct.c_double * 3)]
+                ("row0", ct.c_int32), ("Nk", ct.c_int32), ("bias_mode", ct.c_int32), ("bias", ct.c_double * 3),
+                ("nseg", ct.c_int32)]
 
 
-ABI_VERSION = 8  # include/equistream_b200.h ES_ABI_VERSION
+ABI_VERSION = 9  # include/equistream_b200.h ES_ABI_VERSION
 
 
 class NbrDesc(ct.Structure):

@@ -102,6 +102,10 @@ class NeighborIndex:
     def K(self) -> int:
         return self.table.shape[1]
 
+    @property
+    def nseg(self) -> int:
+        return 0 if self.seg_ptr is None else int(self.seg_ptr.numel()) - 1
+
     def tiles(self, d: "_lib.AttnDesc") -> torch.Tensor | None:
         """The tile structures (tile-skip mask, chunk lists, per-row chunk
         masks and slot order) the tensor-core kernels walk for this index --
@@ -250,7 +254,8 @@ class AttentionConfig:
     bias: tuple | None = None  # radial score bias b(r) = b0 + b1 r + b2 r^2 (None: b == 0)
     keep_scores: bool = False  # the forward keeps the O(N K H) scores for the backward (pays with ES_DK_TC=1)
 
-    def desc(self, N: int, K: int, C: int, dtype: torch.dtype, row0: int = 0, Nk: int = 0) -> _lib.AttnDesc:
+    def desc(self, N: int, K: int, C: int, dtype: torch.dtype, row0: int = 0, Nk: int = 0,
+             nseg: int = 0) -> _lib.AttnDesc:
         if self.value_mode not in _VALUE:
             raise EsInvalidArgument(f"value_mode must be one of {list(_VALUE)}")
         if self.phi not in _PHI:
@@ -261,6 +266,7 @@ class AttentionConfig:
         d.phi_mode = _PHI[self.phi]
         d.dtype = _DT[dtype]
         d.r_cut = float(self.r_cut)
+        d.nseg = int(nseg)
         if self.bias is not None:
             b = tuple(float(x) for x in self.bias) + (0.0,) * (3 - len(self.bias))
             d.bias_mode = _lib.ES_BIAS_POLY2
@@ -326,7 +332,7 @@ def stream_aggregate(q, k, v, pos, idx: NeighborIndex, cfg: AttentionConfig, row
     out = torch.empty((N,) + tuple(v.shape[1:]), dtype=v.dtype, device=v.device)
     lse = torch.empty((N, cfg.heads), dtype=torch.float32, device=v.device)
     scores = torch.empty((cfg.heads, N, idx.K), dtype=torch.float32, device=v.device) if return_scores else None
-    d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk)
+    d = cfg.desc(N, idx.K, C, q.dtype, row0, Nk, idx.nseg if row0 == 0 and Nk == N else 0)
     tiles = idx.tiles(d)
     ws = _workspace(256 if tiles is not None else lib().es_attn_fwd_workspace_size(ct.byref(d)), q.device)
     check(lib().es_attn_fwd(ct.byref(d), _ptr(q), _ptr(k), _ptr(v), _ptr(pos), _ptr(idx.table), _ptr(out),
@@ -355,7 +361,7 @@ def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_g
     N, C, Nk = _check_qkv(s.q, s.k, s.v, s.pos, s.idx, s.cfg, s.row0)
     grad_m = _need(grad_m.contiguous(), "grad_m", s.q.dtype, tuple(s.out.shape))
     rev_ptr, rev_pair = s.idx.transpose(Nk)
-    d = s.cfg.desc(N, s.idx.K, C, s.q.dtype, s.row0, Nk)
+    d = s.cfg.desc(N, s.idx.K, C, s.q.dtype, s.row0, Nk, s.idx.nseg if s.row0 == 0 and Nk == N else 0)
     ws = _workspace(lib().es_attn_bwd_workspace_size(ct.byref(d)), s.q.device)
     dq = torch.empty_like(s.q)
     dk = torch.empty_like(s.k)

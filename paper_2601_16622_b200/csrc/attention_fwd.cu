@@ -216,7 +216,10 @@ bool use_tc_kernel(const AttnArgs& a) {
   // one 128-query tile per CTA: below ~half a wave of tiles (N < 74 * 128)
   // the per-atom SIMT kernel fills the GPU better (r01b sweep: SIMT faster
   // at N = 1k..5k, tie at 10k, tcgen05 faster from 20k)
-  const bool enough_tiles = (a.N + 127) / 128 >= 74;
+  // and only for molecule batches: on one bulk system a tile's ~50-neighbour rows spread over ~150 key
+  // chunks and the per-atom SIMT kernel wins (configs[2]/[4] at 20k / 100k atoms: 0.89 / 5.2 ms vs
+  // 1.13 / 8.6 ms forward, profiles/r02_dispatch.txt)
+  const bool enough_tiles = (a.N + 127) / 128 >= 74 && a.nseg > 0;
   return use_tc && (enough_tiles || use_tc == 2) && attn_tc_supported(a);
 }
 }  // namespace

@@ -1401,7 +1401,7 @@ bool attn_dq_tc_applicable(const AttnArgs& a) {
     const char* e = getenv("ES_ATTN_TC");
     use = (e && e[0] == '0') ? 0 : (e && e[0] == '1') ? 2 : 1;
   }
-  const bool enough_tiles = (a.N + TQ - 1) / TQ >= 74;
+  const bool enough_tiles = (a.N + TQ - 1) / TQ >= 74 && a.nseg > 0;  // molecule batches (see attn_fwd_launch)
   const bool idx32 = (size_t)a.N * a.K * 8 < ((size_t)1 << 31);  // 32-bit gather offsets
   return use && (enough_tiles || use == 2) && a.K <= DQ_KMAX && idx32 && attn_tc_supported(a);
 }

@@ -66,6 +66,7 @@ AttnArgs to_args(const es_attn_desc* d) {
   a.tau = (float)(1.0 / std::sqrt((double)M * (a.Dq / d->H)));
   a.r_cut = (float)d->r_cut;
   for (int x = 0; x < 3; ++x) a.box[x] = d->box[x];
+  a.nseg = d->nseg > 0 ? d->nseg : 0;
   a.bias_mode = d->bias_mode;
   for (int x = 0; x < 3; ++x) a.bias[x] = d->bias_mode ? (float)d->bias[x] : 0.f;
   return a;

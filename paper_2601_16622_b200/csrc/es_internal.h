@@ -44,6 +44,7 @@ struct AttnArgs {
   int value_mode, phi_mode, dtype, periodic;
   float tau, r_cut;
   double box[3];
+  int nseg = 0;                      // molecule segments of the index (0: one system)
   int bias_mode = 0;                 // es_bias_mode
   float bias[3] = {0.f, 0.f, 0.f};   // b(r) = bias[0] + bias[1] r + bias[2] r^2
   const void* tiles = nullptr;  // prebuilt tile lists (es_attn_tiles_build) or NULL

@@ -117,6 +117,7 @@ int main(int argc, char** argv) {
     ea::AttentionProblem p;
     p.N = N; p.K = K; p.heads = H; p.lmax = L; p.channels = C;
     p.dtype = bf ? ea::DType::BF16 : ea::DType::F32;
+    p.nseg = nseg;
     const size_t tiles = ea::tiles_workspace_size(p);
     void* dtiles = tiles ? dalloc<char>(tiles) : nullptr;
     if (tiles) ea::build_tiles(p, idx, dtiles, tiles, nullptr, dseg, nseg);
