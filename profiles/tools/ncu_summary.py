@@ -70,10 +70,14 @@ def main(rep, as_json, traffic=False):
             name = e["kernel"].split("(")[0].split("::")[-1].split("<")[0].strip()
             if name in out["bytes_per_launch"]:
                 continue
+            byt = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            tns = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}
+            rd = (e.get("dram_read") or 0) * byt.get(e.get("dram_read_unit", "byte"), 1)
+            wr = (e.get("dram_write") or 0) * byt.get(e.get("dram_write_unit", "byte"), 1)
             out["bytes_per_launch"][name] = {
-                "dram_read": e.get("dram_read"), "dram_write": e.get("dram_write"),
-                "total": (e.get("dram_read") or 0) + (e.get("dram_write") or 0),
-                "tensor_pipe_pct": e.get("tensor_pipe_pct"), "duration_ns": e.get("duration")}
+                "dram_read": round(rd), "dram_write": round(wr), "total": round(rd + wr),
+                "tensor_pipe_pct": e.get("tensor_pipe_pct"),
+                "duration_ns": round((e.get("duration") or 0) * tns.get(e.get("duration_unit", "nsecond"), 1))}
         print(json.dumps(out, indent=1))
         return
     for e in res:
