@@ -71,7 +71,7 @@ def main(rep, as_json, traffic=False):
             if name in out["bytes_per_launch"]:
                 continue
             byt = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-            tns = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9}
+            tns = {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9}
             rd = (e.get("dram_read") or 0) * byt.get(e.get("dram_read_unit", "byte"), 1)
             wr = (e.get("dram_write") or 0) * byt.get(e.get("dram_write_unit", "byte"), 1)
             out["bytes_per_launch"][name] = {
