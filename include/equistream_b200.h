@@ -160,8 +160,8 @@ es_status es_attn_fwd(const es_attn_desc* d, const void* q, const void* k, const
  * come from es_neighbors_transpose on the same nbr.
  * dpos (optional, NULL = skip): [Nk][3] f64 gradient of sum <dout, out> with
  * respect to the atom positions (forces for the conservative mode, PAPER.md:
- * 786) through phi(r_ij) and the solid harmonics of the value
- * map; L = 2 only (ES_UNSUPPORTED otherwise).  Overwritten, not accumulated. */
+ * 786) through phi(r_ij), the solid harmonics of the value map
+ * and the radial bias b(r_ij); every L.  Overwritten, not accumulated. */
 size_t es_attn_bwd_workspace_size(const es_attn_desc* d);
 /* scores (optional): the forward's scores output for the same inputs; NULL
  * recomputes them. */

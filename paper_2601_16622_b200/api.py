@@ -354,7 +354,7 @@ def attn_stats(cfg: AttentionConfig, N: int, K: int, C: int, n_pairs: int, dtype
 def stream_aggregate_backward(grad_m: torch.Tensor, saved: SavedAttention, pos_grad: bool = False):
     """stream_aggregate_backward (SPEC.md:293): (grad_q, grad_k, grad_v) of
     sum <grad_m, m>, by recomputation (no O(N*K*C) buffer).  pos_grad=True
-    (L = 2) also returns grad_pos [Nk][3] f64 -- the position gradient through
+    (any L) also returns grad_pos [Nk][3] f64 -- the position gradient through
     phi(r_ij) and the solid harmonics of the value map (forces):
     (grad_q, grad_k, grad_v, grad_pos)."""
     s = saved

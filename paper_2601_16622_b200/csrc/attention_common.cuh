@@ -262,6 +262,53 @@ __device__ __forceinline__ void solid2_grad(float x, float y, float z, float (&Y
   Y[8] = 0.5f * c2 * (x * x - y * y); G[8][0] = c2 * x; G[8][1] = -c2 * y; G[8][2] = 0.f;
 }
 
+// Forward-mode derivative (value + gradient in x, y, z): the solid harmonics of
+// any degree and their gradients from the same recursion (position gradients
+// for every L).
+struct D3 {
+  float v, x, y, z;
+};
+__device__ __forceinline__ D3 operator+(D3 a, D3 b) { return {a.v + b.v, a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ D3 operator-(D3 a, D3 b) { return {a.v - b.v, a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ D3 operator*(D3 a, D3 b) {
+  return {a.v * b.v, a.v * b.x + a.x * b.v, a.v * b.y + a.y * b.v, a.v * b.z + a.z * b.v};
+}
+__device__ __forceinline__ D3 operator*(float s, D3 a) { return {s * a.v, s * a.x, s * a.y, s * a.z}; }
+
+// sh_degree<l> with its gradient: out[m] = |r|^l Y_lm(r) and d/d(x, y, z)
+template <int l>
+__device__ __forceinline__ void sh_degree_d3(float px, float py, float pz, D3* out) {
+  if constexpr (l == 0) {
+    out[0] = {0.28209479177387814f, 0.f, 0.f, 0.f};
+  } else {
+    const D3 x = {px, 1.f, 0.f, 0.f}, y = {py, 0.f, 1.f, 0.f}, z = {pz, 0.f, 0.f, 1.f};
+    const D3 r2 = x * x + y * y + z * z;
+    D3 a = {1.f, 0.f, 0.f, 0.f}, b = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int mu = 0; mu <= l; ++mu) {
+      if (mu > 0) {
+        const D3 an = a * x - b * y, bn = a * y + b * x;
+        a = an; b = bn;
+      }
+      float pcs = 1.f;
+#pragma unroll
+      for (int k = 2 * mu - 1; k > 1; k -= 2) pcs *= (float)k;
+      D3 p2 = {0.f, 0.f, 0.f, 0.f}, pc = {pcs, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ll = mu + 1; ll <= l; ++ll) {
+        const D3 pn = (1.f / (float)(ll - mu)) * ((float)(2 * ll - 1) * (z * pc) - (float)(ll + mu - 1) * (r2 * p2));
+        p2 = pc; pc = pn;
+      }
+      const D3 nrm = c_tab.shnorm[l][mu] * pc;
+      if (mu == 0) out[l] = nrm;
+      else {
+        out[l + mu] = ((mu & 1) ? -1.f : 1.f) * (nrm * a);
+        out[l - mu] = nrm * b;
+      }
+    }
+  }
+}
+
 struct KParams {
   int N, K, H, C, Dq;
   int row0, Nk;  // query i <-> atom row0 + i (pos); keys j index k/v/pos in [0, Nk)

@@ -213,7 +213,6 @@ es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const
   return guarded([&] {
     es_status s = check_attn(d);
     if (s != ES_OK) return s;
-    if (dpos && d->L != 2) return fail(ES_UNSUPPORTED, "attn_bwd: position gradients need L = 2");
     if (d->N == 0) {
       // No query rows: dk / dv are still [Nk] outputs (a row shard with an empty slab contributes zeros to the
       // reduce-scatter), and dpos is overwritten.

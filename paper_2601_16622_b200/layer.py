@@ -25,7 +25,7 @@ class _AttnFn(torch.autograd.Function):
     def backward(ctx, grad_out):
         h, W, q, k, v, out, lse, pos = ctx.saved_tensors
         saved = SavedAttention(q, k, v, pos, ctx.idx, out, lse, ctx.cfg, scores=ctx.scores)
-        want_pos = ctx.needs_input_grad[2]  # positions require grad: forces (L = 2)
+        want_pos = ctx.needs_input_grad[2]  # positions require grad: forces
         grads = stream_aggregate_backward(grad_out.contiguous().to(q.dtype), saved, pos_grad=want_pos)
         dq, dk, dv = grads[:3]
         dh, dW = project_qk_backward(h, W, ctx.cfg.L, dq, dk, dv, want_dW=ctx.needs_input_grad[1])

@@ -473,10 +473,9 @@ def test_position_gradients_match_finite_differences(es, oracle, kind, vm, dtype
     assert np.abs(got.sum(0)).max() < 1e-4 * np.abs(got).max()
 
 
-def test_position_gradients_autograd_and_unsupported(es):
-    """pos.requires_grad through the autograd layer; L != 2 is ES_UNSUPPORTED."""
-    from paper_2601_16622_b200 import _lib
-    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention
+def test_position_gradients_autograd(es):
+    """pos.requires_grad through the autograd layer returns finite forces."""
+    from paper_2601_16622_b200.api import AttentionConfig
     L, C, H = 2, 64, 8
     b = S.molecule_batch(4, 20, 30, 26)
     pos = dev(b.pos).requires_grad_(True)
@@ -486,11 +485,30 @@ def test_position_gradients_autograd_and_unsupported(es):
     out = es.attention_layer(h, W, pos, idx, AttentionConfig(heads=H, L=L))
     out.square().sum().backward()
     assert pos.grad is not None and torch.isfinite(pos.grad).all() and pos.grad.abs().max() > 0
-    q = torch.randn(10, 4, 2 * C, device="cuda")
-    k, v = q.clone(), torch.randn(10, 4, C, device="cuda")
-    p1 = dev(S.gen_fcc_system(10, 3.8, 1))
-    i1 = es.build_neighbors(p1, 16, 6.0)
-    cfg = AttentionConfig(heads=H, L=1)
-    o1, l1 = es.stream_aggregate(q, k, v, p1, i1, cfg)
-    with pytest.raises(_lib.EsUnsupported):
-        es.stream_aggregate_backward(torch.ones_like(o1), SavedAttention(q, k, v, p1, i1, o1, l1, cfg), pos_grad=True)
+
+
+@pytest.mark.parametrize("L,C,H", [(0, 32, 4), (1, 64, 8), (3, 64, 4), (4, 128, 8)])
+def test_position_gradients_every_degree(es, oracle, L, C, H):
+    """Forces at every L (config 4 is L = 4): the generated
+    D_f = dO.(G_f v) contraction and forward-mode solid-harmonic gradients
+    against central differences of the fp64 oracle forward, fp32 1e-5; with a
+    radial bias, whose b'(r) term they include."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    pos = S.gen_fcc_system(30, 3.8, 40 + L)
+    N = len(pos)
+    nbr, _, _ = po.build_neighbors(pos, 64, 6.0)
+    q, k, v = po.project(S.random_features(N, L, C, 41), S.random_weights(L, C, 41), L)
+    M = (L + 1) ** 2
+    dout = np.random.default_rng(42).standard_normal((N, M, C))
+    bias = (0.2, -0.15, 0.03)
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE, bias=bias)
+    ref = _fd_pos_grad(P, q, k, v, pos, nbr, dout)
+    cfg = AttentionConfig(heads=H, L=L, bias=bias)
+    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    tq, tk, tv, tp = dev(q, torch.float32), dev(k, torch.float32), dev(v, torch.float32), dev(pos)
+    out, lse = es.stream_aggregate(tq, tk, tv, tp, idx, cfg)
+    *_, dpos = es.stream_aggregate_backward(dev(dout, torch.float32), SavedAttention(tq, tk, tv, tp, idx, out, lse,
+                                                                                     cfg), pos_grad=True)
+    got = dpos.cpu().numpy()
+    assert rel(got, ref) < F32_TOL
+    assert np.abs(got.sum(0)).max() < 1e-4 * np.abs(got).max()
