@@ -126,35 +126,155 @@ class CudaBackend:
         return self.api.stream_aggregate_backward(g_loc, saved)
 
 
+def _all_gather_start(x_loc: torch.Tensor, plan: RowPlan, group=None):
+    """Asynchronous all_gather_rows: returns (work, finish) -- finish() waits and
+    yields the [N, ...] tensor."""
+    per = plan.per
+    pad = torch.zeros((per,) + tuple(x_loc.shape[1:]), dtype=x_loc.dtype, device=x_loc.device)
+    pad[: x_loc.shape[0]] = x_loc
+    if _is_nccl():
+        out = torch.empty((per * plan.world,) + tuple(x_loc.shape[1:]), dtype=x_loc.dtype, device=x_loc.device)
+        work = dist.all_gather_into_tensor(out, pad, group=group, async_op=True)
+        return lambda: (work.wait(), out[: plan.N])[1]
+    parts = [torch.empty_like(pad) for _ in range(plan.world)]
+    work = dist.all_gather(parts, pad, group=group, async_op=True)
+    return lambda: (work.wait(), torch.cat(parts)[: plan.N])[1]
+
+
+def _reduce_scatter_start(x_all: torch.Tensor, plan: RowPlan, rank: int, group=None):
+    """Asynchronous reduce_scatter_rows: returns finish() -> this rank's slab."""
+    per = plan.per
+    pad = torch.zeros((per * plan.world,) + tuple(x_all.shape[1:]), dtype=x_all.dtype, device=x_all.device)
+    pad[: plan.N] = x_all
+    a0, a1 = plan.rows(rank)
+    if _is_nccl():
+        out = torch.empty((per,) + tuple(x_all.shape[1:]), dtype=x_all.dtype, device=x_all.device)
+        work = dist.reduce_scatter_tensor(out, pad, group=group, async_op=True)
+        return lambda: (work.wait(), out[: a1 - a0])[1]
+    work = dist.all_reduce(pad, group=group, async_op=True)  # gloo has no reduce_scatter (test harness)
+    return lambda: (work.wait(), pad[rank * per:rank * per + (a1 - a0)])[1]
+
+
+def interior_span(table_loc: torch.Tensor, a0: int, a1: int):
+    """The longest contiguous run [b_lo, b_hi) of local rows whose neighbours all
+    lie in this rank's own slab [a0, a1): those rows can run against the local
+    K/V while the all-gather is in flight (x-sorted slabs: the slab's middle)."""
+    t = table_loc
+    inside = ((t < 0) | ((t >= a0) & (t < a1))).all(dim=1).to(torch.int8).cpu().numpy()
+    best, cur, start = (0, 0), 0, 0
+    for r, f in enumerate(inside):
+        if f:
+            if cur == 0:
+                start = r
+            cur += 1
+            if cur > best[1] - best[0]:
+                best = (start, r + 1)
+        else:
+            cur = 0
+    return best
+
+
 class RowShardedAttention:
     """One attention layer of one large system, query rows sharded over ranks.
 
     forward(h_loc, W, pos, table_loc) -> out_loc
     backward(g_loc) -> (dh_loc, dW)          (dW summed over ranks)
     `table_loc` is the neighbour index of this rank's rows (global key ids),
-    e.g. rows [a0, a1) of build_neighbors on the replicated positions.
+    e.g. rows [a0, a1) of build_neighbors on the replicated positions
+    (es_neighbors_build with row0 / nrows).
+
+    overlap=True (default with world > 1): the K/V all-gather runs
+    asynchronously while the slab's interior rows (every neighbour inside the
+    slab, `interior_span`) attend to the local K/V; the boundary rows follow
+    once the gather lands.  In the backward the boundary rows' dk/dv partials
+    are reduce-scattered asynchronously while the interior rows' backward
+    (local keys only) runs.
     """
 
-    def __init__(self, N: int, backend, rank: int, world: int, group=None):
+    def __init__(self, N: int, backend, rank: int, world: int, group=None, overlap: bool = True):
         self.plan = RowPlan(N, world)
         self.backend = backend
         self.rank, self.world, self.group = rank, world, group
         self.a0, self.a1 = self.plan.rows(rank)
+        self.overlap = (overlap and world > 1) or overlap == "force"  # "force": exercise the path at world 1
+        self._span_key = None
+
+    def _span(self, table_loc):
+        key = (table_loc.data_ptr(), tuple(table_loc.shape))
+        if self._span_key != key:
+            self._span_val = interior_span(table_loc, self.a0, self.a1)
+            self._span_key = key
+        return self._span_val
+
+    def _local_pos(self, pos):
+        p = pos[self.a0:self.a1]
+        return p if p.data_ptr() % 16 == 0 else p.contiguous().clone()  # es_attn_fwd: 16-byte aligned
 
     def forward(self, h_loc, W, pos, table_loc):
         q, k_loc, v_loc = self.backend.project(h_loc, W)
-        k = all_gather_rows(k_loc, self.plan, self.group)  # one K/V all-gather per layer
-        v = all_gather_rows(v_loc, self.plan, self.group)
-        out, lse, idx = self.backend.attn_fwd(q, k, v, pos, table_loc, self.a0)
-        self._saved = (h_loc, W, q, k, v, pos, idx, out, lse)
+        b_lo, b_hi = self._span(table_loc) if self.overlap else (0, 0)
+        if b_hi <= b_lo:  # nothing to overlap: one blocking all-gather per layer
+            k = all_gather_rows(k_loc, self.plan, self.group)
+            v = all_gather_rows(v_loc, self.plan, self.group)
+            out, lse, idx = self.backend.attn_fwd(q, k, v, pos, table_loc, self.a0)
+            self._saved = (h_loc, W, q, k, v, pos, [(0, q.shape[0], idx, False)], out, lse)
+            return out
+        fin_k = _all_gather_start(k_loc, self.plan, self.group)
+        fin_v = _all_gather_start(v_loc, self.plan, self.group)
+        # interior rows against the local keys (ids remapped into the slab) while the gather is in flight
+        t_int = table_loc[b_lo:b_hi]
+        t_int = torch.where(t_int >= 0, t_int - self.a0, t_int).contiguous()
+        pos_loc = self._local_pos(pos)
+        o_i, l_i, idx_i = self.backend.attn_fwd(q[b_lo:b_hi].contiguous(), k_loc, v_loc, pos_loc, t_int, b_lo)
+        k, v = fin_k(), fin_v()
+        outs, lses, parts = [], [], []
+        for r0, r1, interior in ((0, b_lo, False), (b_lo, b_hi, True), (b_hi, q.shape[0], False)):
+            if r1 <= r0:
+                continue
+            if interior:
+                outs.append(o_i); lses.append(l_i); parts.append((r0, r1, idx_i, True))
+                continue
+            o_b, l_b, idx_b = self.backend.attn_fwd(q[r0:r1].contiguous(), k, v, pos, table_loc[r0:r1].contiguous(),
+                                                    self.a0 + r0)
+            outs.append(o_b); lses.append(l_b); parts.append((r0, r1, idx_b, False))
+        out, lse = torch.cat(outs), torch.cat(lses)
+        self._saved = (h_loc, W, q, k, v, pos, parts, out, lse)
         return out
 
     def backward(self, g_loc):
-        h_loc, W, q, k, v, pos, idx, out, lse = self._saved
-        dq, dk_all, dv_all = self.backend.attn_bwd(g_loc, q, k, v, pos, idx, out, lse, self.a0)
-        acc = torch.float32 if dk_all.dtype in (torch.bfloat16, torch.float16) else dk_all.dtype  # sum in >= fp32
-        dk = reduce_scatter_rows(dk_all.to(acc), self.plan, self.rank, self.group).to(dk_all.dtype)
-        dv = reduce_scatter_rows(dv_all.to(acc), self.plan, self.rank, self.group).to(dv_all.dtype)
+        h_loc, W, q, k, v, pos, parts, out, lse = self._saved
+        acc = torch.float32 if k.dtype in (torch.bfloat16, torch.float16) else k.dtype  # sum in >= fp32
+        dq = torch.empty_like(q)
+        dk_all = dv_all = None
+        for r0, r1, idx, interior in parts:  # boundary rows first: their partials go out asynchronously
+            if interior:
+                continue
+            dq_b, dk_b, dv_b = self.backend.attn_bwd(g_loc[r0:r1].contiguous(), q[r0:r1].contiguous(), k, v, pos, idx,
+                                                     out[r0:r1].contiguous(), lse[r0:r1].contiguous(), self.a0 + r0)
+            dq[r0:r1] = dq_b
+            dk_all = dk_b.to(acc) if dk_all is None else dk_all + dk_b.to(acc)
+            dv_all = dv_b.to(acc) if dv_all is None else dv_all + dv_b.to(acc)
+        if dk_all is None:  # every row interior: the other ranks still expect this rank's (zero) partials
+            dk_all = torch.zeros(k.shape, dtype=acc, device=k.device)
+            dv_all = torch.zeros(v.shape, dtype=acc, device=v.device)
+        fin_dk = _reduce_scatter_start(dk_all, self.plan, self.rank, self.group)
+        fin_dv = _reduce_scatter_start(dv_all, self.plan, self.rank, self.group)
+        dk_int = dv_int = None
+        for r0, r1, idx, interior in parts:  # interior rows (local keys) overlap the reduce-scatter
+            if not interior:
+                continue
+            n_loc = self.a1 - self.a0
+            dq_i, dk_int, dv_int = self.backend.attn_bwd(g_loc[r0:r1].contiguous(), q[r0:r1].contiguous(),
+                                                         k[self.a0:self.a1].contiguous(),
+                                                         v[self.a0:self.a1].contiguous(), self._local_pos(pos), idx,
+                                                         out[r0:r1].contiguous(), lse[r0:r1].contiguous(), r0)
+            assert dk_int.shape[0] == n_loc
+            dq[r0:r1] = dq_i
+        dk, dv = fin_dk(), fin_dv()
+        if dk_int is not None:
+            dk = dk + dk_int.to(acc)
+            dv = dv + dv_int.to(acc)
+        dk, dv = dk.to(k.dtype), dv.to(v.dtype)
         dh, dW = self.backend.project_bwd(h_loc, W, dq, dk.contiguous(), dv.contiguous())
         if dW is not None:
             dist.all_reduce(dW, group=self.group)

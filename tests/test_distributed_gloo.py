@@ -38,16 +38,16 @@ class OracleBackend:
         return full
 
     def attn_fwd(self, q_loc, k, v, pos, table_loc, row0):
-        nk = k.shape[0]  # all atoms (all-gather) or own slab + halo (halo exchange)
+        nk = k.shape[0]  # all atoms (all-gather), own slab (overlapped interior rows) or slab + halo
         nbr = -np.ones((nk, table_loc.shape[1]), np.int32)
         nbr[row0:row0 + len(table_loc)] = table_loc.numpy()
         out, lse = po.attn_fwd(self.P, self._full(q_loc.numpy(), row0, nk), k.numpy(), v.numpy(), pos.numpy(), nbr)
         n = len(table_loc)
-        self._ctx = (nbr, out, lse)
-        return torch.from_numpy(out[row0:row0 + n]), torch.from_numpy(lse[row0:row0 + n]), None
+        ctx = (nbr, out, lse)  # travels as the "index" of this call to its backward
+        return torch.from_numpy(out[row0:row0 + n]), torch.from_numpy(lse[row0:row0 + n]), ctx
 
     def attn_bwd(self, g_loc, q_loc, k, v, pos, idx, out, lse, row0):
-        nbr, out_f, lse_f = self._ctx
+        nbr, out_f, lse_f = idx
         nk = k.shape[0]
         dq, dk, dv = po.attn_bwd(self.P, self._full(q_loc.numpy(), row0, nk), k.numpy(), v.numpy(), pos.numpy(), nbr,
                                  out_f, lse_f, self._full(g_loc.numpy(), row0, nk))
@@ -102,6 +102,59 @@ def test_row_sharding_gloo_matches_unsharded(tmp_path, oracle, world, halo):
     q, k, v = po.project(h, W, L)
     out, lse = po.attn_fwd(P, q, k, v, b.pos, nbr)
     dq, dk, dv = po.attn_bwd(P, q, k, v, b.pos, nbr, out, lse, g)
+    dh, dW = po.project_bwd(h, W, L, dq, dk, dv)
+    np.testing.assert_allclose(got["out"], out, atol=1e-12 * np.abs(out).max())
+    np.testing.assert_allclose(got["dh"], dh, atol=1e-12 * np.abs(dh).max())
+    np.testing.assert_allclose(got["dW"], dW, atol=1e-12 * np.abs(dW).max())
+
+
+def _overlap_worker(rank, world, port, outdir):
+    """x-sorted open FCC system: each slab has interior rows (every neighbour in
+    the slab) that attend to the local K/V while the all-gather is in flight."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    pos = S.gen_fcc_system(400, 3.8, 7)  # site order: x-major -> slabs are x-slabs
+    N = len(pos)
+    h = S.random_features(N, L, C, 8)
+    W = S.random_weights(L, C, 8)
+    g = np.random.default_rng(9).standard_normal((N, (L + 1) ** 2, C))
+    nbr, _, _ = po.build_neighbors(pos, K, 6.0)
+    layer = D.RowShardedAttention(N, OracleBackend(N), rank, world)
+    a0, a1 = layer.a0, layer.a1
+    tl = torch.from_numpy(nbr[a0:a1].copy())
+    span = D.interior_span(tl, a0, a1)
+    out = layer.forward(torch.from_numpy(h[a0:a1].copy()), torch.from_numpy(W), torch.from_numpy(pos), tl)
+    dh, dW = layer.backward(torch.from_numpy(g[a0:a1].copy()))
+    out_all = D.all_gather_rows(out, layer.plan)
+    dh_all = D.all_gather_rows(dh, layer.plan)
+    sp = torch.tensor([span[0], span[1]], dtype=torch.int64)
+    spans = [torch.zeros_like(sp) for _ in range(world)]
+    dist.all_gather(spans, sp)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "ovl.npz"), out=out_all.numpy(), dh=dh_all.numpy(), dW=dW.numpy(),
+                 spans=np.stack([x.numpy() for x in spans]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharding_overlapped_gather_gloo(tmp_path, oracle, world):
+    """RowShardedAttention(overlap=True): interior rows run before the K/V
+    all-gather lands, boundary partials are reduce-scattered while the interior
+    backward runs -- identical to the unsharded layer."""
+    mp.spawn(_overlap_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    got = np.load(tmp_path / "ovl.npz")
+    # the end slabs have rows to overlap (a thin middle slab of world 3 has none: every row sees both faces)
+    assert got["spans"][0, 1] > got["spans"][0, 0] and got["spans"][-1, 1] > got["spans"][-1, 0]
+    pos = S.gen_fcc_system(400, 3.8, 7)
+    h = S.random_features(len(pos), L, C, 8)
+    W = S.random_weights(L, C, 8)
+    g = np.random.default_rng(9).standard_normal((len(pos), (L + 1) ** 2, C))
+    nbr, _, _ = po.build_neighbors(pos, K, 6.0)
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE)
+    q, k, v = po.project(h, W, L)
+    out, lse = po.attn_fwd(P, q, k, v, pos, nbr)
+    dq, dk, dv = po.attn_bwd(P, q, k, v, pos, nbr, out, lse, g)
     dh, dW = po.project_bwd(h, W, L, dq, dk, dv)
     np.testing.assert_allclose(got["out"], out, atol=1e-12 * np.abs(out).max())
     np.testing.assert_allclose(got["dh"], dh, atol=1e-12 * np.abs(dh).max())

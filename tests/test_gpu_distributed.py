@@ -27,7 +27,7 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("halo", [False, True])
+@pytest.mark.parametrize("halo", [False, True, "overlap"])
 def test_sharded_layer_nccl_world1_matches_layer(nccl_group, halo):
     import paper_2601_16622_b200 as es
     from paper_2601_16622_b200 import distributed as D
@@ -41,8 +41,10 @@ def test_sharded_layer_nccl_world1_matches_layer(nccl_group, halo):
     h = torch.tensor(S.random_features(N, L, C, 42), device="cuda", dtype=torch.float32)
     W = torch.tensor(S.random_weights(L, C, 42), device="cuda", dtype=torch.float32)
     g = torch.randn(N, 9, C, device="cuda", generator=torch.Generator(device="cuda").manual_seed(0))
-    cls = D.HaloShardedAttention if halo else D.RowShardedAttention
-    layer = cls(N, D.CudaBackend(cfg), 0, 1)
+    if halo == "overlap":  # the overlapped path (async NCCL gather / reduce-scatter, local-key interior rows)
+        layer = D.RowShardedAttention(N, D.CudaBackend(cfg), 0, 1, overlap="force")
+    else:
+        layer = (D.HaloShardedAttention if halo else D.RowShardedAttention)(N, D.CudaBackend(cfg), 0, 1)
     out = layer.forward(h, W, pos, idx.table)
     dh, dW = layer.backward(g)
     hr = h.clone().requires_grad_(True)
