@@ -637,6 +637,9 @@ def roofline(wl, t, kt_fwd, kt_bwd, kt_step, n_loc, E, s_bytes, fl, step_ms) -> 
         "kernels": per_kernel,
         "tensor_pipe_pct_ncu": tensor_pct or None,
         "fp32_peak_measured": fp,
+        # the SIMT key pass computes in fp32 on the CUDA cores: its compute roofline is the FFMA2 peak
+        "compute_frac_fp32_simt": (round(fl[flop_key] / (t[dom] * 1e-3) / 1e12 / fp["ffma2_tflops"], 4)
+                                   if fp and fp.get("ffma2_tflops", 0) > 0 else None),
         "step_frac_hbm": round(sum(by.values()) / (step_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
     }
 

@@ -383,3 +383,50 @@ def test_tp_microbench_dense_equals_eaas(es, oracle, L):
         assert rel(x.cpu().numpy(), ref) < 1e-4, method
     dm, em = api.tp_madds(L)
     assert dm == {2: 615, 4: 13075}[L] and dm / em > 5
+
+
+# ------------------------------------------------------------------ edge cases: empty inputs, maximum sizes
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_empty_system_every_entry_point(es, dtype):
+    """N = 0 through every public call (neighbours, transpose, projections,
+    forward, backward with forces, layer): empty outputs, no launch errors."""
+    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention
+    L, C, H = 2, 128, 8
+    pos = torch.zeros((0, 3), dtype=torch.float64, device="cuda")
+    idx = es.build_neighbors(pos, 64, 6.0)
+    rev_ptr, rev_pair = idx.transpose()
+    assert rev_ptr.numel() == 1
+    h = torch.zeros((0, 9, C), dtype=dtype, device="cuda")
+    W = torch.randn((L + 1, C, 5 * C), device="cuda").to(dtype)
+    q, k, v = es.project_qk(h, W, L)
+    cfg = AttentionConfig(heads=H, L=L)
+    out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
+    dq, dk, dv, dpos = es.stream_aggregate_backward(out, SavedAttention(q, k, v, pos, idx, out, lse, cfg),
+                                                    pos_grad=True)
+    dh, dW = es.project_qk_backward(h, W, L, dq, dk, dv)
+    torch.cuda.synchronize()
+    assert out.shape == (0, 9, C) and dpos.shape == (0, 3) and torch.count_nonzero(dW) == 0
+
+
+def test_maximum_neighbour_slots(es, oracle):
+    """K = 128 (the builder's maximum) on a dense FCC block with r_cut = 8.5 A
+    (~120 neighbours per atom): neighbour lists bit-exact, attention parity
+    (fp32), and K > 128 is ES_UNSUPPORTED."""
+    from paper_2601_16622_b200._lib import EsUnsupported
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex
+    pos = S.gen_fcc_system(500, 3.8, 3)
+    nbr, _, cnt = po.build_neighbors(pos, 128, 8.5)
+    assert cnt.max() > 100
+    idx = es.build_neighbors(dev(pos), 128, 8.5)
+    torch.cuda.synchronize()
+    assert np.array_equal(idx.table.cpu().numpy(), nbr)
+    L, C, H = 2, 64, 8
+    q, k, v = po.project(S.random_features(500, L, C, 3), S.random_weights(L, C, 3), L)
+    P = po.AttnProblem(L=L, H=H, r_cut=8.5, value_mode=po.VALUE_DENSE)
+    ro, _ = po.attn_fwd(P, q, k, v, pos, nbr)
+    out, _ = es.stream_aggregate(dev(q, torch.float32), dev(k, torch.float32), dev(v, torch.float32), dev(pos),
+                                 NeighborIndex(dev(nbr), None, None, 8.5), AttentionConfig(heads=H, L=L, r_cut=8.5))
+    torch.cuda.synchronize()
+    assert rel(d64(out), ro) < 1e-5
+    with pytest.raises(EsUnsupported):
+        es.build_neighbors(dev(pos), 129, 8.5)
