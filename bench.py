@@ -161,6 +161,18 @@ class ClockSampler:
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
 
+    def wait_live(self, timeout: float = 3.0):
+        """Block until nvidia-smi has written its first sample (its start-up takes longer than a short
+        timed region), so the samples cover the timed steps."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    return
+            except OSError:
+                pass
+            time.sleep(0.02)
+
     def __enter__(self):
         os.makedirs(os.path.dirname(self.path), exist_ok=True)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -376,6 +388,10 @@ def correctness_gate(wl: Workload) -> dict:
 def time_steps(wl: Workload, steps: int, warmup: int, world: int, sample_clocks: int | None = None):
     import torch
     import torch.distributed as dist
+    clk = ClockSampler(sample_clocks) if sample_clocks is not None else None
+    if clk:  # live before the warm-up, so it samples through the timed steps
+        clk.__enter__()
+        clk.wait_live()
     for _ in range(warmup):
         wl.step(*wl.inputs)
     torch.cuda.synchronize()
@@ -384,9 +400,6 @@ def time_steps(wl: Workload, steps: int, warmup: int, world: int, sample_clocks:
     torch.cuda.synchronize()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clk = ClockSampler(sample_clocks) if sample_clocks is not None else None
-    if clk:
-        clk.__enter__()
     e0.record(st)
     for _ in range(steps):
         wl.step(*wl.inputs)
