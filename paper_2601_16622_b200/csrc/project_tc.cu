@@ -84,6 +84,10 @@ __device__ __forceinline__ void store_row32(bf16* dst, const uint32_t (&r)[32]) 
 // double-buffered TMEM accumulator, so the epilogue of chunk c (TMEM ->
 // bf16 rows, warps 0-3) overlaps the MMA of chunk c+1.  Warp 4 (one lane)
 // issues TMA + MMA.
+#ifndef ES_PF_NBUF
+#define ES_PF_NBUF 1
+#endif
+constexpr int NBUF = ES_PF_NBUF;  // B stages = TMEM accumulators; 1: ~75 KB smem, 128 TMEM columns -> 3 CTAs per SM
 __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant__ CUtensorMap mh,
                                                           const __grid_constant__ CUtensorMap mw, TcP p,
                                                           bf16* __restrict__ q, bf16* __restrict__ k,
@@ -91,9 +95,9 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
-  uint8_t* Bs = smem + 32768;         // [2 stages][2 kb][2 nb][64 k-rows][64] bf16, 32 KB per stage
-  uint8_t* Stg = smem + 32768 + 65536;  // [4 warps][32 rows][80 B] epilogue staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 32768 + 65536 + 4 * 32 * 80);
+  uint8_t* Bs = smem + 32768;         // [NBUF stages][2 kb][2 nb][64 k-rows][64] bf16, 32 KB per stage
+  uint8_t* Stg = smem + 32768 + NBUF * 32768;  // [4 warps][32 rows][80 B] epilogue staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Stg + 4 * 32 * 80);
   uint64_t* a_full = bars + 0;
   uint64_t* b_full = bars + 1;        // [2]
   uint64_t* b_empty = bars + 3;       // [2] MMA done reading the stage
@@ -101,7 +105,8 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
   uint64_t* acc_free = bars + 7;      // [2] epilogue read the accumulator (128)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 9);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 128, mm = blockIdx.y;
+  // grid (M, tiles): the M rows of one atom tile run side by side -> their writes land on neighbouring DRAM rows
+  const int n0 = blockIdx.y * 128, mm = blockIdx.x;
   const int l = degree_of_row(mm);
   constexpr int NCH = 5;
   if (threadIdx.x == 0) {
@@ -116,7 +121,7 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
     }
     umma::fence_barrier_init();
   }
-  if (warp == 0) umma::tmem_alloc(tslot, 256);
+  if (warp == 0) umma::tmem_alloc(tslot, 128 * NBUF);
   umma::tc_fence_before();
   __syncthreads();
   umma::tc_fence_after();
@@ -124,25 +129,24 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
   if (warp == 4) {
     if (lane == 0) {
     auto load_b = [&](int c) {
-      uint8_t* B = Bs + (c & 1) * 32768;
-      umma::mbar_arrive_expect_tx(&b_full[c & 1], 32768);
+      uint8_t* B = Bs + (c % NBUF) * 32768;
+      umma::mbar_arrive_expect_tx(&b_full[c % NBUF], 32768);
 #pragma unroll
       for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
         for (int nb = 0; nb < 2; ++nb)
-          umma::tma_load_2d(B + (kb * 2 + nb) * 8192, &mw, &b_full[c & 1], c * 128 + 64 * nb, l * p.C + 64 * kb);
+          umma::tma_load_2d(B + (kb * 2 + nb) * 8192, &mw, &b_full[c % NBUF], c * 128 + 64 * nb, l * p.C + 64 * kb);
     };
     umma::mbar_arrive_expect_tx(a_full, 32768);
     umma::tma_load_3d(As, &mh, a_full, 0, mm, n0);
     umma::tma_load_3d(As + 16384, &mh, a_full, 64, mm, n0);
-    load_b(0);
-    load_b(1);
+    for (int c = 0; c < NBUF; ++c) load_b(c);
     umma::mbar_wait(a_full, 0);
     constexpr uint32_t idesc = umma::idesc_bf16(128, 128, 0, 1);
     for (int c = 0; c < NCH; ++c) {
-      const int b = c & 1;
-      umma::mbar_wait(&b_full[b], (c >> 1) & 1);
-      if (c >= 2) umma::mbar_wait(&acc_free[b], ((c >> 1) - 1) & 1);
+      const int b = c % NBUF;
+      umma::mbar_wait(&b_full[b], (c / NBUF) & 1);
+      if (c >= NBUF) umma::mbar_wait(&acc_free[b], ((c / NBUF) - 1) & 1);
       umma::tc_fence_after();
       const uint8_t* B = Bs + b * 32768;
 #pragma unroll
@@ -154,16 +158,16 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
       }
       umma::mma_commit(&acc_full[b]);
       umma::mma_commit(&b_empty[b]);
-      if (c + 2 < NCH) {
-        umma::mbar_wait(&b_empty[b], (c >> 1) & 1);
-        load_b(c + 2);
+      if (c + NBUF < NCH) {
+        umma::mbar_wait(&b_empty[b], (c / NBUF) & 1);
+        load_b(c + NBUF);
       }
     }
     }
   } else {
   for (int c = 0; c < NCH; ++c) {
-    const int b = c & 1, o0 = c * 128;
-    umma::mbar_wait(&acc_full[b], (c >> 1) & 1);
+    const int b = c % NBUF, o0 = c * 128;
+    umma::mbar_wait(&acc_full[b], (c / NBUF) & 1);
     umma::tc_fence_after();
     // rows -> per-warp staging (32 rows x 32 columns, 80-byte padded rows: no
     // bank conflicts) -> coalesced stores: 4 lanes write one row's 64 bytes,
@@ -204,12 +208,15 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
   }
   umma::tc_fence_before();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(taddr, 256);
+  if (warp == 0) umma::tmem_dealloc(taddr, 128 * NBUF);
 }
 
 // ------------------------------------------------------------------ dh
 // grid (ceil(N/128), M): tile = 128 atoms at (l,m) x 128 channels; K = 5C in 64-wide blocks.
-constexpr int kDhStages = 4;
+#ifndef ES_DH_STAGES
+#define ES_DH_STAGES 2
+#endif
+constexpr int kDhStages = ES_DH_STAGES;  // 2 x 32 KB: three CTAs per SM (short CTAs: residency beats depth)
 __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__ CUtensorMap mdq,
                                                          const __grid_constant__ CUtensorMap mdk,
                                                          const __grid_constant__ CUtensorMap mdv,
@@ -222,7 +229,8 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
   uint64_t* done = empty + kDhStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * 128, mm = blockIdx.y;
+  // grid (M, tiles): the M rows of one atom tile run side by side -> their writes land on neighbouring DRAM rows
+  const int n0 = blockIdx.y * 128, mm = blockIdx.x;
   const int l = degree_of_row(mm);
   const int nkb = (5 * p.C) / 64, kq = (2 * p.C) / 64;
   if (threadIdx.x == 0) {
@@ -301,7 +309,13 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
 // ------------------------------------------------------------------ dW
 // grid (splits, 5): split-K over atoms for one degree l (R = (2l+1)*nb rows
 // per stage); D = [c 128] x [o 128]; fp32 reduction into dW.
-constexpr int kDwStages = 2;
+#ifndef ES_DW_STAGES
+#define ES_DW_STAGES 2
+#endif
+constexpr int kDwStages = ES_DW_STAGES;
+#ifndef ES_DW_SPLITS
+#define ES_DW_SPLITS 60  // atom splits per degree (x 5 column blocks); 118 measured slower (more fp32 atomics)
+#endif
 __global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__ CUtensorMap mh,
                                                          const __grid_constant__ CUtensorMap mdq,
                                                          const __grid_constant__ CUtensorMap mdk,
@@ -405,14 +419,14 @@ es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, vo
   CUtensorMap mh, mw;
   if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64))
     return fail(ES_CUDA_ERROR, "proj_fwd_tc: tensor map encode failed");
-  const size_t smem = 32768 + 65536 + 4 * 32 * 80 + 1024 + 1024;
+  const size_t smem = 32768 + NBUF * 32768 + 4 * 32 * 80 + 1024 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(proj_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   TcP p{a.N, M, a.C, a.L};
-  dim3 grid((a.N + 127) / 128, M);
+  dim3 grid(M, (a.N + 127) / 128);
   proj_fwd_tc_kernel<<<grid, 160, smem, st>>>(mh, mw, p, (bf16*)q, (bf16*)k, (bf16*)v);
   return cuda_status(cudaGetLastError(), "proj_fwd_tc_kernel");
 }
@@ -432,7 +446,7 @@ es_status proj_bwd_tc_launch(const ProjArgs& a, const void* h, const void* W, co
       cudaFuncSetAttribute(proj_dh_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    dim3 grid((a.N + 127) / 128, M);
+    dim3 grid(M, (a.N + 127) / 128);
     proj_dh_tc_kernel<<<grid, 128, smem, st>>>(mdq, mdk, mdv, mwk, p, (bf16*)dh);
     es_status s = cuda_status(cudaGetLastError(), "proj_dh_tc_kernel");
     if (s != ES_OK) return s;
@@ -452,7 +466,7 @@ es_status proj_bwd_tc_launch(const ProjArgs& a, const void* h, const void* W, co
         !map3(&gk, dk, 2 * a.C, M, a.N, 64, 2 * l + 1, nb) || !map3(&gv, dv, a.C, M, a.N, 64, 2 * l + 1, nb))
       return fail(ES_CUDA_ERROR, "proj_dw_tc: tensor map encode failed");
     const size_t smem = (size_t)kDwStages * 4 * R * 128 + 1024 + 1024;
-    int splits = 60;
+    int splits = ES_DW_SPLITS;
     int per = (a.N + splits - 1) / splits;
     per = ((per + nb - 1) / nb) * nb;
     splits = (a.N + per - 1) / per;
