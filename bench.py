@@ -463,9 +463,15 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
     gate = None
     if args.config == 2 and not args.no_gate:
         gate = correctness_gate(wl)
-        if not gate["passed"]:
-            print(json.dumps({"metric": METRIC, "error": "correctness gate failed; timing aborted", "gate": gate}),
-                  flush=True)
+        ok = torch.tensor([1 if gate["passed"] else 0], device=dev)
+        if world > 1:  # every rank checks its own batch; all abort together (no rank left in a collective)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "error": "correctness gate failed; timing aborted",
+                                  "gate": gate}), flush=True)
+            if world > 1:
+                dist.destroy_process_group()
             sys.exit(3)
 
     idx, _, _ = wl.step(*wl.inputs)
