@@ -586,7 +586,9 @@ def gpu_arm(args, rank: int, world: int, local_rank: int):
             "precision": f"{args.dtype} storage, fp32 accumulation",
             "l2": "inputs exceed L2 (h, q, k, v, dout >= 0.47 GB each at bf16, config 2)",
             "parallelism": (f"rows{world} (query-row slabs, NCCL all-gather K/V + reduce-scatter dk/dv)"
-                            if wl.row_sharded else f"dp{world} (molecule batches, no collective)"),
+                            if wl.row_sharded else
+                            f"dp{world} (molecule batches, no collective)" if args.config in (2, 4) else
+                            "one system on one GPU"),
             "latency_ms": round(ms, 4), "flops_per_step_per_gpu": fl,
         },
         "clocks": clocks,
