@@ -60,6 +60,31 @@ def run(name, pos, seg, reps, dense_ok):
     for r in rows:
         r.update({"system": name, "N": N, "pairs": E, "L": L, "C": C, "H": H, "pass": "forward"})
         print(json.dumps(r), flush=True)
+    # forward + backward (the baselines by autograd through their materialised graphs)
+    from paper_2601_16622_b200.api import SavedAttention
+    go = torch.randn(N, 9, C, device="cuda", generator=g).bfloat16()
+
+    def fused_fb():
+        out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
+        es.stream_aggregate_backward(go, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
+
+    bw = [("fused_eaas (this library, bf16)", fused_fb)]
+    if N <= 20000:  # the per-edge graph of the whole system is kept for the backward
+        bw.append(("edge_materialising_dense_cg (torch autograd)", lambda: baselines.baseline_backward(
+            lambda a, b_, c: baselines.edge_materialising_attention(a, b_, c, pos, idx.table, H, L, chunk=8192)[0],
+            q, k, v, go)))
+    if dense_ok:
+        bw.append(("masked_dense_sdpa (torch autograd, plain values)", lambda: baselines.baseline_backward(
+            lambda a, b_, c: baselines.masked_dense_attention(a, b_, c, idx.table, H), q, k, v, go)))
+    for mname, fn in bw:
+        try:
+            ms, gb = timed(fn, reps)
+            r = {"method": mname, "ms": round(ms, 4), "peak_gb": round(gb, 3)}
+        except torch.cuda.OutOfMemoryError:
+            torch.cuda.empty_cache()
+            r = {"method": mname, "error": "OOM"}
+        r.update({"system": name, "N": N, "pairs": E, "L": L, "C": C, "H": H, "pass": "forward+backward"})
+        print(json.dumps(r), flush=True)
 
 
 def main():

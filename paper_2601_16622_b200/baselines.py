@@ -74,7 +74,7 @@ def edge_materialising_attention(q, k, v, pos, nbr, heads: int, L: int = 2, r_cu
     ch = C // H
     tau = 1.0 / math.sqrt(M * dqh)
     G = coupling_tensor(L, q.device) if value == "eaas" else None
-    out = torch.empty_like(v)
+    outs = []  # chunk outputs concatenated (autograd-friendly: the backward baseline differentiates this)
     peak = 0
     for a in range(0, N, chunk):
         rows = torch.arange(a, min(N, a + chunk), device=q.device)
@@ -95,9 +95,18 @@ def edge_materialising_attention(q, k, v, pos, nbr, heads: int, L: int = 2, r_cu
             x = vj
         x = x * phi[..., None, None]
         w = p.repeat_interleave(ch, dim=2)                              # [n, K, C] head weights per channel
-        out[rows] = torch.einsum("nkc,nkoc->noc", w, x).to(v.dtype)
+        outs.append(torch.einsum("nkc,nkoc->noc", w, x).to(v.dtype))
         peak = max(peak, sum(t.numel() * t.element_size() for t in (kj, s, vj, x)))
-    return out, peak
+    return torch.cat(outs), peak
+
+
+def baseline_backward(fn, q, k, v, grad_out):
+    """The backward of a baseline by autograd through its materialised graph
+    (every per-edge tensor of the forward is kept for it): (dq, dk, dv)."""
+    qq, kk, vv = (t.detach().requires_grad_(True) for t in (q, k, v))
+    out = fn(qq, kk, vv)
+    out.backward(grad_out)
+    return qq.grad, kk.grad, vv.grad
 
 
 def masked_dense_attention(q, k, v, nbr, heads: int):
