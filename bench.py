@@ -127,7 +127,7 @@ def kernel_times(fn) -> dict:
 def short_name(n: str) -> str:
     if "attn_dqk_tc_kernel" in n:
         return "attn_dk_tc" if "<true>" in n else "attn_dq_tc"
-    for key in ("attn_fwd_tc", "attn_bwd_q_tc", "attn_bwd_k_tc", "attn_bwd_kv", "attn_dq_tc", "attn_delta",
+    for key in ("attn_fwd_tc", "attn_kv_tc", "attn_bwd_q_tc", "attn_bwd_k_tc", "attn_bwd_kv", "attn_dq_tc", "attn_delta",
                 "attn_fwd_kernel", "attn_bwd_q_kernel", "proj_fwd_tc", "proj_dh_tc", "proj_dw_tc", "proj_fwd_kernel",
                 "proj_bwd", "nbr_segment", "nbr_grid", "tr_sort", "tr_fill", "tr_count", "tc_rowlist", "tc_tiles",
                 "tc_mask", "tc_count", "tc_fill", "tc_rowtile", "grid_", "DeviceScan", "DeviceRadix", "nccl"):

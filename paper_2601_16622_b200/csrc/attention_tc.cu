@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       constexpr int PF = 4;
       auto prefetch = [&](int h, int c) {
         const int k0 = clist[c_begin + c] * KC;
-        for (int mm = 0; mm < MM; ++mm) umma::tma_prefetch_3d(&mk, DH * h, mm, k0);
+        umma::tma_prefetch_3d(&mk, DH * h, k0, 0);
         umma::tma_prefetch_3d(&mv, HD * h, 0, k0);
       };
       for (int c = 0; c < nch && c < PF; ++c) prefetch(0, c);
@@ -264,8 +264,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
           }
           uint8_t* kb = sm + SM_K + st * KBYTES;
           umma::mbar_arrive_expect_tx(&full_kv[st], KBYTES + VBYTES + pbytes);
-          for (int mm = 0; mm < MM; ++mm)
-            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
+          umma::tma_load_3d(kb, &mk, &full_kv[st], DH * h, k0, 0);  // 9 (l,m) blocks [16 keys][32 ch]
           umma::tma_load_3d(sm + SM_VST + st * VBYTES, &mv, &full_kv[st], HD * h, 0, k0);
         TC_TRACE(true, g_trace[0][g]);
           if (pbytes) umma::bulk_load(sm + SM_POS + st * PBYTES, pos + 3 * (size_t)k0, pbytes, &full_kv[st]);
@@ -282,12 +281,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::mbar_wait(&vg_full[b], (g >> 1) & 1);
         if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);  // O of the previous head read out
         umma::tc_fence_after();
-        const uint32_t wa = umma::smem_u32(sm + SM_WT + b * WBYTES), va = umma::smem_u32(sm + SM_VG + b * GBYTES);
-        if (!(a.dbg & 4))
+        // descriptors advance by (byte offset >> 4) from one base: the single issuing thread
+        // would otherwise spend ~100 cycles of dependent integer ops per MMA building them
+        const uint64_t wd = umma::sdesc(umma::smem_u32(sm + SM_WT + b * WBYTES), 128, (KV / 8) * 128, 0);
+        const uint64_t vd = umma::sdesc(umma::smem_u32(sm + SM_VG + b * GBYTES), 128, (KV / 8) * 128, 0);
+        if (!(a.dbg & 4)) {
+          umma::mma_f16(t_out, wd, vd, idesc_v, c > 0 ? 1u : 0u);
 #pragma unroll
-          for (int s = 0; s < MM; ++s)
-            umma::mma_f16(t_out, umma::sdesc(wa + s * 256, 128, (KV / 8) * 128, 0),
-                          umma::sdesc(va + s * 256, 128, (KV / 8) * 128, 0), idesc_v, (c > 0 || s > 0) ? 1u : 0u);
+          for (int s = 1; s < MM; ++s) umma::mma_f16(t_out, wd + (uint64_t)(16 * s), vd + (uint64_t)(16 * s), idesc_v, 1u);
+        }
         umma::mma_commit(&wv_free[b]);
         TC_TRACE(true, g_trace[6][g]);
       };
@@ -296,15 +298,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
         umma::mbar_wait(&full_kv[st], (g / NSTAGE) & 1);
         if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
         umma::tc_fence_after();
-        const uint32_t ka = umma::smem_u32(sm + SM_K + st * KBYTES);
-        const uint32_t tq = t_q0 + 144 * (h & 1);
-        if (!(a.dbg & 8))
+        const uint64_t kd = umma::sdesc(umma::smem_u32(sm + SM_K + st * KBYTES), 16, 512, 4);
+        const uint32_t tq = t_q0 + 144 * (h & 1), ts = t_s0 + 32 * b;
+        if (!(a.dbg & 8)) {
 #pragma unroll
-          for (int s = 0; s < 2 * MM; ++s) {
-            const int mm = s >> 1, kk = s & 1;
-            umma::mma_f16_ts(t_s0 + 32 * b, tq + 8 * s, umma::sdesc(ka + mm * KC * DH * 2 + kk * 32, 16, 512, 4),
-                             idesc_s, s > 0 ? 1u : 0u);
-          }
+          for (int s = 0; s < 2 * MM; ++s)
+            umma::mma_f16_ts(ts, tq + 8 * s, kd + (uint64_t)(((s >> 1) * KC * DH * 2 + (s & 1) * 32) >> 4), idesc_s,
+                             s > 0 ? 1u : 0u);
+        }
         umma::mma_commit(&s_full[b]);
         TC_TRACE(true, g_trace[1][g]);
         umma::mma_commit(&empty_kv[st]);
@@ -916,6 +917,22 @@ bool map3(CUtensorMap* m, const void* base, int inner, int mid, int outer, int b
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The same [outer][mid][inner] bf16 tensor with the mid and outer dimensions swapped, so one
+// box {b_inner, b_outer rows, b_mid} lands as b_mid consecutive [b_outer][b_inner] blocks --
+// e.g. a 16-atom chunk of all nine (l,m) rows of one head in a single TMA instead of nine.
+bool map3t(CUtensorMap* m, const void* base, int inner, int mid, int outer, int b_inner, int b_outer, int b_mid,
+           CUtensorMapSwizzle sw) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return false;
+  cuuint64_t gd[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)mid};
+  cuuint64_t gs[2] = {(cuuint64_t)inner * mid * 2, (cuuint64_t)inner * 2};
+  cuuint32_t bd[3] = {(cuuint32_t)b_inner, (cuuint32_t)b_outer, (cuuint32_t)b_mid};
+  cuuint32_t es_[3] = {1, 1, 1};
+  return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gd, gs, bd, es_,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 es_status upload_tc_tables() {
   static bool done[64] = {false};
   int dev = 0;
@@ -1107,7 +1124,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
   const uint32_t* rowlist = lists.rowlist;
 
   CUtensorMap mk, mv;
-  if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B) ||
+  if (!map3t(&mk, k, 256, MM, a.Nk, DH, KC, MM, CU_TENSOR_MAP_SWIZZLE_64B) ||
       !map3(&mv, v, 128, MM, a.Nk, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE))
     return fail(ES_CUDA_ERROR, "attn_fwd_tc: tensor map encode failed");
   TcArgs ta;
@@ -1217,15 +1234,13 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
             const int cp = c + DQ_NSTAGE + PF;
             const int hp = h + cp / (nch > 0 ? nch : 1), ccp = cp % (nch > 0 ? nch : 1);
             if (hp < 8)
-              for (int mm = 0; mm < MM; ++mm)
-                umma::tma_prefetch_3d(&mk, DH * hp, mm, clist[c_begin + ccp] * KC);
+              umma::tma_prefetch_3d(&mk, DH * hp, clist[c_begin + ccp] * KC, 0);
           }
           if (g >= DQ_NSTAGE) umma::mbar_wait(&empty_kv[st], ((g / DQ_NSTAGE) - 1) & 1);
           const int k0 = clist[c_begin + c] * KC;
           uint8_t* kb = sm + DQ_SM_K + st * KBYTES;
           umma::mbar_arrive_expect_tx(&full_kv[st], KBYTES);
-          for (int mm = 0; mm < MM; ++mm)
-            umma::tma_load_3d(kb + mm * KC * DH * 2, &mk, &full_kv[st], DH * h, mm, k0);
+          umma::tma_load_3d(kb, &mk, &full_kv[st], DH * h, k0, 0);
         }
     }
   } else if (warp == 1) {
@@ -1428,7 +1443,7 @@ es_status attn_dq_tc_launch(const AttnArgs& a, const void* k, const int32_t* nbr
     if (s != ES_OK) return s;
   }
   CUtensorMap mk;
-  if (!map3(&mk, k, 256, MM, a.Nk, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B))
+  if (!map3t(&mk, k, 256, MM, a.Nk, DH, KC, MM, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(ES_CUDA_ERROR, "attn_dq_tc: tensor map encode failed");
   const int smem = DQ_SM_TOTAL + 1024;
   static bool attr = false;
@@ -1488,6 +1503,9 @@ bool attn_dk_tc_applicable(const AttnArgs& a) {
   return e && e[0] == '1' && attn_dq_tc_applicable(a);
 }
 
+// the tile buffer also carries the key-side lists (tensor-core key pass or dk)
+bool tc_key_lists(const AttnArgs& a) { return attn_dk_tc_applicable(a) || attn_kv_tc_applicable(a); }
+
 size_t attn_dk_tc_workspace(const AttnArgs& a) { return a.N > 0 ? tc_scratch(key_side(a)).total : 0; }
 
 es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr, const int32_t* rev_ptr,
@@ -1505,7 +1523,7 @@ es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr
     if (s != ES_OK) return s;
   }
   CUtensorMap mq;
-  if (!map3(&mq, q, 256, MM, a.N, DH, 1, KC, CU_TENSOR_MAP_SWIZZLE_64B))
+  if (!map3t(&mq, q, 256, MM, a.N, DH, KC, MM, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(ES_CUDA_ERROR, "attn_dk_tc: tensor map encode failed");
   const int smem = DQ_SM_TOTAL + 1024;
   static bool attr = false;
@@ -1539,7 +1557,7 @@ void attn_tc_tiles_layout(const AttnArgs& a, es_attn_tiles_layout* out) {
     o->rank_of = query ? base + ((const char*)p.rank_of - z) : -1;
   };
   side(a, 0, &out->query, true);
-  if (attn_dk_tc_applicable(a)) side(key_side(a), (int64_t)tiles_query_bytes(a), &out->key, false);
+  if (tc_key_lists(a)) side(key_side(a), (int64_t)tiles_query_bytes(a), &out->key, false);
 }
 
 const int* attn_tc_rank_of(const AttnArgs& a, const void* tiles) {
@@ -1552,7 +1570,7 @@ bool attn_tc_tiles_used(const AttnArgs& a) { return attn_dq_tc_applicable(a) || 
 
 size_t attn_tc_tiles_bytes(const AttnArgs& a) {
   if (a.N <= 0) return 0;
-  return tiles_query_bytes(a) + (attn_dk_tc_applicable(a) ? attn_dk_tc_workspace(a) : 0);
+  return tiles_query_bytes(a) + (tc_key_lists(a) ? attn_dk_tc_workspace(a) : 0);
 }
 
 // The tile structures of one neighbour index, built once and reused by every
@@ -1563,13 +1581,603 @@ es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32
   if (a.N == 0) return ES_OK;
   const TcScratch t = tc_scratch(a);
   if (!tiles || bytes < attn_tc_tiles_bytes(a)) return fail(ES_INVALID_ARGUMENT, "attn_tiles: buffer too small");
-  const bool keys = attn_dk_tc_applicable(a);
+  const bool keys = tc_key_lists(a);
   if (keys && (!rev_ptr || !rev_pair))
     return fail(ES_INVALID_ARGUMENT, "attn_tiles: the tensor-core backward needs rev_ptr / rev_pair (key-side lists)");
   TcLists lists;
   es_status s = tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st, seg, nseg);
   if (s != ES_OK || !keys) return s;
   return tc_build_key_lists(a, nbr, rev_ptr, rev_pair, (char*)tiles + tiles_query_bytes(a), &lists, st, seg, nseg);
+}
+
+
+// ---------------------------------------------------------------- key pass on the tensor cores
+// dv_j and the per-pair dscores of the backward (stream_aggregate_backward,
+// SPEC.md:293-301) over the key-side tiles (128 key atoms; 16-query chunks of
+// the transposed relation), per head h and chunk three tcgen05 MMA groups:
+//   S^T[j, i]     = K_h . Q_chunk^T                 M=128 keys, N=16,  K=288  (A = K_h in TMEM)
+//   D[j, (f,i)]   = V_h . dOg^T                     M=128,      N=144, K=144  (A = V_h, TMA SW32;
+//                                                                             B = dOg read MN-major)
+//   dV[j,(i',c)] += Wt'[j,(f,i)] . dOg[(f,i),(i',c)] M=128,     N=144, K=144
+// with the query-side source coupling dOg[(f,i),(i',c)] = sum_o G_f[o,i'] dO_i[o][c]
+// (the transpose of the forward's per-key Vg) and per valid pair, on the key rows,
+//   P = exp(tau s + b(r) - lse_i),  dP = phi sum_f Y^f D[j,(f,i)],  dS = P (dP - delta_i),
+//   Wt'[j,(f,i)] = P phi Y^f       (zero for non-neighbours).
+// This is the SIMT key pass's math (attn_bwd_kv_kernel: dv_j += P y, dP = y . v_j with
+// y = phi (EAAS map)^T dO_i) with the map written as sum_f Y^f G_f (Prop. 1).  dk and dq
+// follow from the dscores on the tensor cores (attn_dqk_tc_kernel).  The pair geometry
+// (phi Y^f, b(r)) is head-independent: attn_pair_geom_kernel writes it once per pair in
+// key-side order, and the eight head passes read it back (L2-resident).
+// The (f, i) index of D, Wt' and dOg is quarter-major, k = 36 (i / 4) + 4 f + i % 4, so a
+// row thread's 4 queries x 9 f of one quarter are 36 consecutive TMEM columns.
+namespace {
+constexpr int KV_NA = 2;                               // Q / dO stages (freed early: S MMA + coupling)
+constexpr int KV_NB = 4;                               // position / lse / delta stages (freed by the rows)
+constexpr int KV_QB = MM * KC * DH * 2;                // 9216: Q chunk, 9 SW64 boxes [16 q][32 ch]
+constexpr int KV_OB = KC * MM * HD * 2;                // 4608: dO chunk [16 q][9][16 c]
+constexpr int KV_ASTAGE = 14 * 1024;                   // Q | dO
+constexpr int KV_B_L = KC * 24;                        // [16][3] f64 positions | [16][8] lse | [16][8] delta
+constexpr int KV_B_D = KV_B_L + KC * 32;
+constexpr int KV_BSTAGE = 1536;
+static_assert(KV_QB + KV_OB <= KV_ASTAGE && KV_B_D + KC * 32 <= KV_BSTAGE, "kv stage overflow");
+constexpr int KV_VHB = TQ * MM * HD * 2;               // 36864: V_h as 9 SW32 boxes [128 keys][16 c]
+constexpr int KV_SM_B = KV_NA * KV_ASTAGE;
+constexpr int KV_SM_WT = KV_SM_B + KV_NB * KV_BSTAGE;  // Wt' (single buffer: rows write it after dV(g-1))
+constexpr int KV_SM_DOG = KV_SM_WT + WBYTES;           // 2 x GBYTES
+constexpr int KV_SM_VH = KV_SM_DOG + 2 * GBYTES;       // 2 x KV_VHB: V_(h+1) lands while head h runs
+constexpr int KV_SM_BAR = KV_SM_VH + 2 * KV_VHB;
+constexpr int KV_SM_TOTAL = KV_SM_BAR + 512;
+static_assert(KV_SM_TOTAL + 1024 <= 232448, "key-pass kernel exceeds 227 KB of shared memory");
+static_assert(KV_SM_WT % 1024 == 0 && KV_SM_DOG % 1024 == 0 && KV_SM_VH % 1024 == 0, "kv smem alignment");
+
+__device__ __forceinline__ int kv_k(int f, int i) { return (i >> 2) * 36 + 4 * f + (i & 3); }
+
+#ifdef ES_TC_TRACE
+__device__ long long g_ktrace[12][256];  // per-chunk event clocks of CTA 1 (ES_KV_DBG=64)
+#define KV_TRACE(cond, ev, idx) \
+  do {                          \
+    if (KTRACE && (cond) && (idx) < 256) g_ktrace[ev][idx] = clock64(); \
+  } while (0)
+#else
+#define KV_TRACE(cond, ev, idx) \
+  do {                          \
+  } while (0)
+#endif
+
+// Per-pair record of the key pass, key-side order (entry e of rev_pair): phi Y^f (9 x fp16),
+// b(r) (f32), the pair index i K + slot.  32 bytes.
+struct __align__(16) PairGeom {
+  __half2 y01, y23, y45, y67;
+  __half y8, pad;
+  float bias;
+  int pr;
+  int pad2;
+};
+static_assert(sizeof(PairGeom) == 32, "pair record");
+
+__global__ void __launch_bounds__(256) attn_pair_geom_kernel(TcArgs a, const double* __restrict__ pos,
+                                                             const int* __restrict__ rev_ptr,
+                                                             const int* __restrict__ rev_pair,
+                                                             PairGeom* __restrict__ geom) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.Nk) return;
+  const double kx = pos[3 * (size_t)j], ky = pos[3 * (size_t)j + 1], kz = pos[3 * (size_t)j + 2];
+  const int e1 = rev_ptr[j + 1];
+  for (int e = rev_ptr[j]; e < e1; ++e) {
+    const int pr = rev_pair[e];
+    const size_t i = (size_t)(pr / a.K);
+    // r_ij = pos_j - pos_i, as the forward (key minus query)
+    double dx = kx - pos[3 * i], dy = ky - pos[3 * i + 1], dz = kz - pos[3 * i + 2];
+    if (a.periodic) {
+      dx -= a.bx * rint(dx / a.bx);
+      dy -= a.by * rint(dy / a.by);
+      dz -= a.bz * rint(dz / a.bz);
+    }
+    const float rx = (float)dx, ry = (float)dy, rz = (float)dz;
+    const float rn = sqrtf(rx * rx + ry * ry + rz * rz);
+    float phi = 1.f;
+    if (a.phi_mode == 0) phi = rn < a.r_cut ? 0.5f * (cospif(rn * a.inv_rcut) + 1.f) : 0.f;
+    float y[MM];
+    solid_l2(rx, ry, rz, y);
+    PairGeom g;
+    g.y01 = __floats2half2_rn(phi * y[0], phi * y[1]);
+    g.y23 = __floats2half2_rn(phi * y[2], phi * y[3]);
+    g.y45 = __floats2half2_rn(phi * y[4], phi * y[5]);
+    g.y67 = __floats2half2_rn(phi * y[6], phi * y[7]);
+    g.y8 = __float2half_rn(phi * y[8]);
+    g.pad = __float2half_rn(0.f);
+    g.bias = a.bias_mode ? fmaf(fmaf(a.b2, rn, a.b1), rn, a.b0) : 0.f;
+    g.pr = pr;
+    g.pad2 = 0;
+    geom[e] = g;
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) attn_kv_tc_kernel(
+    const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mo,
+    const __grid_constant__ CUtensorMap mvh, TcArgs a, const bf16* __restrict__ k, const double* __restrict__ pos,
+    const float* __restrict__ lse, const float* __restrict__ delta, const int* __restrict__ cptr,
+    const int* __restrict__ clist, const uint32_t* __restrict__ rowlist, const int* __restrict__ tstart,
+    const int* __restrict__ rev_ptr, const PairGeom* __restrict__ geom, float* __restrict__ dsbuf,
+    bf16* __restrict__ dv) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + KV_SM_BAR);
+  uint64_t* full_a = bars + 0;     // [4] Q + dO landed (tx)
+  uint64_t* empty_a = bars + 4;    // [4] S MMA + coupling threads done (129)
+  uint64_t* full_b = bars + 8;     // [4] positions / lse / delta landed (tx)
+  uint64_t* empty_b = bars + 12;   // [4] rows done (256)
+  uint64_t* s_full = bars + 16;    // [2] S^T committed
+  uint64_t* s_free = bars + 18;    // [2] rows read S^T (256)
+  uint64_t* d_full = bars + 20;    // D committed
+  uint64_t* d_free = bars + 21;    // rows read D (256)
+  uint64_t* dog_full = bars + 22;  // [2] coupling threads wrote dOg (128)
+  uint64_t* wv_free = bars + 24;   // [2] dV MMA committed (Wt', dOg buffer free)
+  uint64_t* wt_full = bars + 26;   // rows wrote Wt' (256)
+  uint64_t* acc_done = bars + 27;  // last dV MMA of the head committed
+  uint64_t* epi_done = bars + 28;  // rows read dV (256)
+  uint64_t* k_ready = bars + 29;   // K_h stored into TMEM (coupling warps, 128)
+  uint64_t* k_free = bars + 30;    // last S MMA of the head committed
+  uint64_t* vh_full = bars + 31;   // [2] V_h landed (tx)
+  uint64_t* vh_free = bars + 33;   // [2] last D MMA of the head committed (V_h buffer free)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 35);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int j0 = tstart[blockIdx.x], j1 = tstart[blockIdx.x + 1];
+  if (j0 >= j1) return;  // surplus (empty) tile
+  const int c_begin = cptr[blockIdx.x], nch = cptr[blockIdx.x + 1] - cptr[blockIdx.x];
+#ifdef ES_TC_TRACE
+  const bool KTRACE = (a.dbg & 64) && blockIdx.x == 1;
+#endif
+  const bool is_row = warp >= 2 && warp <= 9;
+  const int row = ((warp & 3) << 5) | lane;  // TMEM lane = key row of the tile
+  const int kj = j0 + row;
+  const bool kin = kj < j1;
+
+  if (tid == 0) {
+    umma::prefetch_tmap(&mq);
+    umma::prefetch_tmap(&mo);
+    umma::prefetch_tmap(&mvh);
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&s_full[b], 1);
+      umma::mbar_init(&s_free[b], 256);
+      umma::mbar_init(&dog_full[b], 128);
+      umma::mbar_init(&wv_free[b], 1);
+    }
+    for (int b = 0; b < KV_NA; ++b) {
+      umma::mbar_init(&full_a[b], 1);
+      umma::mbar_init(&empty_a[b], 1 + 128);
+    }
+    umma::mbar_init(&vh_full[0], 1);
+    umma::mbar_init(&vh_full[1], 1);
+    umma::mbar_init(&vh_free[0], 1);
+    umma::mbar_init(&vh_free[1], 1);
+    for (int b = 0; b < KV_NB; ++b) {
+      umma::mbar_init(&full_b[b], 1);
+      umma::mbar_init(&empty_b[b], 256);
+    }
+    umma::mbar_init(d_full, 1);
+    umma::mbar_init(d_free, 256);
+    umma::mbar_init(wt_full, 256);
+    umma::mbar_init(acc_done, 1);
+    umma::mbar_init(epi_done, 256);
+    umma::mbar_init(k_ready, 128);
+    umma::mbar_init(k_free, 1);
+    umma::fence_barrier_init();
+  }
+  if (warp == 0) umma::tmem_alloc(tslot, 512);
+  umma::tc_fence_before();
+  __syncthreads();
+  umma::tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t t_k = tmem, t_d = tmem + 144, t_dv = tmem + 288, t_s0 = tmem + 448;
+  const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+  // K_hh rows (l,m) in [m0, m0 + 3) of this thread's key -> TMEM (the S MMA's A operand)
+  const bf16* krow = k + (size_t)(kin ? kj : 0) * MM * 256;
+  auto load_k3 = [&](int hh, int m0) {
+    uint32_t rr[3][16];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint4* src = reinterpret_cast<const uint4*>(krow + (m0 + d) * 256 + DH * hh);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const uint4 u = kin ? __ldg(src + t) : make_uint4(0, 0, 0, 0);
+        rr[d][4 * t] = u.x; rr[d][4 * t + 1] = u.y; rr[d][4 * t + 2] = u.z; rr[d][4 * t + 3] = u.w;
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) umma::tmem_st16(t_k + lane_base + 16 * (m0 + d), rr[d]);
+  };
+  auto load_k = [&](int hh) {  // the coupling warps: all nine (l,m) rows
+    load_k3(hh, 0);
+    load_k3(hh, 3);
+    load_k3(hh, 6);
+    umma::tc_fence_before();
+    umma::mbar_arrive(k_ready);
+  };
+
+  if (nch == 0) {
+    // no key of the tile is anyone's neighbour: dv = 0, no dscores
+    if (is_row && kin) {
+      const int half = (warp - 2) >> 2;
+      for (int h = 0; h < 8; ++h)
+        for (int cc = half ? 5 : 0; cc < (half ? MM : 5); ++cc) {
+          uint4* dst = reinterpret_cast<uint4*>(dv + ((size_t)kj * MM + cc) * 128 + HD * h);
+          dst[0] = make_uint4(0, 0, 0, 0);
+          dst[1] = make_uint4(0, 0, 0, 0);
+        }
+    }
+  } else if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer: query chunks (Q + dO; positions, lse, delta) and V_h
+      constexpr int PF = 4;
+      auto prefetch = [&](int h, int c) {
+        const int i0 = clist[c_begin + c] * KC;
+        umma::tma_prefetch_3d(&mq, DH * h, i0, 0);
+        umma::tma_prefetch_3d(&mo, HD * h, 0, i0);
+      };
+      auto load_vh = [&](int h) {  // 9 i' blocks [128 keys][16 c] into buffer h & 1
+        umma::mbar_arrive_expect_tx(&vh_full[h & 1], KV_VHB);
+        umma::tma_load_3d(sm + KV_SM_VH + (h & 1) * KV_VHB, &mvh, &vh_full[h & 1], HD * h, j0, 0);
+      };
+      load_vh(0);
+      load_vh(1);
+      for (int c = 0; c < nch && c < PF; ++c) prefetch(0, c);
+      int g = 0;
+      for (int h = 0; h < 8; ++h) {
+        for (int c = 0; c < nch; ++c, ++g) {
+          {
+            const int cp = c + PF;
+            if (cp < nch) prefetch(h, cp);
+            else if (h + 1 < 8 && cp - nch < nch) prefetch(h + 1, cp - nch);
+          }
+          const int i0 = clist[c_begin + c] * KC;
+          const int nq = min(KC, a.N - i0);
+          {
+            const int st = g % KV_NA;
+            if (g >= KV_NA) umma::mbar_wait(&empty_a[st], ((g / KV_NA) - 1) & 1);
+            uint8_t* sa = sm + st * KV_ASTAGE;
+            umma::mbar_arrive_expect_tx(&full_a[st], KV_QB + KV_OB);
+            umma::tma_load_3d(sa, &mq, &full_a[st], DH * h, i0, 0);
+            umma::tma_load_3d(sa + KV_QB, &mo, &full_a[st], HD * h, 0, i0);
+            KV_TRACE(true, 0, g);
+          }
+          {
+            const int st = g % KV_NB;
+            if (g >= KV_NB) umma::mbar_wait(&empty_b[st], ((g / KV_NB) - 1) & 1);
+            uint8_t* sb = sm + KV_SM_B + st * KV_BSTAGE;
+            const uint32_t pbytes = (uint32_t)((nq & ~1) * 24), lbytes = (uint32_t)(nq * 32);
+            if (nq & 1) {  // odd tail: the last query's 24 bytes by plain loads (ordered by the arrive)
+              double* tail = reinterpret_cast<double*>(sb) + 3 * (nq - 1);
+              const double* src = pos + 3 * ((size_t)i0 + nq - 1);
+              tail[0] = src[0]; tail[1] = src[1]; tail[2] = src[2];
+            }
+            umma::mbar_arrive_expect_tx(&full_b[st], pbytes + 2 * lbytes);
+            if (pbytes) umma::bulk_load(sb, pos + 3 * (size_t)i0, pbytes, &full_b[st]);
+            umma::bulk_load(sb + KV_B_L, lse + (size_t)i0 * 8, lbytes, &full_b[st]);
+            umma::bulk_load(sb + KV_B_D, delta + (size_t)i0 * 8, lbytes, &full_b[st]);
+          }
+          if (c == 0 && h >= 1 && h + 1 < 8) {  // V_(h+1) into the buffer head h-1 used
+            umma::mbar_wait(&vh_free[(h + 1) & 1], ((h - 1) >> 1) & 1);
+            load_vh(h + 1);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer
+      constexpr uint32_t idesc_s = umma::idesc_bf16(128, KC, 0, 0);
+      constexpr uint32_t idesc_d = umma::idesc_bf16(128, KV, 0, 1);
+      constexpr uint32_t idesc_v = umma::idesc_bf16(128, NV, 0, 0);
+      auto issue_s = [&](int g, bool last) {
+        const int b = g & 1, st = g % KV_NA;
+        umma::mbar_wait(&full_a[st], (g / KV_NA) & 1);
+        if (g >= 2) umma::mbar_wait(&s_free[b], ((g >> 1) - 1) & 1);
+        umma::tc_fence_after();
+        // descriptors advance by (byte offset >> 4) from one base: the single issuing thread
+        // would otherwise spend ~100 cycles of dependent integer ops per MMA building them
+        const uint64_t qd = umma::sdesc(umma::smem_u32(sm + st * KV_ASTAGE), 16, 512, 4);
+        const uint32_t ts = t_s0 + 32 * b;
+        if (!(a.dbg & 16)) {
+#pragma unroll
+          for (int s = 0; s < 2 * MM; ++s)
+            umma::mma_f16_ts(ts, t_k + 8 * s, qd + (uint64_t)(((s >> 1) * KC * DH * 2 + (s & 1) * 32) >> 4), idesc_s,
+                             s > 0 ? 1u : 0u);
+        }
+        umma::mma_commit(&s_full[b]);
+        umma::mma_commit(&empty_a[st]);
+        if (last) umma::mma_commit(k_free);
+        KV_TRACE(true, 1, g);
+      };
+      auto issue_d = [&](int g, int h, bool last) {
+        const int b = g & 1;
+        umma::mbar_wait(&dog_full[b], (g >> 1) & 1);
+        if (g >= 1) umma::mbar_wait(d_free, (g - 1) & 1);
+        umma::tc_fence_after();
+        // A: V_h K-major SW32 (one 32-byte atom row per key, 8-key groups 256 B apart), one box per i';
+        // B: dOg read MN-major (no swizzle: 8 (f,i) x 8 (i',c) core matrices, (f,i) groups 128 B
+        //    apart (SBO), (i',c) groups 2304 B apart (LBO))
+        const uint64_t vd = umma::sdesc(umma::smem_u32(sm + KV_SM_VH + (h & 1) * KV_VHB), 16, 256, 6);
+        const uint64_t dd = umma::sdesc(umma::smem_u32(sm + KV_SM_DOG + b * GBYTES), (KV / 8) * 128, 128, 0);
+        if (!(a.dbg & 4)) {
+#pragma unroll
+          for (int s = 0; s < MM; ++s)
+            umma::mma_f16(t_d, vd + (uint64_t)((s * (KV_VHB / MM)) >> 4), dd + (uint64_t)((s * 2 * (KV / 8) * 128) >> 4),
+                          idesc_d, s > 0 ? 1u : 0u);
+        }
+        umma::mma_commit(d_full);
+        if (last) umma::mma_commit(&vh_free[h & 1]);
+        KV_TRACE(true, 2, g);
+      };
+      auto issue_v = [&](int g, int c, int h) {
+        const int b = g & 1;
+        umma::mbar_wait(wt_full, g & 1);
+        if (c == 0 && h > 0) umma::mbar_wait(epi_done, (h - 1) & 1);  // dV of the previous head read out
+        umma::tc_fence_after();
+        const uint64_t wd = umma::sdesc(umma::smem_u32(sm + KV_SM_WT), 128, (KV / 8) * 128, 0);
+        const uint64_t dd = umma::sdesc(umma::smem_u32(sm + KV_SM_DOG + b * GBYTES), 128, (KV / 8) * 128, 0);
+        if (!(a.dbg & 8)) {
+          umma::mma_f16(t_dv, wd, dd, idesc_v, c > 0 ? 1u : 0u);
+#pragma unroll
+          for (int s = 1; s < MM; ++s) umma::mma_f16(t_dv, wd + (uint64_t)(16 * s), dd + (uint64_t)(16 * s), idesc_v, 1u);
+        }
+        umma::mma_commit(&wv_free[b]);
+        KV_TRACE(true, 3, g);
+      };
+      int g0 = 0;
+      for (int h = 0; h < 8; ++h) {
+        umma::mbar_wait(k_ready, h & 1);
+        KV_TRACE(true, 10, h);
+        umma::mbar_wait(&vh_full[h & 1], (h >> 1) & 1);
+        KV_TRACE(true, 10, 8 + h);
+        issue_s(g0, nch == 1);
+        issue_d(g0, h, nch == 1);
+        for (int c = 0; c < nch; ++c) {
+          if (c + 1 < nch) {
+            issue_s(g0 + c + 1, c + 2 == nch);
+            issue_d(g0 + c + 1, h, c + 2 == nch);
+          }
+          issue_v(g0 + c, c, h);
+        }
+        umma::mma_commit(acc_done);
+        g0 += nch;
+      }
+    }
+  } else if (is_row) {
+    // ================= key rows: P, dP, dscores, Wt'; dv epilogue
+    const int half = (warp - 2) >> 2;  // this warp's queries: quarters 2 half, 2 half + 1 of every chunk
+    const int e0 = kin ? rev_ptr[kj] : 0;
+    const int nvk = kin ? rev_ptr[kj + 1] - e0 : 0;
+    const uint32_t* rl = rowlist + e0;
+    int g0 = 0;
+    for (int h = 0; h < 8; ++h) {
+      int rp = 0, rbase = 0;
+      uint32_t ent = nvk > 0 ? __ldg(rl) : 0xffff0000u;
+      for (int c = 0; c < nch; ++c) {
+        const int g = g0 + c, b = g & 1, sb_i = g % KV_NB;
+        unsigned vmask = 0u;
+        if ((int)(ent >> 16) == c) {
+          vmask = ent & 0xffffu;
+          ++rp;
+          ent = rp < nvk ? __ldg(rl + rp) : 0xffff0000u;
+        }
+        if (a.dbg & 1) vmask = 0u;
+        // the pair records of my 8 queries, issued before the barrier waits (their latency hides there)
+        uint4 gr[2][4][2];
+        {
+          int eq = e0 + rbase + (half ? __popc(vmask & 0xffu) : 0);  // my first valid query's entry
+          const unsigned hm = (vmask >> (8 * half)) & 0xffu;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const uint4* src = reinterpret_cast<const uint4*>(geom + eq + __popc(hm & ((1u << t) - 1u)));
+            if (hm >> t & 1) {
+              gr[t >> 2][t & 3][0] = __ldg(src);
+              gr[t >> 2][t & 3][1] = __ldg(src + 1);
+            } else {
+              gr[t >> 2][t & 3][0] = gr[t >> 2][t & 3][1] = make_uint4(0, 0, 0, 0);
+            }
+          }
+        }
+        rbase += __popc(vmask);
+        umma::mbar_wait(&s_full[b], (g >> 1) & 1);
+        umma::mbar_wait(d_full, g & 1);
+        umma::mbar_wait(&full_b[sb_i], (g / KV_NB) & 1);
+        umma::tc_fence_after();
+        KV_TRACE(tid == 64, 4, g);
+        const uint8_t* sb = sm + KV_SM_B + sb_i * KV_BSTAGE;
+        uint8_t* wt = sm + KV_SM_WT;
+#pragma unroll
+        for (int qq = 0; qq < 2; ++qq) {
+          const int quarter = 2 * half + qq;
+          const unsigned qm = (vmask >> (4 * quarter)) & 0xfu;
+          uint32_t r[40];  // [0, 4): S^T of the quarter's queries; [4, 40): D at 4 + 4 f + t
+          umma::tmem_ld_4_36(t_s0 + 32 * b + 4 * quarter + lane_base, t_d + 36 * quarter + lane_base, r);
+          if (qq == 1) {
+            umma::tc_fence_before();
+            umma::mbar_arrive(&s_free[b]);
+            umma::mbar_arrive(d_free);
+          }
+          const float* ls = reinterpret_cast<const float*>(sb + KV_B_L) + 32 * quarter + h;
+          const float* dl = reinterpret_cast<const float*>(sb + KV_B_D) + 32 * quarter + h;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float y[MM];
+            {
+              const __half2* h2 = reinterpret_cast<const __half2*>(&gr[qq][t][0]);
+              float2 f;
+              f = __half22float2(h2[0]); y[0] = f.x; y[1] = f.y;
+              f = __half22float2(h2[1]); y[2] = f.x; y[3] = f.y;
+              f = __half22float2(h2[2]); y[4] = f.x; y[5] = f.y;
+              f = __half22float2(h2[3]); y[6] = f.x; y[7] = f.y;
+              y[8] = __low2float(*reinterpret_cast<const __half2*>(&gr[qq][t][1].x));
+            }
+            if (qm >> t & 1) {
+              const float sc = fmaf(a.tau, __uint_as_float(r[t]), __uint_as_float(gr[qq][t][1].y));
+              const float P = __expf(sc - ls[8 * t]);
+              float dp = 0.f;
+#pragma unroll
+              for (int f = 0; f < MM; ++f) dp = fmaf(y[f], __uint_as_float(r[4 + 4 * f + t]), dp);
+              dsbuf[(size_t)(int)gr[qq][t][1].z * 8 + h] = P * (dp - dl[8 * t]);
+#pragma unroll
+              for (int f = 0; f < MM; ++f) r[4 + 4 * f + t] = __float_as_uint(P * y[f]);
+            } else {
+#pragma unroll
+              for (int f = 0; f < MM; ++f) r[4 + 4 * f + t] = 0u;
+            }
+          }
+          if (qq == 0) KV_TRACE(tid == 64, 5, g);
+          if (qq == 0 && g >= 1) umma::mbar_wait(&wv_free[(g - 1) & 1], ((g - 1) >> 1) & 1);  // Wt' free
+          if (qq == 0) KV_TRACE(tid == 64, 6, g);
+#pragma unroll
+          for (int f = 0; f < MM; ++f) {
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(__uint_as_float(r[4 + 4 * f]), __uint_as_float(r[5 + 4 * f]));
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(__uint_as_float(r[6 + 4 * f]), __uint_as_float(r[7 + 4 * f]));
+            uint2 u;
+            u.x = *reinterpret_cast<const uint32_t*>(&lo);
+            u.y = *reinterpret_cast<const uint32_t*>(&hi);
+            *reinterpret_cast<uint2*>(wt + cm_off(row, 36 * quarter + 4 * f)) = u;
+          }
+        }
+        umma::mbar_arrive(&empty_b[sb_i]);  // done with the stage's positions, lse and delta
+        umma::fence_proxy_async();
+        umma::mbar_arrive(wt_full);
+        KV_TRACE(tid == 64, 7, g);
+      }
+      g0 += nch;
+      KV_TRACE(tid == 64, 11, 16 + h);
+      // ---- epilogue: dv_j of head h, the two halves each store half of the (i', c) columns
+      KV_TRACE(tid == 64, 11, h);
+      umma::mbar_wait(acc_done, h & 1);
+      umma::tc_fence_after();
+      KV_TRACE(tid == 64, 11, 8 + h);
+      for (int cc = half ? 5 : 0; cc < (half ? MM : 5); ++cc) {
+        uint32_t rr[16];
+        umma::tmem_ld16(t_dv + lane_base + cc * 16, rr);
+        float v[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) v[t] = __uint_as_float(rr[t]);
+        if (kin) {
+          uint4* dst = reinterpret_cast<uint4*>(dv + ((size_t)kj * MM + cc) * 128 + HD * h);
+          dst[0] = pack8(v);
+          dst[1] = pack8(v + 8);
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(epi_done);
+    }
+  } else {
+    // ================= query-side source coupling dOg (+ K_h rows 0-2 into TMEM) (warps 10-13)
+    const int vt_id = tid - 320;
+    const int vc = vt_id & 15, vjp = vt_id >> 4;  // channel, query pair (2 vjp, 2 vjp + 1)
+    load_k(0);
+    int g0 = 0;
+    for (int h = 0; h < 8; ++h) {
+      if (h + 1 < 8 && kin)  // next head's K rows into L2 while this head runs
+        for (int m = 0; m < MM; ++m) asm volatile("prefetch.global.L2 [%0];" ::"l"(krow + m * 256 + DH * (h + 1)));
+      for (int c = 0; c < nch; ++c) {
+        const int g = g0 + c, b = g & 1, st = g % KV_NA;
+        umma::mbar_wait(&full_a[st], (g / KV_NA) & 1);
+        KV_TRACE(vt_id == 0, 8, g);
+        const unsigned short* ost = reinterpret_cast<const unsigned short*>(sm + st * KV_ASTAGE + KV_QB);
+        float d2[MM][2];
+#pragma unroll
+        for (int o = 0; o < MM; ++o)
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            d2[o][t] = __uint_as_float((uint32_t)ost[((2 * vjp + t) * MM + o) * HD + vc] << 16);
+        umma::mbar_arrive(&empty_a[st]);
+        if (g >= 2) umma::mbar_wait(&wv_free[b], ((g >> 1) - 1) & 1);  // dOg buffer b free
+        uint8_t* dog = sm + KV_SM_DOG + b * GBYTES;
+        if (!(a.dbg & 2))
+          es_vgT_all(d2, [&](int ip, int f, float x0, float x1) {
+            const __nv_bfloat162 pk = __floats2bfloat162_rn(x0, x1);
+            *reinterpret_cast<uint32_t*>(dog + cm_off(ip * HD + vc, kv_k(f, 2 * vjp))) =
+                *reinterpret_cast<const uint32_t*>(&pk);
+          });
+        umma::fence_proxy_async();
+        umma::mbar_arrive(&dog_full[b]);
+        KV_TRACE(vt_id == 0, 9, g);
+      }
+      g0 += nch;
+      if (h + 1 < 8) {  // K_(h+1) rows 0-2 once the head's last S MMA is done (its dOg all produced: no cycle)
+        KV_TRACE(vt_id == 0, 11, 32 + h);
+        umma::mbar_wait(k_free, h & 1);
+        KV_TRACE(vt_id == 0, 11, 40 + h);
+        umma::tc_fence_after();
+        if (a.dbg & 32) umma::mbar_arrive(k_ready);
+        else load_k(h + 1);
+        KV_TRACE(vt_id == 0, 11, 48 + h);
+      }
+    }
+  }
+  umma::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tmem, 512);
+#ifdef ES_TC_TRACE
+  if (KTRACE && tid == 0) {
+    const long long t0 = g_ktrace[0][0];
+    printf("KTRACE nch=%d\n", nch);
+    for (int g = 0; g < 8 * nch && g < 256; ++g)
+      printf("KTRACE g=%d tmaA=%lld S=%lld D=%lld V=%lld rowW=%lld rowM=%lld rowWt=%lld rowE=%lld cpA=%lld cpE=%lld\n", g,
+             g_ktrace[0][g] - t0, g_ktrace[1][g] - t0, g_ktrace[2][g] - t0, g_ktrace[3][g] - t0, g_ktrace[4][g] - t0,
+             g_ktrace[5][g] - t0, g_ktrace[6][g] - t0, g_ktrace[7][g] - t0, g_ktrace[8][g] - t0, g_ktrace[9][g] - t0);
+    for (int h = 0; h < 8; ++h)
+      printf("KTRACE h=%d k_ready=%lld vh_full=%lld epi_wait=%lld epi_go=%lld rowK0=%lld rowK1=%lld cpVdone=%lld "
+             "cpKfree=%lld cpK1=%lld\n", h, g_ktrace[10][h] - t0, g_ktrace[10][8 + h] - t0, g_ktrace[11][h] - t0,
+             g_ktrace[11][8 + h] - t0, g_ktrace[11][16 + h] - t0, g_ktrace[11][24 + h] - t0, g_ktrace[11][32 + h] - t0,
+             g_ktrace[11][40 + h] - t0, g_ktrace[11][48 + h] - t0);
+  }
+#endif
+}
+}  // namespace
+
+bool attn_kv_tc_applicable(const AttnArgs& a) {
+  const char* e = getenv("ES_KV_TC");  // read per call: the tests switch it
+  if (e && e[0] == '0') return false;
+  return attn_dq_tc_applicable(a) && a.N == a.Nk && a.row0 == 0;
+}
+
+size_t attn_kv_tc_geom_bytes(const AttnArgs& a) { return align256((size_t)a.N * a.K * sizeof(PairGeom)); }
+
+es_status attn_kv_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                            const int32_t* rev_ptr, const int32_t* rev_pair, const float* lse, const void* dout,
+                            const float* delta, float* dsbuf, void* dv, void* geom_ws, cudaStream_t st) {
+  if (a.N == 0) return ES_OK;
+  if (!a.tiles) return fail(ES_INVALID_ARGUMENT, "attn_kv_tc: needs the key-side tile lists");
+  if (!geom_ws) return fail(ES_INVALID_ARGUMENT, "attn_kv_tc: no pair-geometry workspace");
+  es_status s = upload_tc_tables();
+  if (s != ES_OK) return s;
+  const TcScratch t = tc_scratch(key_side(a));
+  const TcPtrs pp = tc_ptrs(const_cast<char*>(static_cast<const char*>(a.tiles)) + tiles_query_bytes(a), t);
+  CUtensorMap mq, mo, mvh;
+  if (!map3t(&mq, q, 256, MM, a.N, DH, KC, MM, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mo, dout, 128, MM, a.N, HD, MM, KC, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !map3t(&mvh, v, 128, MM, a.Nk, HD, TQ, MM, CU_TENSOR_MAP_SWIZZLE_32B))
+    return fail(ES_CUDA_ERROR, "attn_kv_tc: tensor map encode failed");
+  TcArgs ta{};
+  ta.N = a.N; ta.K = a.K; ta.row0 = a.row0; ta.Nk = a.Nk;
+  ta.tau = a.tau; ta.r_cut = a.r_cut; ta.inv_rcut = 1.f / a.r_cut;
+  ta.phi_mode = a.phi_mode; ta.periodic = a.periodic;
+  ta.bx = a.box[0]; ta.by = a.box[1]; ta.bz = a.box[2];
+  ta.bias_mode = a.bias_mode; ta.b0 = a.bias[0]; ta.b1 = a.bias[1]; ta.b2 = a.bias[2];
+  {  // profiling switches (ES_KV_DBG, outputs wrong): 1 no pair math, 2 no dOg math, 4 no D MMA,
+     // 8 no dV MMA, 16 no S MMA, 32 no per-head K reload (coupling rows)
+    const char* e = getenv("ES_KV_DBG");
+    ta.dbg = e ? atoi(e) : 0;
+  }
+  PairGeom* geom = static_cast<PairGeom*>(geom_ws);
+  attn_pair_geom_kernel<<<(a.Nk + 255) / 256, 256, 0, st>>>(ta, pos, rev_ptr, rev_pair, geom);
+  const int smem = KV_SM_TOTAL + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_kv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  attn_kv_tc_kernel<<<t.ntiles, TC_THREADS, smem, st>>>(mq, mo, mvh, ta, (const bf16*)k, pos, lse, delta, pp.cptr,
+                                                        pp.clist, pp.rowlist, pp.tstart, rev_ptr, geom, dsbuf,
+                                                        (bf16*)dv);
+  return cuda_status(cudaGetLastError(), "attn_kv_tc_kernel");
 }
 
 }  // namespace es

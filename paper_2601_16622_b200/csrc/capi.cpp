@@ -203,7 +203,9 @@ size_t es_attn_bwd_workspace_size(const es_attn_desc* d) {
   if (!d || d->N <= 0 || check_attn(d) != ES_OK) return 256;
   const AttnArgs a = to_args(d);
   // tensor-core passes without prebuilt tiles: the tile lists (query + key side) are built in the workspace
-  return bwd_base_bytes(d) + (attn_dq_tc_applicable(a) ? attn_tc_tiles_bytes(a) : 0);
+  // (+ the tensor-core key pass's per-pair geometry records after them)
+  return bwd_base_bytes(d) + (attn_dq_tc_applicable(a) ? align256(attn_tc_tiles_bytes(a)) : 0) +
+         (attn_kv_tc_applicable(a) ? attn_kv_tc_geom_bytes(a) : 0);
 }
 
 es_status es_attn_bwd(const es_attn_desc* d, const void* q, const void* k, const void* v, const double* pos,

@@ -75,6 +75,13 @@ void attn_tc_tiles_layout(const AttnArgs& a, es_attn_tiles_layout* out);
 const int* attn_tc_rank_of(const AttnArgs& a, const void* tiles);
 // tensor-core dk = tau dS^T Q over key tiles (key-side lists in the tiles buffer or the workspace)
 bool attn_dk_tc_applicable(const AttnArgs& a);
+// the key pass (dv + dscores) on the tensor cores; dk / dq then follow on the tensor cores
+bool attn_kv_tc_applicable(const AttnArgs& a);
+es_status attn_kv_tc_launch(const AttnArgs& a, const void* q, const void* k, const void* v, const double* pos,
+                            const int32_t* rev_ptr, const int32_t* rev_pair, const float* lse, const void* dout,
+                            const float* delta, float* dsbuf, void* dv, void* geom_ws, cudaStream_t st);
+size_t attn_kv_tc_geom_bytes(const AttnArgs& a);  // per-pair geometry records of the key pass
+es_status attn_delta_launch(const AttnArgs& a, const void* out, const void* dout, float* delta, cudaStream_t st);
 size_t attn_dk_tc_workspace(const AttnArgs& a);
 es_status attn_dk_tc_launch(const AttnArgs& a, const void* q, const int32_t* nbr, const int32_t* rev_ptr,
                             const int32_t* rev_pair, const float* dsbuf, void* dk, void* ws, size_t ws_bytes,

@@ -149,12 +149,14 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
       if (c >= NBUF) umma::mbar_wait(&acc_free[b], ((c / NBUF) - 1) & 1);
       umma::tc_fence_after();
       const uint8_t* B = Bs + b * 32768;
+      // descriptors advance by (byte offset >> 4) from one base (no per-MMA descriptor arithmetic
+      // on the single issuing thread)
+      const uint64_t ad0 = umma::sdesc(umma::smem_u32(As), 16, 1024), bd0 = umma::sdesc(umma::smem_u32(B), 8192, 1024);
 #pragma unroll
       for (int s = 0; s < 8; ++s) {
         const int kb = s >> 2, ks = s & 3;
-        const uint64_t ad = umma::sdesc(umma::smem_u32(As + kb * 16384) + ks * 32, 16, 1024);
-        const uint64_t bd = umma::sdesc(umma::smem_u32(B + kb * 16384) + ks * 2048, 8192, 1024);
-        umma::mma_f16(taddr + 128 * b, ad, bd, idesc, s > 0 ? 1u : 0u);
+        umma::mma_f16(taddr + 128 * b, ad0 + (uint64_t)((kb * 16384 + ks * 32) >> 4),
+                      bd0 + (uint64_t)((kb * 16384 + ks * 2048) >> 4), idesc, s > 0 ? 1u : 0u);
       }
       umma::mma_commit(&acc_full[b]);
       umma::mma_commit(&b_empty[b]);
@@ -264,10 +266,10 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
       umma::mbar_wait(&full[s], round & 1);
       umma::tc_fence_after();
       const uint32_t a0 = umma::smem_u32(smem + s * 32768);
+      const uint64_t ad0 = umma::sdesc(a0, 16, 1024), bd0 = umma::sdesc(a0 + 16384, 16, 1024);
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks)
-        umma::mma_f16(taddr, umma::sdesc(a0 + ks * 32, 16, 1024), umma::sdesc(a0 + 16384 + ks * 32, 16, 1024),
-                      idesc, (kb | ks) ? 1u : 0u);
+        umma::mma_f16(taddr, ad0 + (uint64_t)(2 * ks), bd0 + (uint64_t)(2 * ks), idesc, (kb | ks) ? 1u : 0u);
       umma::mma_commit(&empty[s]);
     }
     umma::mma_commit(done);
@@ -370,9 +372,10 @@ __global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__
         umma::mbar_wait(&full[s], round & 1);
         umma::tc_fence_after();
         const uint32_t a0 = umma::smem_u32(smem + s * stage_bytes);
+        const uint64_t ad0 = umma::sdesc(a0, half, 1024), bd0 = umma::sdesc(a0 + 2 * half, half, 1024);
+#pragma unroll 4
         for (int ks = 0; ks < R / 16; ++ks)
-          umma::mma_f16(taddr, umma::sdesc(a0 + ks * 2048, half, 1024),
-                        umma::sdesc(a0 + 2 * half + ks * 2048, half, 1024), idesc, (it | ks) ? 1u : 0u);
+          umma::mma_f16(taddr, ad0 + (uint64_t)(128 * ks), bd0 + (uint64_t)(128 * ks), idesc, (it | ks) ? 1u : 0u);
         umma::mma_commit(&empty[s]);
       }
       umma::mma_commit(done);

@@ -41,9 +41,12 @@ def has_gpu() -> bool:
         return False
 
 
-@pytest.fixture(params=["simt_dk", "tc_dk"])
+@pytest.fixture(params=["tc_kv", "simt_dk", "tc_dk"])
 def dk_path(request, monkeypatch):
-    """Both backward variants: dk in the key-centric SIMT pass (default) and the
-    tensor-core dk pass over key-side tiles (ES_DK_TC=1)."""
+    """The backward variants of a molecule batch: the tensor-core key pass
+    (default: dv + dscores, then dk and dq on the tensor cores), the SIMT key
+    pass with dk (ES_KV_TC=0), and the SIMT key pass without dk followed by the
+    tensor-core dk pass (ES_KV_TC=0, ES_DK_TC=1)."""
+    monkeypatch.setenv("ES_KV_TC", "1" if request.param == "tc_kv" else "0")
     monkeypatch.setenv("ES_DK_TC", "1" if request.param == "tc_dk" else "0")
     return request.param
