@@ -127,7 +127,7 @@ def kernel_times(fn) -> dict:
 def short_name(n: str) -> str:
     if "attn_dqk_tc_kernel" in n:
         return "attn_dk_tc" if "<true>" in n else "attn_dq_tc"
-    for key in ("attn_fwd_tc", "attn_kv_tc", "attn_bwd_q_tc", "attn_bwd_k_tc", "attn_bwd_kv", "attn_dq_tc", "attn_delta",
+    for key in ("attn_fwd_tc", "attn_kv_tc", "attn_pair_geom", "attn_dk_tc", "attn_bwd_q_tc", "attn_bwd_k_tc", "attn_bwd_kv", "attn_dq_tc", "attn_delta",
                 "attn_fwd_kernel", "attn_bwd_q_kernel", "proj_fwd_tc", "proj_dh_tc", "proj_dw_tc", "proj_fwd_kernel",
                 "proj_bwd", "nbr_segment", "nbr_grid", "tr_sort", "tr_fill", "tr_count", "tc_rowlist", "tc_tiles",
                 "tc_mask", "tc_count", "tc_fill", "tc_rowtile", "grid_", "DeviceScan", "DeviceRadix", "nccl"):
@@ -658,9 +658,11 @@ def roofline(wl, t, kt_fwd, kt_bwd, kt_step, n_loc, E, s_bytes, fl, step_ms) -> 
         "kernels": per_kernel,
         "tensor_pipe_pct_ncu": tensor_pct or None,
         "fp32_peak_measured": fp,
-        # the SIMT key pass computes in fp32 on the CUDA cores: its compute roofline is the FFMA2 peak
+        # a SIMT key pass (forces / ES_KV_TC=0) computes in fp32 on the CUDA cores: its compute roofline is
+        # the FFMA2 peak; the tensor-core key pass is reported against the bf16 peak above
         "compute_frac_fp32_simt": (round(fl[flop_key] / (t[dom] * 1e-3) / 1e12 / fp["ffma2_tflops"], 4)
-                                   if fp and fp.get("ffma2_tflops", 0) > 0 else None),
+                                   if fp and fp.get("ffma2_tflops", 0) > 0 and "attn_bwd_kv" in per_kernel
+                                   else None),
         "step_frac_hbm": round(sum(by.values()) / (step_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
     }
 

@@ -67,7 +67,10 @@ def main(rep, as_json, traffic=False):
     if traffic:  # profiles/ncu_traffic.json: what bench.py's roofline line reads (first launch of each kernel)
         out = {"source": f"{rep} (ncu --set full)", "bytes_per_launch": {}}
         for e in res:
-            name = e["kernel"].split("(")[0].split("::")[-1].split("<")[0].strip()
+            full = e["kernel"].split("(")[0].split("::")[-1].strip()
+            name = full.split("<")[0]
+            if name == "attn_dqk_tc_kernel":  # the two instances: <0> dq (query tiles), <1> dk (key tiles)
+                name = "attn_dk_tc_kernel" if full.endswith("<1>") else "attn_dq_tc_kernel"
             if name in out["bytes_per_launch"]:
                 continue
             byt = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
