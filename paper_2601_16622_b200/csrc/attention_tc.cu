@@ -1659,11 +1659,12 @@ __global__ void __launch_bounds__(256) attn_pair_geom_kernel(TcArgs a, const dou
                                                              const int* __restrict__ rev_ptr,
                                                              const int* __restrict__ rev_pair,
                                                              PairGeom* __restrict__ geom) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  // 4 threads per key, entries strided by 4: independent loads in flight instead of one dependent chain
+  const int j = (int)(((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2), sub = threadIdx.x & 3;
   if (j >= a.Nk) return;
   const double kx = pos[3 * (size_t)j], ky = pos[3 * (size_t)j + 1], kz = pos[3 * (size_t)j + 2];
   const int e1 = rev_ptr[j + 1];
-  for (int e = rev_ptr[j]; e < e1; ++e) {
+  for (int e = rev_ptr[j] + sub; e < e1; e += 4) {
     const int pr = rev_pair[e];
     const size_t i = (size_t)(pr / a.K);
     // r_ij = pos_j - pos_i, as the forward (key minus query)
@@ -2167,7 +2168,7 @@ es_status attn_kv_tc_launch(const AttnArgs& a, const void* q, const void* k, con
     ta.dbg = e ? atoi(e) : 0;
   }
   PairGeom* geom = static_cast<PairGeom*>(geom_ws);
-  attn_pair_geom_kernel<<<(a.Nk + 255) / 256, 256, 0, st>>>(ta, pos, rev_ptr, rev_pair, geom);
+  attn_pair_geom_kernel<<<(unsigned)(((size_t)a.Nk * 4 + 255) / 256), 256, 0, st>>>(ta, pos, rev_ptr, rev_pair, geom);
   const int smem = KV_SM_TOTAL + 1024;
   static bool attr = false;
   if (!attr) {
