@@ -16,7 +16,9 @@ es_status attn_bwd_launch(const AttnArgs& a, const void* q, const void* k, const
     return ES_OK;
   }
   const bool tc_dq = attn_dq_tc_applicable(a);
-  const bool tc_kv = !dpos && attn_kv_tc_applicable(a);  // forces stay on the SIMT key pass (any L)
+  // forces stay on the SIMT key pass (any L); the tensor-core key pass bulk-copies query positions and
+  // lse rows in 16-byte units (an unaligned caller buffer takes the SIMT pass)
+  const bool tc_kv = !dpos && attn_kv_tc_applicable(a) && ((uintptr_t)pos & 15) == 0 && ((uintptr_t)lse & 15) == 0;
   const bool tc_dk = tc_kv || attn_dk_tc_applicable(a);
   AttnArgs at = a;
   if (tc_dq && !at.tiles) {  // no prebuilt tile lists: build query- and key-side lists in the workspace first
