@@ -1469,13 +1469,17 @@ AttnArgs key_side(const AttnArgs& a) {
 }
 
 es_status tc_build_key_lists(const AttnArgs& a, const int32_t* nbr, const int32_t* rev_ptr, const int32_t* rev_pair,
-                             void* ws, TcLists* out, cudaStream_t st, const int32_t* seg = nullptr, int nseg = 0) {
+                             void* ws, TcLists* out, cudaStream_t st, const int32_t* seg = nullptr, int nseg = 0,
+                             const int* q_tstart = nullptr) {
   const AttnArgs b = key_side(a);
   const TcScratch t = tc_scratch(b);
   const TcPtrs pp = tc_ptrs(ws, t);
   size_t cub_bytes = t.cub_bytes;
-  // key tiles: the query tiles' packing when keys and queries are the same atoms (molecule batches)
-  if (seg && nseg > 0 && a.N == a.Nk) tc_tiles_packed_kernel<<<1, 1024, 0, st>>>(b.N, nseg, seg, t.ntiles, pp.tstart);
+  // key tiles: the query tiles' packing when keys and queries are the same atoms (molecule batches) --
+  // copied from the query-side lists when the caller just built them (the packing is one CTA's serial scan)
+  if (seg && nseg > 0 && a.N == a.Nk && q_tstart)
+    cudaMemcpyAsync(pp.tstart, q_tstart, sizeof(int) * (size_t)(t.ntiles + 1), cudaMemcpyDeviceToDevice, st);
+  else if (seg && nseg > 0 && a.N == a.Nk) tc_tiles_packed_kernel<<<1, 1024, 0, st>>>(b.N, nseg, seg, t.ntiles, pp.tstart);
   else tc_tiles_uniform_kernel<<<(t.ntiles + 256) / 256, 256, 0, st>>>(b.N, t.ntiles, pp.tstart);
   tc_rowtile_kernel<<<t.ntiles, 128, 0, st>>>(t.ntiles, pp.tstart, pp.rtile);
   cudaMemsetAsync(pp.mask, 0, (size_t)t.ntiles * t.words * 4, st);
@@ -1589,7 +1593,8 @@ es_status attn_tc_tiles_build(const AttnArgs& a, const int32_t* nbr, const int32
   TcLists lists;
   es_status s = tc_build_lists(a, nbr, tiles, t, (int*)((char*)tiles + t.total), &lists, st, seg, nseg);
   if (s != ES_OK || !keys) return s;
-  return tc_build_key_lists(a, nbr, rev_ptr, rev_pair, (char*)tiles + tiles_query_bytes(a), &lists, st, seg, nseg);
+  return tc_build_key_lists(a, nbr, rev_ptr, rev_pair, (char*)tiles + tiles_query_bytes(a), &lists, st, seg, nseg,
+                            lists.tstart);
 }
 
 
