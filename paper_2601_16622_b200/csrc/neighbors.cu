@@ -27,9 +27,11 @@ __device__ __forceinline__ double d2_exact(double xi, double yi, double zi, doub
                                            int periodic, double bx, double by, double bz) {
   double dx = __dsub_rn(xj, xi), dy = __dsub_rn(yj, yi), dz = __dsub_rn(zj, zi);
   if (periodic) {
-    dx = __dsub_rn(dx, __dmul_rn(bx, rint(__ddiv_rn(dx, bx))));
-    dy = __dsub_rn(dy, __dmul_rn(by, rint(__ddiv_rn(dy, by))));
-    dz = __dsub_rn(dz, __dmul_rn(bz, rint(__ddiv_rn(dz, bz))));
+    // |dx| < box/2 => rint(dx/box) == 0 exactly (a correctly rounded quotient can reach 0.5 at most,
+    // which rounds to even 0): the fp64 divisions run only for pairs that actually wrap
+    if (!(fabs(dx) < 0.5 * bx)) dx = __dsub_rn(dx, __dmul_rn(bx, rint(__ddiv_rn(dx, bx))));
+    if (!(fabs(dy) < 0.5 * by)) dy = __dsub_rn(dy, __dmul_rn(by, rint(__ddiv_rn(dy, by))));
+    if (!(fabs(dz) < 0.5 * bz)) dz = __dsub_rn(dz, __dmul_rn(bz, rint(__ddiv_rn(dz, bz))));
   }
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
@@ -70,14 +72,61 @@ __device__ __forceinline__ void emit(const NbrK& p, int i, const TopK& t, int32_
   count[i] = t.n;
 }
 
-// Warp per atom for segments of <= SEG_WARP_MAX + 1 atoms (molecule
-// batches): the lanes evaluate the segment's candidates 32 at a time and
-// compact the kept ones (d2 < r_cut^2, j != i) into shared memory; each kept
-// candidate's slot is then its rank under (d2, j) -- the same order the
-// sorted top-K produces -- so no per-thread sorted list (the scan kernel's
-// TopK lives in local memory).  Larger segments: lane 0 runs the scan.
+// Warp per atom: the lanes evaluate candidates 32 at a time and compact the
+// kept ones (d2 < r_cut^2, j != i) into shared memory; each kept candidate's
+// slot is then its rank under (d2, j) -- the same order the sorted top-K
+// produces -- so no per-thread sorted list (TopK lives in local memory).  The
+// buffer bounds the KEPT candidates (an atom's neighbours within r_cut), not
+// the segment or cell population; an atom with more falls back to lane 0's
+// TopK scan of the same candidate set.
 constexpr int SEG_WARP_MAX = 256;
 constexpr int SEG_WARPS = 8;
+
+struct WarpCand {  // one warp's kept-candidate buffer
+  double* cd;
+  int* cj;
+  int n;
+  // lanes offer (d, j, keep); the kept ones are appended in lane order
+  __device__ __forceinline__ void offer(bool keep, double d, int j, int lane) {
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+      const int at = n + __popc(m & ((1u << lane) - 1u));
+      if (at < SEG_WARP_MAX) {
+        cd[at] = d;
+        cj[at] = j;
+      }
+    }
+    n += __popc(m);
+  }
+  // slots by rank under (d2, j); returns false when the buffer overflowed (caller falls back)
+  __device__ __forceinline__ bool emit_ranked(const NbrK& p, int r, int lane, int32_t* nbr, float* dist,
+                                              int32_t* count) const {
+    if (n > SEG_WARP_MAX) return false;
+    __syncwarp();
+    const int K = p.K;
+    int32_t* orow = nbr + (size_t)r * K;
+    float* drow = dist ? dist + (size_t)r * K : nullptr;
+    for (int c = lane; c < n; c += 32) {
+      const double d = cd[c];
+      const int j = cj[c];
+      int rank = 0;
+      for (int o = 0; o < n; ++o) {
+        const double od = cd[o];
+        rank += (od < d || (od == d && cj[o] < j)) ? 1 : 0;
+      }
+      if (rank < K) {
+        orow[rank] = j;
+        if (drow) drow[rank] = (float)sqrt(d);
+      }
+    }
+    for (int s = min(n, K) + lane; s < K; s += 32) {
+      orow[s] = -1;
+      if (drow) drow[s] = 0.f;
+    }
+    if (lane == 0) count[r] = min(n, K);
+    return true;
+  }
+};
 
 __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p, const double* __restrict__ pos,
                                                                           const int32_t* __restrict__ seg_ptr,
@@ -102,21 +151,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p
     a1 = seg_ptr[lo + 1];
   }
   const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
-  if (a1 - a0 > SEG_WARP_MAX + 1) {  // more candidates than the shared buffer holds
-    if (lane == 0) {
-      TopK t;
-      t.n = 0;
-      for (int j = a0; j < a1; ++j) {
-        if (j == i) continue;
-        const double d =
-            d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
-        if (d < p.rc2) t.insert(d, j, p.K);
-      }
-      emit(p, i, t, nbr, dist, count);
-    }
-    return;
-  }
-  int n = 0;
+  WarpCand wc{cd[warp], cj[warp], 0};
   for (int j0 = a0; j0 < a1; j0 += 32) {
     const int j = j0 + lane;
     double d = 0.0;
@@ -125,36 +160,19 @@ __global__ void __launch_bounds__(SEG_WARPS * 32) nbr_segment_warp_kernel(NbrK p
       d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
       keep = d < p.rc2;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (keep) {
-      const int at = n + __popc(m & ((1u << lane) - 1u));
-      cd[warp][at] = d;
-      cj[warp][at] = j;
-    }
-    n += __popc(m);
+    wc.offer(keep, d, j, lane);
   }
-  __syncwarp();
-  const int K = p.K;
-  int32_t* orow = nbr + (size_t)r * K;
-  float* drow = dist ? dist + (size_t)r * K : nullptr;
-  for (int c = lane; c < n; c += 32) {
-    const double d = cd[warp][c];
-    const int j = cj[warp][c];
-    int rank = 0;
-    for (int o = 0; o < n; ++o) {
-      const double od = cd[warp][o];
-      rank += (od < d || (od == d && cj[warp][o] < j)) ? 1 : 0;
+  if (wc.emit_ranked(p, r, lane, nbr, dist, count)) return;
+  if (lane == 0) {  // more than SEG_WARP_MAX atoms within r_cut: the sorted scan
+    TopK t;
+    t.n = 0;
+    for (int j = a0; j < a1; ++j) {
+      if (j == i) continue;
+      const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
+      if (d < p.rc2) t.insert(d, j, p.K);
     }
-    if (rank < K) {
-      orow[rank] = j;
-      if (drow) drow[rank] = (float)sqrt(d);
-    }
+    emit(p, i, t, nbr, dist, count);
   }
-  for (int s = min(n, K) + lane; s < K; s += 32) {
-    orow[s] = -1;
-    if (drow) drow[s] = 0.f;
-  }
-  if (lane == 0) count[r] = min(n, K);
 }
 
 // ---------------------------------------------------------------- hashed grid
@@ -205,38 +223,71 @@ __global__ void grid_bounds_kernel(int N, const unsigned* __restrict__ skey, int
   if (s == N - 1 || skey[s + 1] != k) end[k] = s + 1;
 }
 
-__global__ void __launch_bounds__(128) nbr_grid_kernel(NbrK p, GridK g, const double* __restrict__ pos,
-                                                       const int4* __restrict__ cell, const int* __restrict__ sidx,
-                                                       const int* __restrict__ start, const int* __restrict__ end,
-                                                       int32_t* __restrict__ nbr, float* __restrict__ dist,
-                                                       int32_t* __restrict__ count) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+// Warp per atom over the 27-cell stencil (the cell's candidates 32 at a time),
+// compact + rank as in the segment kernel; lane 0's TopK scan on overflow.
+__global__ void __launch_bounds__(SEG_WARPS * 32) nbr_grid_kernel(NbrK p, GridK g, const double* __restrict__ pos,
+                                                                  const int4* __restrict__ cell,
+                                                                  const int* __restrict__ sidx,
+                                                                  const int* __restrict__ start,
+                                                                  const int* __restrict__ end,
+                                                                  int32_t* __restrict__ nbr, float* __restrict__ dist,
+                                                                  int32_t* __restrict__ count) {
+  __shared__ double cd[SEG_WARPS][SEG_WARP_MAX];
+  __shared__ int cj[SEG_WARPS][SEG_WARP_MAX];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * SEG_WARPS + warp;
   if (r >= p.nrows) return;
   const int i = p.row0 + r;
-  TopK t;
-  t.n = 0;
   const double xi = pos[3 * i], yi = pos[3 * i + 1], zi = pos[3 * i + 2];
   const int4 ci = cell[i];
-  for (int ox = -1; ox <= 1; ++ox)
-    for (int oy = -1; oy <= 1; ++oy)
-      for (int oz = -1; oz <= 1; ++oz) {
-        int cx = ci.x + ox, cy = ci.y + oy, cz = ci.z + oz;
-        if (g.periodic) {
-          cx = (cx + g.nc[0]) % g.nc[0];
-          cy = (cy + g.nc[1]) % g.nc[1];
-          cz = (cz + g.nc[2]) % g.nc[2];
+  auto stencil = [&](auto&& visit) {
+    for (int ox = -1; ox <= 1; ++ox)
+      for (int oy = -1; oy <= 1; ++oy)
+        for (int oz = -1; oz <= 1; ++oz) {
+          int cx = ci.x + ox, cy = ci.y + oy, cz = ci.z + oz;
+          if (g.periodic) {
+            cx = (cx + g.nc[0]) % g.nc[0];
+            cy = (cy + g.nc[1]) % g.nc[1];
+            cz = (cz + g.nc[2]) % g.nc[2];
+          }
+          const unsigned h = cell_hash(cx, cy, cz, g.mask);
+          visit(cx, cy, cz, start[h], end[h]);
         }
-        const unsigned h = cell_hash(cx, cy, cz, g.mask);
-        for (int s = start[h]; s < end[h]; ++s) {
-          const int j = sidx[s];
-          const int4 cj = cell[j];
-          if (cj.x != cx || cj.y != cy || cj.z != cz || j == i) continue;
-          const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by,
-                                    p.bz);
-          if (d < p.rc2) t.insert(d, j, p.K);
+  };
+  WarpCand wc{cd[warp], cj[warp], 0};
+  stencil([&](int cx, int cy, int cz, int s0, int s1) {
+    for (int b = s0; b < s1; b += 32) {
+      const int s = b + lane;
+      double d = 0.0;
+      bool keep = false;
+      int j = -1;
+      if (s < s1) {
+        j = sidx[s];
+        const int4 cj4 = cell[j];
+        if (cj4.x == cx && cj4.y == cy && cj4.z == cz && j != i) {  // hash collisions filtered exactly
+          d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by, p.bz);
+          keep = d < p.rc2;
         }
       }
-  emit(p, i, t, nbr, dist, count);
+      wc.offer(keep, d, j, lane);
+    }
+  });
+  if (wc.emit_ranked(p, r, lane, nbr, dist, count)) return;
+  if (lane == 0) {  // more than SEG_WARP_MAX atoms within r_cut: the sorted scan over the same stencil
+    TopK t;
+    t.n = 0;
+    stencil([&](int cx, int cy, int cz, int s0, int s1) {
+      for (int s = s0; s < s1; ++s) {
+        const int j = sidx[s];
+        const int4 cj4 = cell[j];
+        if (cj4.x != cx || cj4.y != cy || cj4.z != cz || j == i) continue;
+        const double d = d2_exact(xi, yi, zi, pos[3 * j], pos[3 * j + 1], pos[3 * j + 2], p.periodic, p.bx, p.by,
+                                  p.bz);
+        if (d < p.rc2) t.insert(d, j, p.K);
+      }
+    });
+    emit(p, i, t, nbr, dist, count);
+  }
 }
 
 namespace {
@@ -334,7 +385,8 @@ es_status nbr_build_launch(const NbrArgs& a, const double* pos, const int32_t* s
   cudaMemsetAsync(start, 0, sizeof(int) * nb, st);
   cudaMemsetAsync(end, 0, sizeof(int) * nb, st);
   grid_bounds_kernel<<<blocks, tpb, 0, st>>>(a.N, skey, start, end);
-  nbr_grid_kernel<<<(a.nrows + tpb - 1) / tpb, tpb, 0, st>>>(p, g, pos, cell, sidx, start, end, nbr, dist, count);
+  nbr_grid_kernel<<<(a.nrows + SEG_WARPS - 1) / SEG_WARPS, SEG_WARPS * 32, 0, st>>>(p, g, pos, cell, sidx, start, end,
+                                                                                   nbr, dist, count);
   return cuda_status(cudaGetLastError(), "nbr_grid_kernel");
 }
 
