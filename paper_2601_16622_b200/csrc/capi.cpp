@@ -335,8 +335,10 @@ es_status es_attn_stats_query(const es_attn_desc* d, int64_t n_pairs, es_attn_st
     out->madds_proj_bwd = 2 * out->madds_proj_fwd;
     // forward: (mu, z, A) live on chip (registers / TMEM), no floating-point scratch in HBM
     out->aux_float_bytes_fwd = 0;
-    // backward: Delta [N][H] and the per-pair-head dscore [N][K][H] -- O(N K H), never O(N K C)
+    // backward: Delta [N][H] and the per-pair-head dscore [N][K][H] -- O(N K H), never O(N K C) -- plus,
+    // with the tensor-core key pass, its head-independent per-pair geometry records (32 bytes per slot)
     out->aux_float_bytes_bwd = 4 * N * H + 4 * N * K * H;
+    if (attn_kv_tc_applicable(to_args(d))) out->aux_float_bytes_bwd += 32 * N * K;
     out->aux_index_bytes = es_attn_tiles_workspace_size(d);
     out->workspace_fwd_bytes = es_attn_fwd_workspace_size(d);
     out->workspace_bwd_bytes = es_attn_bwd_workspace_size(d);
