@@ -38,7 +38,7 @@ EncodeTiledFn encode_fn() {
 
 // bf16 tensor map, dims innermost-first, 128B swizzle
 bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-              const uint32_t* box) {
+              const uint32_t* box, CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn f = encode_fn();
   if (!f) return false;
   cuuint64_t gd[5], gs[4];
@@ -50,7 +50,7 @@ bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, 
   }
   for (int i = 0; i < rank - 1; ++i) gs[i] = strides_bytes[i];
   return f(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gd, gs, bd, es_,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -90,14 +90,15 @@ __device__ __forceinline__ void store_row32(bf16* dst, const uint32_t (&r)[32]) 
 constexpr int NBUF = ES_PF_NBUF;  // B stages = TMEM accumulators; 1: ~75 KB smem, 128 TMEM columns -> 3 CTAs per SM
 __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant__ CUtensorMap mh,
                                                           const __grid_constant__ CUtensorMap mw, TcP p,
-                                                          bf16* __restrict__ q, bf16* __restrict__ k,
-                                                          bf16* __restrict__ v) {
+                                                          const __grid_constant__ CUtensorMap mq,
+                                                          const __grid_constant__ CUtensorMap mk,
+                                                          const __grid_constant__ CUtensorMap mv) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (umma::smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in .shared
   uint8_t* As = smem;                 // [2 kb][128 rows][64] bf16, 16 KB each
   uint8_t* Bs = smem + 32768;         // [NBUF stages][2 kb][2 nb][64 k-rows][64] bf16, 32 KB per stage
-  uint8_t* Stg = smem + 32768 + NBUF * 32768;  // [4 warps][32 rows][80 B] epilogue staging
-  uint64_t* bars = reinterpret_cast<uint64_t*>(Stg + 4 * 32 * 80);
+  uint8_t* Stg = smem + 32768 + NBUF * 32768;  // [4 warps][32 rows][64 B] epilogue staging (TMA-store SW64 box)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Stg + 4 * 2048);
   uint64_t* a_full = bars + 0;
   uint64_t* b_full = bars + 1;        // [2]
   uint64_t* b_empty = bars + 3;       // [2] MMA done reading the stage
@@ -171,12 +172,12 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
     const int b = c % NBUF, o0 = c * 128;
     umma::mbar_wait(&acc_full[b], (c / NBUF) & 1);
     umma::tc_fence_after();
-    // rows -> per-warp staging (32 rows x 32 columns, 80-byte padded rows: no
-    // bank conflicts) -> coalesced stores: 4 lanes write one row's 64 bytes,
-    // so every store instruction fills whole 32-byte sectors of 8 rows
-    // (the direct row stores wrote half sectors of 32 rows)
-    uint8_t* stg = Stg + warp * (32 * 80);
-#pragma unroll
+    // rows -> per-warp staging (32 rows x 32 columns, the 64-byte-swizzled layout of a TMA box:
+    // conflict-free, lane = row) -> one TMA store per 32 x 32 block, clipped at N by the tensor map
+    uint8_t* stg = Stg + warp * 2048;
+    const CUtensorMap* om = o0 < 2 * p.C ? &mq : o0 < 4 * p.C ? &mk : &mv;
+    const int oc = o0 < 2 * p.C ? o0 : o0 < 4 * p.C ? o0 - 2 * p.C : o0 - 4 * p.C;
+#pragma unroll 1
     for (int cc = 0; cc < 4; ++cc) {
       uint32_t r[32];
       umma::tmem_ld32(taddr + 128 * b + ((uint32_t)(warp * 32) << 16) + cc * 32, r);
@@ -187,27 +188,23 @@ __global__ void __launch_bounds__(160) proj_fwd_tc_kernel(const __grid_constant_
         const __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]));
         w[t] = *reinterpret_cast<const uint32_t*>(&h2);
       }
-#pragma unroll
-      for (int t = 0; t < 4; ++t) *reinterpret_cast<uint4*>(stg + lane * 80 + t * 16) = pk[t];
+      if (lane == 0) umma::bulk_wait_read0();  // the previous block's store has read the staging buffer
       __syncwarp();
 #pragma unroll
-      for (int it = 0; it < 4; ++it) {
-        const int rr = it * 8 + (lane >> 2), part = lane & 3;
-        const int nn = n0 + warp * 32 + rr;
-        if (nn < p.N) {
-          bf16* drow;
-          if (o0 < 2 * p.C) drow = q + ((size_t)nn * p.M + mm) * (2 * p.C) + o0;
-          else if (o0 < 4 * p.C) drow = k + ((size_t)nn * p.M + mm) * (2 * p.C) + (o0 - 2 * p.C);
-          else drow = v + ((size_t)nn * p.M + mm) * p.C + (o0 - 4 * p.C);
-          *reinterpret_cast<uint4*>(drow + cc * 32 + part * 8) = *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
-        }
+      for (int t = 0; t < 4; ++t)
+        *reinterpret_cast<uint4*>(stg + lane * 64 + ((t ^ ((lane >> 1) & 3)) << 4)) = pk[t];
+      umma::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) {
+        umma::tma_store_3d(om, stg, oc + cc * 32, mm, n0 + warp * 32);
+        umma::bulk_commit();
       }
-      __syncwarp();
     }
     umma::tc_fence_before();
     umma::mbar_arrive(&acc_free[b]);
   }
   }
+  if (warp < 4 && lane == 0) umma::bulk_wait0();  // stores complete before the CTA's shared memory goes
   umma::tc_fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(taddr, 128 * NBUF);
@@ -400,11 +397,12 @@ __global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__
   if (warp == 0) umma::tmem_dealloc(taddr, 128);
 }
 
-bool map3(CUtensorMap* m, const void* base, int inner, int M, int N, int box0, int box1, int box2) {
+bool map3(CUtensorMap* m, const void* base, int inner, int M, int N, int box0, int box1, int box2,
+          CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   const uint64_t dims[3] = {(uint64_t)inner, (uint64_t)M, (uint64_t)N};
   const uint64_t strides[2] = {(uint64_t)inner * 2, (uint64_t)inner * M * 2};
   const uint32_t box[3] = {(uint32_t)box0, (uint32_t)box1, (uint32_t)box2};
-  return make_map(m, base, 3, dims, strides, box);
+  return make_map(m, base, 3, dims, strides, box, sw);
 }
 bool map2(CUtensorMap* m, const void* base, int inner, int rows, int box0, int box1) {
   const uint64_t dims[2] = {(uint64_t)inner, (uint64_t)rows};
@@ -423,9 +421,13 @@ es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, vo
                              cudaStream_t st) {
   const int M = (a.L + 1) * (a.L + 1);
   CUtensorMap mh, mw;
-  if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64))
+  CUtensorMap mq, mk, mv;  // output boxes [32 rows][1 (l,m)][32 columns], 64-byte swizzle
+  if (!map3(&mh, h, a.C, M, a.N, 64, 1, 128) || !map2(&mw, W, 5 * a.C, (a.L + 1) * a.C, 64, 64) ||
+      !map3(&mq, q, 2 * a.C, M, a.N, 32, 1, 32, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mk, k, 2 * a.C, M, a.N, 32, 1, 32, CU_TENSOR_MAP_SWIZZLE_64B) ||
+      !map3(&mv, v, a.C, M, a.N, 32, 1, 32, CU_TENSOR_MAP_SWIZZLE_64B))
     return fail(ES_CUDA_ERROR, "proj_fwd_tc: tensor map encode failed");
-  const size_t smem = 32768 + NBUF * 32768 + 4 * 32 * 80 + 1024 + 1024;
+  const size_t smem = 32768 + NBUF * 32768 + 4 * 2048 + 1024 + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(proj_fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -433,7 +435,7 @@ es_status proj_fwd_tc_launch(const ProjArgs& a, const void* h, const void* W, vo
   }
   TcP p{a.N, M, a.C, a.L};
   dim3 grid(M, (a.N + 127) / 128);
-  proj_fwd_tc_kernel<<<grid, 160, smem, st>>>(mh, mw, p, (bf16*)q, (bf16*)k, (bf16*)v);
+  proj_fwd_tc_kernel<<<grid, 160, smem, st>>>(mh, mw, p, mq, mk, mv);
   return cuda_status(cudaGetLastError(), "proj_fwd_tc_kernel");
 }
 
