@@ -46,12 +46,15 @@ def main():
                 tot[e.name] = tot.get(e.name, 0.0) + e.device_time / 3
         return tot
 
+    var = os.environ.get("ABL_VAR", "ES_KV_DBG")  # ES_DQ_DBG: the dq / dk kernels' switches
     for d in [int(x) for x in (sys.argv[1:] or ["0", "1", "2", "4", "8", "16", "32", "63"])]:
-        os.environ["ES_KV_DBG"] = str(d)
+        os.environ[var] = str(d)
         tot = kv_us()
         kv = sum(v for k_, v in tot.items() if "attn_kv_tc" in k_)
-        print(f"dbg {d:2d}: kv {kv:8.1f} us", flush=True)
-    os.environ["ES_KV_DBG"] = "0"
+        dq = sum(v for k_, v in tot.items() if "attn_dqk_tc_kernel<false>" in k_)
+        dk = sum(v for k_, v in tot.items() if "attn_dqk_tc_kernel<true>" in k_)
+        print(f"dbg {d:2d}: kv {kv:8.1f} us  dq {dq:7.1f} us  dk {dk:7.1f} us", flush=True)
+    os.environ[var] = "0"
 
 
 if __name__ == "__main__":
