@@ -1168,7 +1168,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
 // TMA-staged K chunk read MN-major (the 64-byte-swizzled [16 keys][32 ch]
 // boxes of the forward's S MMA are exactly the MN-major SW64 atoms).
 namespace {
-constexpr int DQ_THREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2-5 rows + epilogue
+constexpr int DQ_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 rows (dscore tiles), warps 6-9 epilogue
 constexpr int DQ_ABYTES = TQ * KC * 2;  // 4096: [128 rows][16 keys] bf16, no-swizzle core matrices
 constexpr int DQ_SM_K = 0;
 constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA latency dominates
@@ -1275,8 +1275,53 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
         }
       }
     }
+  } else if (warp >= 6) {
+    // ================= epilogue: out[row][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..].  The
+    // accumulator is drained into registers (bf16, 144 per thread) and released at once; the global
+    // stores then overlap the next head's MMAs, which the row warps keep fed (the drain used to stall
+    // the whole pipeline once per head: ~a quarter of the kernel)
+    const int erow0 = q0 + (warp & 3) * 32;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    uint8_t* stg = sm + DQ_SM_STG + (warp - 6) * (32 * 80);
+    for (int h = 0; h < 8; ++h) {
+      umma::mbar_wait(acc_done, h & 1);
+      umma::tc_fence_after();
+      uint32_t pk[MM][16];  // [mm][32 channels as bf16 pairs]
+#pragma unroll
+      for (int mm = 0; mm < MM; ++mm) {
+        uint32_t r[32];
+        if (nch > 0 && !(dbg & 4)) umma::tmem_ld32(tmem + lane_base + 32 * mm, r);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const float x0 = nch > 0 ? tau * __uint_as_float(r[2 * t]) : 0.f;
+          const float x1 = nch > 0 ? tau * __uint_as_float(r[2 * t + 1]) : 0.f;
+          const __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
+          pk[mm][t] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+      }
+      umma::tc_fence_before();
+      umma::mbar_arrive(epi_done);
+      if (dbg & 4) continue;
+      // staged, coalesced stores: 4 lanes write one row's 64 bytes
+#pragma unroll
+      for (int mm = 0; mm < MM; ++mm) {
+        uint4* sw = reinterpret_cast<uint4*>(stg + lane * 80);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) sw[t] = make_uint4(pk[mm][4 * t], pk[mm][4 * t + 1], pk[mm][4 * t + 2], pk[mm][4 * t + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int it = 0; it < 4; ++it) {
+          const int rr = it * 8 + (lane >> 2), part = lane & 3;
+          const int qq = erow0 + rr;
+          if (qq < q1)
+            *reinterpret_cast<uint4*>(dq + ((size_t)qq * MM + mm) * 256 + DH * h + part * 8) =
+                *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
+        }
+        __syncwarp();
+      }
+    }
   } else {
-    // ================= rows: dscore tiles, epilogue
+    // ================= rows: dscore tiles
     const int row = ((warp & 3) << 5) | lane;
     const int qi = q0 + row;
     const bool qin = qi < q1;
@@ -1370,43 +1415,6 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
         umma::fence_proxy_async();
         umma::mbar_arrive(&a_full[b]);
       }
-      // epilogue: out[row][mm][32 h .. 32 h + 32] = tau * D[row][32 mm ..]
-      umma::mbar_wait(acc_done, h & 1);
-      umma::tc_fence_after();
-      // staged, coalesced stores: 4 lanes write one row's 64 bytes (a 32 x 32 TMA store per (l,m)
-      // row measured slower here: 0.85 -> 0.90 ms)
-      uint8_t* stg = sm + DQ_SM_STG + (warp - 2) * (32 * 80);
-#pragma unroll 1
-      for (int mm = 0; mm < ((dbg & 4) ? 0 : MM); ++mm) {
-        uint32_t r0[16], r1[16];
-        if (nch > 0) {
-          umma::tmem_ld16(tmem + lane_base + 32 * mm, r0);
-          umma::tmem_ld16(tmem + lane_base + 32 * mm + 16, r1);
-        }
-        float v[32];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          v[t] = nch > 0 ? tau * __uint_as_float(r0[t]) : 0.f;
-          v[16 + t] = nch > 0 ? tau * __uint_as_float(r1[t]) : 0.f;
-        }
-        uint4* sw = reinterpret_cast<uint4*>(stg + lane * 80);
-        sw[0] = pack8(v);
-        sw[1] = pack8(v + 8);
-        sw[2] = pack8(v + 16);
-        sw[3] = pack8(v + 24);
-        __syncwarp();
-#pragma unroll
-        for (int it = 0; it < 4; ++it) {
-          const int rr = it * 8 + (lane >> 2), part = lane & 3;
-          const int qq = q0 + (warp & 3) * 32 + rr;
-          if (qq < q1)
-            *reinterpret_cast<uint4*>(dq + ((size_t)qq * MM + mm) * 256 + DH * h + part * 8) =
-                *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
-        }
-        __syncwarp();
-      }
-      umma::tc_fence_before();
-      umma::mbar_arrive(epi_done);
     }
   }
   umma::tc_fence_before();
