@@ -1168,7 +1168,7 @@ es_status attn_fwd_tc_launch(const AttnArgs& a, const void* q, const void* k, co
 // TMA-staged K chunk read MN-major (the 64-byte-swizzled [16 keys][32 ch]
 // boxes of the forward's S MMA are exactly the MN-major SW64 atoms).
 namespace {
-constexpr int DQ_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2-5 rows (dscore tiles), warps 6-9 epilogue
+constexpr int DQ_THREADS = 448;  // warp 0 TMA, warp 1 MMA, warps 2-5 rows (dscore tiles), warps 6-13 epilogue
 constexpr int DQ_ABYTES = TQ * KC * 2;  // 4096: [128 rows][16 keys] bf16, no-swizzle core matrices
 constexpr int DQ_SM_K = 0;
 constexpr int DQ_NSTAGE = 8;  // deep K pipeline: per-chunk work is tiny, TMA latency dominates
@@ -1178,7 +1178,7 @@ constexpr int DQ_SM_DS = DQ_SM_A + DQ_NA * DQ_ABYTES;  // [2 heads][128 rows][64
 constexpr int DQ_KMAX = 64;
 constexpr int DQ_SM_OFF = DQ_SM_DS + 2 * TQ * DQ_KMAX * 4;  // [128 rows][64] i32: the rows' dscore gather offsets
 constexpr int DQ_SM_STG = DQ_SM_OFF + TQ * DQ_KMAX * 4;     // [4 warps][32 rows][80 B] epilogue staging
-constexpr int DQ_SM_BAR = DQ_SM_STG + 4 * 32 * 80;
+constexpr int DQ_SM_BAR = DQ_SM_STG + 8 * 32 * 80;  // 8 epilogue warps
 constexpr int DQ_SM_TOTAL = DQ_SM_BAR + 256;
 
 // KEYS = false: dq (rows = query rows, chunks = key chunks, B = K chunk, dscores
@@ -1200,7 +1200,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
   uint64_t* a_full = bars + 16;    // [DQ_NA] rows wrote the dscore tile (128)
   uint64_t* a_free = bars + 20;    // [DQ_NA] MMA done with the dscore tile
   uint64_t* acc_done = bars + 24;
-  uint64_t* epi_done = bars + 25;  // rows read the accumulator (128)
+  uint64_t* epi_done = bars + 25;  // epilogue warps read the accumulator (256)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 26);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = tstart[blockIdx.x], q1 = tstart[blockIdx.x + 1];
@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       umma::mbar_init(&a_free[b], 1);
     }
     umma::mbar_init(acc_done, 1);
-    umma::mbar_init(epi_done, 128);
+    umma::mbar_init(epi_done, 256);
     umma::fence_barrier_init();
   }
   if (warp == 0) umma::tmem_alloc(tslot, 512);
@@ -1280,23 +1280,26 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
     // accumulator is drained into registers (bf16, 144 per thread) and released at once; the global
     // stores then overlap the next head's MMAs, which the row warps keep fed (the drain used to stall
     // the whole pipeline once per head: ~a quarter of the kernel)
+    // two warps per TMEM lane quadrant: (l,m) rows [0, 5) and [5, 9) (80 / 64 registers held)
+    const int ehalf = (warp - 6) >> 2, m0 = ehalf ? 5 : 0, nm = ehalf ? MM - 5 : 5;
     const int erow0 = q0 + (warp & 3) * 32;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     uint8_t* stg = sm + DQ_SM_STG + (warp - 6) * (32 * 80);
     for (int h = 0; h < 8; ++h) {
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
-      uint32_t pk[MM][16];  // [mm][32 channels as bf16 pairs]
+      uint32_t pk[5][16];  // [mm - m0][32 channels as bf16 pairs]
 #pragma unroll
-      for (int mm = 0; mm < MM; ++mm) {
-        uint32_t r[32];
-        if (nch > 0 && !(dbg & 4)) umma::tmem_ld32(tmem + lane_base + 32 * mm, r);
+      for (int hb = 0; hb < 10; ++hb) {
+        if (hb >= 2 * nm) break;
+        uint32_t r[16];
+        if (nch > 0 && !(dbg & 4)) umma::tmem_ld16(tmem + lane_base + 32 * m0 + 16 * hb, r);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
+        for (int t = 0; t < 8; ++t) {
           const float x0 = nch > 0 ? tau * __uint_as_float(r[2 * t]) : 0.f;
           const float x1 = nch > 0 ? tau * __uint_as_float(r[2 * t + 1]) : 0.f;
           const __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-          pk[mm][t] = *reinterpret_cast<const uint32_t*>(&b2);
+          pk[hb >> 1][8 * (hb & 1) + t] = *reinterpret_cast<const uint32_t*>(&b2);
         }
       }
       umma::tc_fence_before();
@@ -1304,10 +1307,12 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       if (dbg & 4) continue;
       // staged, coalesced stores: 4 lanes write one row's 64 bytes
 #pragma unroll
-      for (int mm = 0; mm < MM; ++mm) {
+      for (int i = 0; i < 5; ++i) {
+        if (i >= nm) break;
+        const int mm = m0 + i;
         uint4* sw = reinterpret_cast<uint4*>(stg + lane * 80);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) sw[t] = make_uint4(pk[mm][4 * t], pk[mm][4 * t + 1], pk[mm][4 * t + 2], pk[mm][4 * t + 3]);
+        for (int t = 0; t < 4; ++t) sw[t] = make_uint4(pk[i][4 * t], pk[i][4 * t + 1], pk[i][4 * t + 2], pk[i][4 * t + 3]);
         __syncwarp();
 #pragma unroll
         for (int it = 0; it < 4; ++it) {
