@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_fwd_tc_kernel(
       umma::tc_fence_after();
       const float inv = zt > 0.f ? 1.f / zt : 0.f;
       if (qvalid && half == 0) lse[(size_t)qi * 8 + h] = zt > 0.f ? mu + __logf(zt) : -INFINITY;
-      const int cc0 = half ? 5 : 0, cc1 = half ? NV / 16 : 5;
+      const int cc0 = half ? 5 : 0, cc1 = (a.dbg & 32) ? cc0 : half ? NV / 16 : 5;  // 32: no epilogue (profiling)
       for (int cc = cc0; cc < cc1; ++cc) {
         uint32_t r[16];
         if (nch > 0) umma::tmem_ld16(t_out + lane_base + cc * 16, r);
@@ -2081,7 +2081,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_kv_tc_kernel(
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
       KV_TRACE(tid == 64, 11, 8 + h);
-      for (int cc = half ? 5 : 0; cc < (half ? MM : 5); ++cc) {
+      for (int cc = half ? 5 : 0; cc < ((a.dbg & 128) ? (half ? 5 : 0) : (half ? MM : 5)); ++cc) {  // 128: no epilogue
         uint32_t rr[16];
         umma::tmem_ld16(t_dv + lane_base + cc * 16, rr);
         float v[16];
