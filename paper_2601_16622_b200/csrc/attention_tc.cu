@@ -12,11 +12,13 @@
 // so both contractions run on the tensor cores:
 //   S  = Q_h K_h^T            M=128 queries, N=16 keys,  K=288   (TMA, 64B swizzle)
 //   O += Wt . Vg^T            M=128 queries, N=144 (o,c), K=144 (f,j)   (no-swizzle core matrices)
-// A CTA owns a tile of 128 consecutive query atoms; key chunks of 16 atoms
-// are the non-empty entries of the tile-skip mask.  Softmax in two passes
-// (statistics, then exact normalised P) so the TMEM accumulator never needs
-// rescaling.  Invalid (non-neighbour) pairs get Wt = 0; pair validity comes
-// from the neighbour index itself (never re-tested in fp32).
+// A CTA owns a tile of 128 query atoms (whole molecules packed, or 128
+// consecutive rows); key chunks of 16 atoms are the non-empty entries of the
+// tile-skip mask.  One-pass online softmax: the running maximum only moves the
+// exponent base when a chunk raises it by more than 5 (lazy rescale of the TMEM
+// accumulator, rarely taken), and the epilogue divides by the row sum.  Invalid
+// (non-neighbour) pairs get Wt = 0; pair validity comes from the neighbour
+// index itself (never re-tested in fp32).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
