@@ -1292,16 +1292,16 @@ __global__ void __launch_bounds__(DQ_THREADS, 1) attn_dqk_tc_kernel(
       umma::tc_fence_after();
       uint32_t pk[5][16];  // [mm - m0][32 channels as bf16 pairs]
 #pragma unroll
-      for (int hb = 0; hb < 10; ++hb) {
-        if (hb >= 2 * nm) break;
-        uint32_t r[16];
-        if (nch > 0 && !(dbg & 4)) umma::tmem_ld16(tmem + lane_base + 32 * m0 + 16 * hb, r);
+      for (int i = 0; i < 5; ++i) {  // one (l,m) row = 32 columns per TMEM load + wait
+        if (i >= nm) break;
+        uint32_t r[32];
+        if (nch > 0 && !(dbg & 4)) umma::tmem_ld32(tmem + lane_base + 32 * (m0 + i), r);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
+        for (int t = 0; t < 16; ++t) {
           const float x0 = nch > 0 ? tau * __uint_as_float(r[2 * t]) : 0.f;
           const float x1 = nch > 0 ? tau * __uint_as_float(r[2 * t + 1]) : 0.f;
           const __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-          pk[hb >> 1][8 * (hb & 1) + t] = *reinterpret_cast<const uint32_t*>(&b2);
+          pk[i][t] = *reinterpret_cast<const uint32_t*>(&b2);
         }
       }
       umma::tc_fence_before();
@@ -2083,7 +2083,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) attn_kv_tc_kernel(
       umma::mbar_wait(acc_done, h & 1);
       umma::tc_fence_after();
       KV_TRACE(tid == 64, 11, 8 + h);
-      for (int cc = half ? 5 : 0; cc < ((a.dbg & 128) ? (half ? 5 : 0) : (half ? MM : 5)); ++cc) {  // 128: no epilogue
+      for (int cc = half ? 5 : 0; cc < (half ? MM : 5); ++cc) {
         uint32_t rr[16];
         umma::tmem_ld16(t_dv + lane_base + cc * 16, rr);
         float v[16];
