@@ -54,3 +54,32 @@ def test_tensor_core_key_pass_matches_simt_at_size(n_mol, monkeypatch):
         assert torch.isfinite(a).all(), name
         err = float((a - r).abs().max() / r.abs().max())
         assert err < 2e-2, (name, err)
+
+
+def test_key_pass_unaligned_lse_takes_simt_pass():
+    """The tensor-core key pass bulk-copies lse rows in 16-byte units; an lse buffer that is only
+    4-byte aligned (a caller's sliced view) must take the SIMT key pass and give the same gradients."""
+    import paper_2601_16622_b200 as es
+    from paper_2601_16622_b200 import systems as S
+    from paper_2601_16622_b200.api import AttentionConfig, SavedAttention
+    b = S.molecule_batch(200, 40, 60, 12)
+    dev = torch.device("cuda")
+    pos = torch.tensor(b.pos, device=dev)
+    g = torch.Generator(device=dev).manual_seed(5)
+    h = torch.randn((b.n_atoms, 9, 128), device=dev, generator=g).bfloat16()
+    W = (torch.randn((3, 128, 640), device=dev, generator=g) / 128 ** 0.5).bfloat16()
+    idx = es.build_neighbors(pos, 64, 6.0, torch.tensor(b.seg_ptr, device=dev))
+    q, k, v = es.project_qk(h, W, 2)
+    cfg = AttentionConfig(heads=8, L=2)
+    out, lse = es.stream_aggregate(q, k, v, pos, idx, cfg)
+    dout = torch.randn(out.shape, device=dev, generator=g).bfloat16()
+    ref = es.stream_aggregate_backward(dout, SavedAttention(q, k, v, pos, idx, out, lse, cfg))
+    buf = torch.empty(lse.numel() + 1, dtype=lse.dtype, device=dev)
+    lse_odd = buf[1:].view_as(lse)
+    lse_odd.copy_(lse)
+    assert lse_odd.data_ptr() % 16 != 0
+    got = es.stream_aggregate_backward(dout, SavedAttention(q, k, v, pos, idx, out, lse_odd, cfg))
+    torch.cuda.synchronize()
+    for name, a_, r_ in zip(("dq", "dk", "dv"), got, ref):
+        err = float((a_.float() - r_.float()).abs().max() / r_.float().abs().max())
+        assert err < 2e-2, (name, err)
