@@ -8,6 +8,9 @@
 // where G = [dq | dk | dv] along o.  The rows of degree l are the (n, m)
 // pairs of the irreps layout -- a 3-D TMA box (C, M, N) picks them without
 // any host-side re-layout.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -313,7 +316,7 @@ __global__ void __launch_bounds__(128) proj_dh_tc_kernel(const __grid_constant__
 #endif
 constexpr int kDwStages = ES_DW_STAGES;
 #ifndef ES_DW_SPLITS
-#define ES_DW_SPLITS 60  // atom splits per degree (x 5 column blocks); 118 measured slower (more fp32 atomics)
+#define ES_DW_SPLITS 60  // fallback atom splits per degree (x 5 column blocks); the launcher uses 2 x SMs / 5
 #endif
 __global__ void __launch_bounds__(128) proj_dw_tc_kernel(const __grid_constant__ CUtensorMap mh,
                                                          const __grid_constant__ CUtensorMap mdq,
@@ -474,7 +477,22 @@ es_status proj_bwd_tc_launch(const ProjArgs& a, const void* h, const void* W, co
         !map3(&gk, dk, 2 * a.C, M, a.N, 64, 2 * l + 1, nb) || !map3(&gv, dv, a.C, M, a.N, 64, 2 * l + 1, nb))
       return fail(ES_CUDA_ERROR, "proj_dw_tc: tensor map encode failed");
     const size_t smem = (size_t)kDwStages * 4 * R * 128 + 1024 + 1024;
+    // atom splits: at most two resident CTAs per SM, all in one wave (5 column blocks each) -- 60 splits
+    // put 300 CTAs on 296 slots at l = 2 (a second, nearly empty wave: 0.59 -> 0.47 ms at 59); more
+    // CTAs per SM (l = 0, 1 fit 3-4) measured slower (smaller splits, more fp32 atomics).
+    // ES_DW_SPLITS overrides
     int splits = ES_DW_SPLITS;
+    {
+      static int nsm = 0;
+      if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      }
+      if (nsm > 0) splits = std::max(1, 2 * nsm / 5);  // two 82 KB CTAs per SM at l = 2
+      const char* e = getenv("ES_DW_SPLITS");
+      if (e && atoi(e) > 0) splits = atoi(e);
+    }
     int per = (a.N + splits - 1) / splits;
     per = ((per + nb - 1) / nb) * nb;
     splits = (a.N + per - 1) / per;
