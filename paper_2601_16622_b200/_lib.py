@@ -9,7 +9,9 @@ import ctypes as ct
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libequistream_b200.so")
+# ES_LIB_PATH: an experiment build of the same library (A/B variants built with
+# ES_NVCC_EXTRA into _variants/); the default is the in-tree build
+LIB_PATH = os.environ.get("ES_LIB_PATH") or os.path.join(HERE, "libequistream_b200.so")
 
 ES_OK, ES_INVALID_ARGUMENT, ES_UNSUPPORTED, ES_CUDA_ERROR, ES_NCCL_ERROR = range(5)
 ES_F32, ES_BF16 = 0, 1

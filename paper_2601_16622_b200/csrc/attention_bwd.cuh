@@ -54,9 +54,25 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 // DK = false: dk is left to the tensor-core dk pass (attn_dk_tc_kernel), so the
 // gathered q_i rows are needed only for the score -- and not at all when the
 // forward's scores are supplied (p.scores_in).
+// L >= 3 at C = 128 (configs[3]): 128-thread CTAs; the query rows of a pair
+// are re-read (L1) for the dk update instead of held across the EAAS adjoint
+// (2 M registers), and ES_L34_BWD_MINB CTAs reside per SM.
+#ifndef ES_L34_BWD_MINB
+#define ES_L34_BWD_MINB 2
+#endif
+#ifndef ES_L34_QRELOAD
+#define ES_L34_QRELOAD 1
+#endif
+template <int L, int CC>
+struct KvShape {
+  static constexpr bool BIG = L >= 3 && CC == 128;
+  static constexpr int THREADS = BIG ? 128 : (ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 : (L <= 2 ? 192 : 256));
+  static constexpr int MINB = BIG ? ES_L34_BWD_MINB : (ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? ES_BWD_MINB : (L <= 2 ? 2 : 1));
+  static constexpr bool QRELOAD = BIG && ES_L34_QRELOAD;
+};
+
 template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0, bool FORCE = false, bool DK = true>
-__global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 : (L <= 2 ? 192 : 256)),
-                                  (ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? ES_BWD_MINB : (L <= 2 ? 2 : 1)))
+__global__ void __launch_bounds__(KvShape<L, CC>::THREADS, KvShape<L, CC>::MINB)
     attn_bwd_kv_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                           const T* __restrict__ v, const double* __restrict__ pos,
                                                           const int* __restrict__ rev_ptr,
@@ -133,7 +149,8 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
       // packed FFMA2 forms only for even CPL: with CPL = 1 (L = 4) the
       // register pairing they impose costs spills
       constexpr bool PK = CPL % 2 == 0;
-      float qv[DK ? M : 1][2 * CPL];
+      constexpr bool QH = DK && !KvShape<L, CC>::QRELOAD;  // hold q_i in registers for the dk update
+      float qv[QH ? M : 1][2 * CPL];
       float score;
       if (!DK && p.scores_in) {
         score = p.scores_in[(size_t)head * p.N * p.K + __float_as_int(rec[LY::OFF_SI])];  // [H][N][K]
@@ -145,7 +162,7 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
         for (int mm = 0; mm < M; ++mm) {
           float qt[2 * CPL];
           ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qt);
-          if constexpr (DK) {
+          if constexpr (QH) {
 #pragma unroll
             for (int c = 0; c < 2 * CPL; ++c) qv[mm][c] = qt[c];
           }
@@ -304,11 +321,18 @@ __global__ void __launch_bounds__((ES_BWD_MINB > 0 && CC == 128 && L <= 2 ? 64 :
         const float tds = p.tau * ds;
 #pragma unroll
         for (int mm = 0; mm < M; ++mm) {
+          float qt[2 * CPL];
+          if constexpr (QH) {
+#pragma unroll
+            for (int c = 0; c < 2 * CPL; ++c) qt[c] = qv[mm][c];
+          } else {
+            ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qt);
+          }
           if constexpr (PK) {
-            fmac<2 * CPL>(tds, qv[mm], dkr[mm]);
+            fmac<2 * CPL>(tds, qt, dkr[mm]);
           } else {
 #pragma unroll
-            for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qv[mm][c], dkr[mm][c]);
+            for (int c = 0; c < 2 * CPL; ++c) dkr[mm][c] = fmaf(tds, qt[c], dkr[mm][c]);
           }
         }
       }

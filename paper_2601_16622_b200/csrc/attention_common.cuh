@@ -519,11 +519,85 @@ __device__ __forceinline__ void eaas_apply_scalar(const float* __restrict__ rec,
   }
 }
 
+// The same three EAAS steps ordered by target degree (L >= 3): the aligned
+// vector vt is built first, then for each target degree t its re-indexed block
+// w^t (at most 2L+1 rows instead of M) is formed and un-aligned into acc at
+// once, so vt, one w block and acc are live together (the M-row w of the
+// forms above is what spills at L = 4).  Each output element accumulates its
+// terms in the same order as eaas_apply_scalar: bit-identical results.
+template <int L, int CPL, bool ADJ>
+__device__ __forceinline__ void eaas_apply_blk(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
+                                               float (&acc)[Lay<L>::M][CPL]) {
+  constexpr int M = Lay<L>::M;
+  float vt[M][CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) vt[0][c] = v[0][c];
+#pragma unroll
+  for (int l = 1; l <= L; ++l) {
+    const float* D = rec + Lay<L>::doff(l);
+    const int d = 2 * l + 1;
+#pragma unroll
+    for (int m = 0; m < d; ++m) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) vt[l * l + m][c] = 0.f;
+#pragma unroll
+      for (int mp = 0; mp < d; ++mp) fmac<CPL>(D[m * d + mp], v[l * l + mp], vt[l * l + m]);
+    }
+  }
+#pragma unroll
+  for (int tl = 0; tl <= L; ++tl) {
+    float w[2 * L + 1][CPL];
+#pragma unroll
+    for (int t = 0; t < 2 * tl + 1; ++t)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) w[t][c] = 0.f;
+#pragma unroll
+    for (int sl = 0; sl <= L; ++sl) {
+      const int lo = ADJ ? sl : tl, li = ADJ ? tl : sl;
+      const int mm = cmin(lo, li);
+#pragma unroll
+      for (int m = -mm; m <= mm; ++m) {
+        const int e = Lay<L>::eoff(lo, li) + m + mm;
+        const float a = rec[Lay<L>::OFF_AB + 2 * e];
+        const float b = rec[Lay<L>::OFF_AB + 2 * e + 1];
+        fmac<CPL>(a, vt[sl * sl + sl + m], w[tl + m]);
+        if (m != 0) {
+          if constexpr (!ADJ) fmac<CPL>(b, vt[sl * sl + sl - m], w[tl + m]);
+          else fmac<CPL>(b, vt[sl * sl + sl + m], w[tl - m]);
+        }
+      }
+    }
+    if (tl == 0) {
+      fmac<CPL>(s, w[0], acc[0]);
+    } else {
+      const float* D = rec + Lay<L>::doff(tl);
+      const int d = 2 * tl + 1;
+#pragma unroll
+      for (int m = 0; m < d; ++m) {
+        float t[CPL];
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) t[c] = 0.f;
+#pragma unroll
+        for (int mp = 0; mp < d; ++mp) fmac<CPL>(D[mp * d + m], w[mp], t);
+        fmac<CPL>(s, t, acc[tl * tl + m]);
+      }
+    }
+  }
+}
+
+#ifndef ES_L34_BLK
+#define ES_L34_BLK 1
+#endif
+
 // x += s * (D^T P D) v  per channel (EAAS forward value operator), or the
 // adjoint y += s * (D^T P^T D) g when ADJ.  v: [M][CPL] registers.
 template <int L, int CPL, bool ADJ>
 __device__ __forceinline__ void eaas_apply(const float* __restrict__ rec, const float (&v)[Lay<L>::M][CPL], float s,
                                            float (&acc)[Lay<L>::M][CPL]) {
+  if constexpr (ES_L34_BLK && L >= 3) {
+    eaas_apply_blk<L, CPL, ADJ>(rec, v, s, acc);
+    return;
+  }
   if constexpr (CPL % 2 == 1) {
     eaas_apply_scalar<L, CPL, ADJ>(rec, v, s, acc);
     return;

@@ -9,8 +9,39 @@ namespace {
 // ------------------------------------------------------------------ forward
 // CC, HH > 0: channels / heads fixed at compile time (the BASELINE shape C=128,
 // H=8): row strides become immediates, no per-row 64-bit address arithmetic.
+// L >= 3 at C = 128 (the OMol25-like shape of configs[3]): one 128-thread CTA
+// per query atom, CPL = 1.  The query rows are staged in shared memory for the
+// score phase instead of 2 M registers per thread (50 at L = 4), which frees
+// the registers the value phase needs and lets ES_L34_FWD_MINB CTAs reside.
+#ifndef ES_L34_FWD_MINB
+#define ES_L34_FWD_MINB 2
+#endif
+#ifndef ES_L34_QSMEM
+#define ES_L34_QSMEM 1
+#endif
+// ES_L34_FWD_CPL = 2: two channels per thread (64-thread CTAs, packed FFMA2 in
+// the target-degree-ordered EAAS form, half the broadcast shared-memory loads
+// of the per-pair operator per FMA)
+// pairs per neighbour batch at L >= 3, C = 128: 16 (half of Lay<L>::BP) keeps the
+// records + staged q under a quarter of shared memory, so the register limit
+// (4 CTAs of 64 threads at 255 registers) and not shared memory bounds occupancy
+#ifndef ES_L34_FWD_BP
+#define ES_L34_FWD_BP 16
+#endif
+#ifndef ES_L34_FWD_CPL
+#define ES_L34_FWD_CPL 2
+#endif
+template <int L, int CC, int CPL>
+struct FwdShape {
+  static constexpr bool BIG = L >= 3 && CC == 128;
+  static constexpr bool QS = ES_L34_QSMEM && BIG;
+  static constexpr int THREADS = BIG ? 128 / CPL : 256;
+  static constexpr int MINB = BIG ? ES_L34_FWD_MINB * CPL : (L <= 2 ? 2 : 1);
+  static constexpr int BP = BIG ? ES_L34_FWD_BP : Lay<L>::BP;
+};
+
 template <int L, int CPL, bool EAAS, typename T, int CC = 0, int HH = 0>
-__global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
+__global__ void __launch_bounds__(FwdShape<L, CC, CPL>::THREADS, FwdShape<L, CC, CPL>::MINB) attn_fwd_kernel(KParams p, const T* __restrict__ q, const T* __restrict__ k,
                                                        const T* __restrict__ v, const double* __restrict__ pos,
                                                        const int* __restrict__ nbr, T* __restrict__ out,
                                                        float* __restrict__ lse) {
@@ -18,7 +49,7 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
   using LY = Lay<L>;
   constexpr int M = LY::M;
   constexpr int REC = LY::REC;
-  constexpr int BP = LY::BP;
+  constexpr int BP = FwdShape<L, CC, CPL>::BP;
   extern __shared__ float4 smem4[];
   __shared__ int cnt_w[32];
   float* recs = reinterpret_cast<float*>(smem4);
@@ -32,9 +63,26 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
   const int head = c0 / Ch;
   const int Dq = PDq;
 
-  float qr[M][2 * CPL];
+  constexpr bool QS = FwdShape<L, CC, CPL>::QS;
+  float qr[QS ? 1 : M][2 * CPL];
+  float* qs = sc + BP * PH;  // QS: [M][tpq][2 CPL] fp32 (conflict-free vector LDS)
+  if constexpr (QS) {
 #pragma unroll
-  for (int mm = 0; mm < M; ++mm) ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qr[mm]);
+    for (int mm = 0; mm < M; ++mm) {
+      float t[2 * CPL];
+      ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, t);
+#pragma unroll
+      for (int c = 0; c < 2 * CPL; ++c) qs[(mm * tpq + threadIdx.x) * 2 * CPL + c] = t[c];
+    }
+  } else {
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm) ldvec<2 * CPL>(q + ((size_t)i * M + mm) * Dq + 2 * c0, qr[mm]);
+  }
+  // this thread's query channels of row mm (registers, or the staged copy)
+  auto qrow = [&](int mm, int c) -> float {
+    if constexpr (QS) return qs[(mm * tpq + threadIdx.x) * 2 * CPL + c];
+    else return qr[mm][c];
+  };
   float A[M][CPL];
 #pragma unroll
   for (int mm = 0; mm < M; ++mm)
@@ -79,8 +127,9 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         ldvec<2 * CPL>(k + ((size_t)j1 * M + mm) * Dq + 2 * c0, k1);
 #pragma unroll
         for (int c = 0; c < 2 * CPL; ++c) {
-          s0 = fmaf(qr[mm][c], k0[c], s0);
-          s1 = fmaf(qr[mm][c], k1[c], s1);
+          const float qc = qrow(mm, c);
+          s0 = fmaf(qc, k0[c], s0);
+          s1 = fmaf(qc, k1[c], s1);
         }
       }
       for (int o = lph >> 1; o > 0; o >>= 1) {
@@ -100,7 +149,7 @@ __global__ void __launch_bounds__(256, (L <= 2 ? 2 : 1)) attn_fwd_kernel(KParams
         float kv[2 * CPL];
         ldvec<2 * CPL>(k + ((size_t)j * M + mm) * Dq + 2 * c0, kv);
 #pragma unroll
-        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qr[mm][c], kv[c], s);
+        for (int c = 0; c < 2 * CPL; ++c) s = fmaf(qrow(mm, c), kv[c], s);
       }
       for (int o = lph >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if ((lane % lph) == 0) sc[e * PH + head] = fmaf(s, p.tau, recs[e * REC + LY::OFF_B]);
@@ -160,9 +209,11 @@ template <int L, int CPL, bool EAAS, typename T>
 es_status run_fwd(const KParams& kp, const void* q, const void* k, const void* v, const double* pos,
                   const int32_t* nbr, void* out, float* lse, cudaStream_t st) {
   const int tpq = kp.C / CPL;
-  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)Lay<L>::BP * kp.H * 4;
-  auto fn = (kp.C == 128 && kp.H == 8) ? attn_fwd_kernel<L, CPL, EAAS, T, 128, 8>
-                                                               : attn_fwd_kernel<L, CPL, EAAS, T>;
+  const bool fixed = kp.C == 128 && kp.H == 8;
+  const int bp = fixed ? FwdShape<L, 128, CPL>::BP : Lay<L>::BP;
+  size_t smem = (size_t)bp * Lay<L>::REC * 4 + (size_t)bp * kp.H * 4;
+  if (fixed && FwdShape<L, 128, CPL>::QS) smem += (size_t)Lay<L>::M * tpq * 2 * CPL * 4;
+  auto fn = fixed ? attn_fwd_kernel<L, CPL, EAAS, T, 128, 8> : attn_fwd_kernel<L, CPL, EAAS, T>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   fn<<<kp.N, tpq, smem, st>>>(kp, (const T*)q, (const T*)k, (const T*)v, pos, nbr, (T*)out, lse);
   return cuda_status(cudaGetLastError(), "attn_fwd_kernel");
@@ -184,13 +235,17 @@ template <template <int, int, bool, typename> class Op, typename... Args>
 es_status dispatch(const AttnArgs& a, Args&&... args) {
   const bool eaas = a.value_mode == ES_VALUE_EAAS;
   const bool bf = a.dtype == ES_BF16;
-  const int cpl = (a.L <= 2 && a.C % 64 == 0 && (a.C / a.H) % 2 == 0) ? 2 : 1;
+  const int cpl = (a.L <= 2 && a.C % 64 == 0 && (a.C / a.H) % 2 == 0) ? 2
+                  : (a.L >= 3 && a.C == 128 && a.H == 8) ? ES_L34_FWD_CPL : 1;
 #define ES_CASE(LL, CC)                                                                                  \
   if (a.L == LL && cpl == CC) {                                                                          \
     if (eaas) return bf ? Op<LL, CC, true, __nv_bfloat16>::run(args...) : Op<LL, CC, true, float>::run(args...); \
     return bf ? Op<LL, CC, false, __nv_bfloat16>::run(args...) : Op<LL, CC, false, float>::run(args...);        \
   }
   ES_CASE(0, 2) ES_CASE(1, 2) ES_CASE(2, 2) ES_CASE(0, 1) ES_CASE(1, 1) ES_CASE(2, 1) ES_CASE(3, 1) ES_CASE(4, 1)
+#if ES_L34_FWD_CPL == 2
+  ES_CASE(3, 2) ES_CASE(4, 2)
+#endif
 #undef ES_CASE
   return fail(ES_UNSUPPORTED, "attention: no kernel for this (L, C, H)");
 }

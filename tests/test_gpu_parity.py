@@ -175,7 +175,7 @@ def _run_attn(es, pos, nbr, q, k, v, L, H, vm, dtype, box=None, dout=None, seg=N
 
 ATTN_CASES = [  # (L, C, H, N, K)
     (0, 64, 8, 64, 64), (1, 64, 8, 80, 64), (2, 64, 8, 64, 64), (2, 128, 8, 150, 64), (2, 32, 4, 90, 32),
-    (3, 64, 4, 70, 64), (4, 128, 8, 60, 64), (2, 256, 8, 40, 64),
+    (3, 64, 4, 70, 64), (3, 128, 8, 50, 64), (4, 128, 8, 60, 64), (2, 256, 8, 40, 64),
 ]
 
 
