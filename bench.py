@@ -242,6 +242,8 @@ class Workload:
         else:
             self.sys = systems.config_system(cfgno, seed, n_atoms=args.atoms)
         self.box = None if self.sys.box is None else tuple(float(b) for b in self.sys.box)
+        # scores are recomputed in the backward at every L (keeping them was measured slower at L = 4:
+        # key pass 17.1 -> 19.6 ms, profiles/r02e_l4_variants.jsonl)
         self.cfg = AttentionConfig(heads=self.H, L=self.L, r_cut=RCUT, value_mode="eaas", box=self.box)
         N = self.sys.n_atoms
         self.N = N

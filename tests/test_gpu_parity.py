@@ -200,6 +200,43 @@ def test_attention_fwd_bwd_fp32(es, oracle, vm, L, C, H, N, K):
     assert rel(dv.cpu(), rdv) < F32_TOL
 
 
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, F32_TOL), (torch.bfloat16, BF16_TOL)])
+@pytest.mark.parametrize("L", [3, 4])
+def test_kept_scores_backward_l34(es, oracle, L, dtype, tol):
+    """L >= 3, C = 128 (configs[3]): the forward keeps its [H][N][K] scores and the
+    key pass reads them instead of recomputing Q.K (dk re-reads q_i); gradients
+    match the oracle and the recomputing backward."""
+    from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
+    C, H, K = 128, 8, 64
+    pos, nbr, q, k, v, _ = _attn_inputs(60, L, C, H, K, seed=40 + L)
+    nbr[5] = -1
+    nbr[9, 2:] = -1
+    if dtype == torch.bfloat16:
+        q, k, v = (torch.tensor(x).bfloat16().double().numpy() for x in (q, k, v))
+    P = po.AttnProblem(L=L, H=H, value_mode=po.VALUE_DENSE)
+    rout, rlse = po.attn_fwd(P, q, k, v, pos, nbr)
+    dout = np.random.default_rng(8).standard_normal(rout.shape)
+    if dtype == torch.bfloat16:
+        dout = torch.tensor(dout).bfloat16().double().numpy()
+    rdq, rdk, rdv = po.attn_bwd(P, q, k, v, pos, nbr, rout, rlse, dout)
+    idx = NeighborIndex(dev(nbr), None, None, 6.0)
+    tq, tk, tv, tp = dev(q, dtype), dev(k, dtype), dev(v, dtype), dev(pos)
+    got = []
+    for keep in (True, False):
+        cfg = AttentionConfig(heads=H, L=L, r_cut=6.0, value_mode="eaas", keep_scores=keep)
+        res = es.stream_aggregate(tq, tk, tv, tp, idx, cfg, return_scores=keep)
+        out, lse, scores = res if keep else (*res, None)
+        g = es.stream_aggregate_backward(dev(dout, dtype), SavedAttention(tq, tk, tv, tp, idx, out, lse, cfg,
+                                                                          scores=scores))
+        torch.cuda.synchronize()
+        assert rel(out.float().cpu(), rout) < tol
+        for a, b in zip(g, (rdq, rdk, rdv)):
+            assert rel(a.float().cpu(), b) < tol
+        got.append([x.float().cpu() for x in g])
+    for a, b in zip(*got):
+        assert rel(a, b.double().numpy()) < (1e-5 if dtype == torch.float32 else 1e-2)
+
+
 @pytest.mark.parametrize("L,C,H,N,K", [(2, 128, 8, 120, 64), (4, 128, 8, 50, 64), (1, 64, 4, 80, 32)])
 def test_attention_bf16(es, oracle, L, C, H, N, K):
     pos, nbr, q, k, v, _ = _attn_inputs(N, L, C, H, K, seed=11)
