@@ -105,8 +105,6 @@ __global__ void __launch_bounds__(KvShape<L, CC>::THREADS, KvShape<L, CC>::MINB)
   const int nthr = blockDim.x;
   float* ks = recs + BP * REC;
   float* vs = ks + M * nthr * 2 * CPL;
-  float* kept = vs + M * nthr * CPL;  // [BP][H] the batch's kept scores (gathered by the preparing threads)
-  constexpr bool KEPT_OK = !DK || KvShape<L, CC>::QRELOAD;  // see the score below
   {
     const T* kj = k + (size_t)j * M * Dq + 2 * c0;
     const T* vj = v + (size_t)j * M * PC + c0;
@@ -141,12 +139,7 @@ __global__ void __launch_bounds__(KvShape<L, CC>::THREADS, KvShape<L, CC>::MINB)
       pair_prepare<L, EAAS>(p, pos, i, j, rec);
       rec[LY::OFF_J] = __int_as_float(i);
       rec[LY::OFF_X] = __int_as_float(pr);
-      if (p.scores_in) {
-        const int si = p.rank_of ? i * p.K + __ldg(p.rank_of + pr) : pr;
-        rec[LY::OFF_SI] = __int_as_float(si);
-        if (KEPT_OK)
-          for (int h = 0; h < PH; ++h) kept[t * PH + h] = p.scores_in[(size_t)h * p.N * p.K + si];
-      }
+      if (p.scores_in) rec[LY::OFF_SI] = __int_as_float(p.rank_of ? i * p.K + __ldg(p.rank_of + pr) : pr);
     }
     __syncthreads();
     for (int e = 0; e < nb; ++e) {
@@ -159,10 +152,8 @@ __global__ void __launch_bounds__(KvShape<L, CC>::THREADS, KvShape<L, CC>::MINB)
       constexpr bool QH = DK && !KvShape<L, CC>::QRELOAD;  // hold q_i in registers for the dk update
       float qv[QH ? M : 1][2 * CPL];
       float score;
-      // the forward's kept scores replace the recompute whenever q_i is not needed
-      // in registers afterwards (no dk here, or dk re-reads q_i: L >= 3)
-      if (KEPT_OK && p.scores_in) {
-        score = kept[e * PH + head];  // [H][N][K] gathered at preparation
+      if (!DK && p.scores_in) {
+        score = p.scores_in[(size_t)head * p.N * p.K + __float_as_int(rec[LY::OFF_SI])];  // [H][N][K]
       } else {
         float sc[2 * CPL];
 #pragma unroll
@@ -459,8 +450,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
   es_status s = cuda_status(cudaGetLastError(), "attn_delta_kernel");
   if (s != ES_OK) return s;
   const int threads = kp.C / CPL;
-  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)M * threads * 3 * CPL * 4 +
-                      (size_t)Lay<L>::BP * kp.H * 4;
+  const size_t smem = (size_t)Lay<L>::BP * Lay<L>::REC * 4 + (size_t)M * threads * 3 * CPL * 4;
   auto fn = (kp.C == 128 && kp.H == 8) ? attn_bwd_kv_kernel<L, CPL, EAAS, T, 128, 8>
                                                                : attn_bwd_kv_kernel<L, CPL, EAAS, T>;
   if (dpos) {  // position gradients (forces), every L

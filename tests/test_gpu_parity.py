@@ -203,9 +203,10 @@ def test_attention_fwd_bwd_fp32(es, oracle, vm, L, C, H, N, K):
 @pytest.mark.parametrize("dtype,tol", [(torch.float32, F32_TOL), (torch.bfloat16, BF16_TOL)])
 @pytest.mark.parametrize("L", [3, 4])
 def test_kept_scores_backward_l34(es, oracle, L, dtype, tol):
-    """L >= 3, C = 128 (configs[3]): the forward keeps its [H][N][K] scores and the
-    key pass reads them instead of recomputing Q.K (dk re-reads q_i); gradients
-    match the oracle and the recomputing backward."""
+    """L >= 3, C = 128 (configs[3]) with keep_scores: the forward also writes its
+    [H][N][K] scores; the SIMT key pass (dk inside it) recomputes Q.K regardless
+    (reading the kept scores was measured slower at L = 4).  Gradients match the
+    oracle and the backward without kept scores."""
     from paper_2601_16622_b200.api import AttentionConfig, NeighborIndex, SavedAttention
     C, H, K = 128, 8, 64
     pos, nbr, q, k, v, _ = _attn_inputs(60, L, C, H, K, seed=40 + L)
