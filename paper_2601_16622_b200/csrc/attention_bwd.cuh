@@ -60,9 +60,6 @@ __global__ void __launch_bounds__(256) attn_delta_kernel(int N, int M, int C, in
 #ifndef ES_L34_BWD_MINB
 #define ES_L34_BWD_MINB 2
 #endif
-#ifndef ES_L34_DQ_UNR8
-#define ES_L34_DQ_UNR8 1
-#endif
 #ifndef ES_L34_QRELOAD
 #define ES_L34_QRELOAD 1
 #endif
@@ -361,9 +358,10 @@ __global__ void __launch_bounds__(KvShape<L, CC>::THREADS, KvShape<L, CC>::MINB)
 // compacts the valid slots of row i (ballot over the row, so any sentinel
 // pattern works) and their per-head dscore rows into shared memory; the
 // gather loop then runs over valid pairs only, UNR k_j rows in flight.
-// UNR k rows in flight per thread: 8 at L >= 3 (the 12.8 KB k rows of an L = 4
-// pair make this an L2 gather), 4 otherwise
-template <typename T, int UNR = 4>
+// UNR k rows in flight per thread: the pass is an L2 gather of k rows (12.8 KB
+// per pair at L = 4); 8 in flight instead of 4 took dq from 4.73 to 3.91 ms on
+// configs[3], 1.81 to 1.62 ms on the 100k box, 0.32 to 0.30 ms at 20k atoms
+template <typename T, int UNR = 8>
 __global__ void __launch_bounds__(1024) attn_bwd_q_kernel(int M, int K, int H, int Dq, float tau,
                                                           const T* __restrict__ k, const int* __restrict__ nbr,
                                                           const float* __restrict__ dsbuf, T* __restrict__ dq) {
@@ -484,7 +482,7 @@ es_status run_bwd(const KParams& kp, const void* q, const void* k, const void* v
     if (tq > 1024) return fail(ES_UNSUPPORTED, "attn_bwd: K > 1024");
     const size_t qsm = (size_t)kp.K * (1 + kp.H) * 4;
     if (qsm > 200 * 1024) return fail(ES_UNSUPPORTED, "attn_bwd: K * (H + 1) too large for the dq pass");
-    auto qfn = (L >= 3 && ES_L34_DQ_UNR8) ? attn_bwd_q_kernel<T, 8> : attn_bwd_q_kernel<T, 4>;
+    auto qfn = attn_bwd_q_kernel<T>;
     if (qsm > 48 * 1024) cudaFuncSetAttribute(qfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
     qfn<<<kp.N, tq, qsm, st>>>(M, kp.K, kp.H, kp.Dq, kp.tau, (const T*)k, nbr, dsbuf, (T*)dq);
   }
